@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the synchronous lazy-PCA sweep (arXiv 2507.14869) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--sweeps S] [--impl ours|reference]
+
+Metric (BASELINE.json): PCA site-updates per second (SU/s = sites x sweeps / time).
+
+One *step* = one pass of the whole hot path over one batch of
+synthetic input: pca_reset (x0 = g, counts = 0, t = 0), S synchronous sweeps with fused MPM
+counts, the MPM estimate, and PSNR/SSIM of the LAST and MPM estimates against the truth.
+
+* N = 1: config 3 -- 8192 x 8192 single lattice, l = 2, Moore-8 torus, sigma = 0.5,
+  fixed beta = 1.5 (steady-state timing), q = 0.51, MPM counting every sweep.
+* N > 1 (torchrun, one process per GPU, NCCL): config 4 weak scaling -- a 32768-wide torus
+  of 4096*N rows, row strips of 4096 x 32768 per GPU with a one-row halo exchange per
+  sweep over NCCL (P = 8 is exactly 32768^2).
+
+`value` is device-timed (CUDA events on the library's stream, inputs resident in HBM);
+`e2e` repeats the step through the same C ABI with pinned HOST buffers (g and truth
+host->device, MPM image device->host inside the timed region).  `--impl reference` times
+the CPU oracle (oracle/, one core) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCA site-updates/sec"
+UNIT = "site-updates/s"
+BYTES_PER_SU = 7  # x_t read (1) + g read (1) + x_{t+1} write (1) + uint16 count RMW (2+2)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--sweeps", type=int, default=100, help="PCA sweeps per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rows-per-thread", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload(n_gpus: int):
+    if n_gpus == 1:
+        return dict(name="config3: 8192x8192 single lattice on 1 B200, l=2, Moore-8 torus, "
+                         "sigma=0.5, beta=1.5 fixed, q=0.51, MPM counts every sweep",
+                    H=8192, W=8192, rows=8192, levels=2, nbhd=8, periodic=True, sigma=0.5,
+                    beta=1.5, parallelism="1 GPU")
+    return dict(name=f"config4 weak scaling: {4096 * n_gpus}x32768 torus (32768 wide), row strips "
+                     f"4096x32768 per GPU, NCCL halo exchange per sweep, l=2, Moore-8, sigma=0.5, "
+                     f"beta=1.5, q=0.51, MPM every sweep",
+                H=4096 * n_gpus, W=32768, rows=4096, levels=2, nbhd=8, periodic=True, sigma=0.5,
+                beta=1.5, parallelism=f"row-strip x{n_gpus}")
+
+
+def make_inputs(wl, rank):
+    import synth
+
+    rows, W = wl["rows"], wl["W"]
+    truth = synth.tiled_labels(rows, W, wl["levels"], seed=1000 + rank)
+    g = synth.degrade(truth, wl["levels"], wl["sigma"], seed=2000 + rank)
+    return truth, g
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_traffic():
+    """dram bytes per sweep launch from the committed ncu --set full summary, if any."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary*.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+            if d.get("workload_H") == 8192 and d.get("dram_bytes_per_launch"):
+                return float(d["dram_bytes_per_launch"]), os.path.relpath(f, ROOT)
+        except Exception:
+            pass
+    return None, None
+
+
+def measured_peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline_oracle(wl, truth, g, rows=None, sweeps=2):
+    """The oracle, as it stands (single-threaded C, fp64), on a bounded sample of the
+    workload: `sweeps` sweeps of the first `rows` rows treated as their own torus."""
+    import oracle as orc
+
+    rows = rows or wl["rows"]
+    m = orc.model(rows, wl["W"], wl["levels"], nbhd=wl["nbhd"], periodic=wl["periodic"],
+                  sigma=wl["sigma"], q=0.51)
+    gs = np.ascontiguousarray(g[:rows])
+    t0 = time.perf_counter()
+    x, cnt = orc.pca_run(m, gs, gs, sweeps, wl["beta"], 0.0, 1 << 30, 11, burn_in=0)
+    orc.metrics(np.ascontiguousarray(truth[:rows]), x, wl["levels"])
+    dt = time.perf_counter() - t0
+    su = rows * wl["W"] * sweeps
+    return {"value": su / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{sweeps} oracle sweeps (+MPM counts, +metrics) of a {rows}x{wl['W']} "
+                      f"torus cut from the same input, 1 thread, {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = workload(args.gpus)
+    truth, g = make_inputs(wl, 0)
+    rows = 512
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline_oracle(wl, truth, g, rows=rows, sweeps=1)
+        if i >= args.warmup:
+            times.append(r)
+    vals = [r["value"] for r in times]
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * rows * wl["W"] / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": wl["name"], "H": wl["H"], "W": wl["W"],
+                                        "reference_sample_rows": rows, "sweeps_per_step": 1},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"each step: 1 oracle sweep (+MPM, +metrics) of a {rows}x"
+                                   f"{wl['W']} torus cut from the workload, 1 thread"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2507_14869_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = max(args.gpus, world)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    wl = workload(n)
+    truth, g = make_inputs(wl, rank)
+    rows, W = wl["rows"], wl["W"]
+    cfg = P.make_config(wl["H"], W, wl["levels"], neighborhood=wl["nbhd"], periodic=wl["periodic"],
+                        sigma=wl["sigma"], q=0.51, beta0=wl["beta"], beta_step=0.0,
+                        beta_period=1 << 30, seed=11, mpm_burn_in=0, row0=rank * rows,
+                        rows=rows if world > 1 else 0, rows_per_thread=args.rows_per_thread)
+    stream = torch.cuda.Stream(device=dev)
+    g_dev = torch.from_numpy(g).to(dev).reshape(1, rows, W).contiguous()
+    t_dev = torch.from_numpy(truth).to(dev).reshape(1, rows, W).contiguous()
+    mpm_dev = torch.empty_like(g_dev)
+    ctx = P.PcaContext(cfg, g_dev, stream=stream)
+    if world > 1:
+        uid = [P.pca_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.pca_attach_nccl(uid[0], world, rank)
+    S = args.sweeps
+
+    def step_device():
+        ctx.pca_reset(None, None)
+        ctx.pca_sweep(S)
+        ctx.pca_estimate(P.EST_MPM, mpm_dev)
+        ctx.pca_psnr_ssim(t_dev, P.EST_LAST)
+        return ctx.pca_psnr_ssim(t_dev, P.EST_MPM)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-timed run ----
+    for _ in range(args.warmup):
+        step_device()
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    st0 = ctx.pca_get_stats()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sw_ms = 0.0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ctx.pca_reset(None, None)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.pca_sweep(S)
+        b.record(stream)
+        ctx.pca_estimate(P.EST_MPM, mpm_dev)  # synchronises the stream
+        sw_ms += a.elapsed_time(b)
+        ctx.pca_psnr_ssim(t_dev, P.EST_LAST)
+        psnr, ssim = ctx.pca_psnr_ssim(t_dev, P.EST_MPM)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    st1 = ctx.pca_get_stats()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    sw_ms = max_over_ranks(sw_ms)
+    sites_all = wl["H"] * W
+    value = sites_all * S * args.steps / (ms * 1e-3)
+    launches = int(st1.kernel_launches - st0.kernel_launches)
+
+    # roofline of the dominant kernel (the fused sweep): algorithmic bytes / mean duration
+    sweep_s = sw_ms * 1e-3 / (S * args.steps)
+    alg_bytes = BYTES_PER_SU * rows * W
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / sweep_s / 1e9
+    traffic, traffic_src = load_traffic()
+
+    # ---- end-to-end through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        g_h = torch.from_numpy(g).reshape(1, rows, W).pin_memory()
+        t_h = torch.from_numpy(truth).reshape(1, rows, W).pin_memory()
+        mpm_h = torch.empty((1, rows, W), dtype=torch.uint8).pin_memory()
+
+        def step_e2e():
+            ctx.pca_reset(g_h, None)           # H2D of g inside the step
+            ctx.pca_sweep(S)
+            ctx.pca_estimate(P.EST_MPM, mpm_h)  # D2H of the MPM image
+            ctx.pca_psnr_ssim(t_h, P.EST_LAST)  # H2D of the truth
+            return ctx.pca_psnr_ssim(t_h, P.EST_MPM)
+
+        for _ in range(max(1, args.warmup)):
+            step_e2e()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        e1.record(stream)
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": sites_all * S * args.steps / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(g_h.numel() + 2 * t_h.numel()),
+               "d2h_bytes_per_step": int(mpm_h.numel() + 2 * 8 * 8),
+               "ms_per_step": ems / args.steps}
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_oracle(wl, truth, g, rows=wl["rows"], sweeps=2)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl["name"], "H": wl["H"], "W": W, "rows_per_gpu": rows,
+                       "levels": wl["levels"], "sweeps_per_step": S,
+                       "step": "reset + S fused sweeps (MPM on) + MPM estimate + PSNR/SSIM x2",
+                       "l2": "working set ~320 MiB/GPU > 126 MB L2: inputs larger than L2, no flush",
+                       "parallelism": wl["parallelism"],
+                       "psnr_ssim_mpm": [float(psnr[0]), float(ssim[0])]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "sweep_binary_kernel (fused PCA sweep + MPM counts)",
+                         "bytes_per_launch_alg": alg_bytes,
+                         "alg_bytes_per_site_update": BYTES_PER_SU,
+                         "mean_launch_us": sweep_s * 1e6, "peak_source": peak_src,
+                         "traffic_source": traffic_src},
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.pca_destroy()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

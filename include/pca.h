@@ -1,0 +1,212 @@
+/*
+ * include/pca.h -- C ABI of the B200-native synchronous lazy-PCA sweep library
+ * (libpca_b200.so), arXiv 2507.14869.  SURVEY.md section 8(b) is the contract.
+ *
+ * The library samples the lazy Probabilistic Cellular Automaton of PAPER.md section 5.2
+ * (transition display PAPER.md:462-477): at every sweep t each site i
+ * of the lattice independently draws its new gray level w_i with probability
+ *     p_i(s; x) ∝ exp( a*n_i(s;x) - b*(lum g_i - lum s)^2 - c*1{s != x_i} ),
+ *     a = coef_scale*2*beta_t*J,  b = coef_scale/(2 sigma^2),  c = beta_t*q,
+ *     beta_t = beta0 + beta_step*floor(t/beta_period),
+ * from the PREVIOUS configuration x (double buffering), where n_i(s;x) is
+ * the number of neighbours (Moore-8, or von Neumann-4) carrying s and
+ * lum(k) = k/(levels-1).  DESIGN.md section 3 lists the readings
+ * (R1..R20) taken where the paper is ambiguous.  Running per-site label counts give the
+ * posterior-marginal (MPM) estimate; PSNR and global SSIM are
+ * reduced on the device.
+ *
+ * Random numbers: Philox4x32-10 keyed by (seed mod 2^32, seed >> 32) with counter
+ * (col>>2, row, t, 1<<24 | chain), word col&3, u = r*2^-32, so a
+ * chain is a pure function of (config, g, x0, number of sweeps): independent of GPU
+ * count, row split, batch composition and launch configuration.
+ *
+ * Layout of every image argument: dense, row-major uint8 level indices
+ * [batch][rows][width] (chain-major), values in [0, levels).  Count arrays are uint16,
+ * planar: levels == 2 -> [batch][rows][width] (count of label 1); levels > 2 ->
+ * [batch][levels][rows][width].
+ *
+ * Pointers: every image/count pointer may be HOST memory (pageable or pinned) or DEVICE
+ * memory of the context's device; the library detects which (CUDA UVA) and copies
+ * accordingly.  Device memory is never allocated by the library: the caller owns one
+ * workspace buffer of pca_workspace_bytes() bytes, which must outlive the context.
+ *
+ * Streams: all device work is enqueued on the caller's stream given to pca_init.
+ * pca_sweep is asynchronous; every call that returns data (estimate, read_*, psnr_ssim,
+ * metric_sums, get_stats) synchronises that stream before returning.
+ *
+ * Errors: every call returns a pca_status and never aborts or throws across the ABI.
+ * Arguments are validated before any device work.  Asynchronous CUDA/NCCL errors
+ * surface at the next synchronising call as PCA_ECUDA / PCA_ENCCL; after any CUDA/NCCL
+ * error the context is poisoned and every call except pca_destroy returns PCA_ESTATE.
+ * pca_last_error() returns a thread-local message for the most recent failure.
+ */
+#ifndef PCA_B200_H
+#define PCA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCA_ABI_VERSION 1
+
+typedef struct pca_ctx pca_ctx; /* opaque; one per GPU per lattice strip / chain batch */
+
+typedef enum {
+    PCA_OK = 0,
+    PCA_EINVAL = -1,        /* invalid argument or configuration                       */
+    PCA_ESTATE = -2,        /* context poisoned by an earlier CUDA/NCCL error          */
+    PCA_ECUDA = -3,         /* CUDA runtime error                                      */
+    PCA_ENCCL = -4,         /* NCCL error (or NCCL library not loadable)               */
+    PCA_ENOSPACE = -5,      /* workspace smaller than pca_workspace_bytes()            */
+    PCA_EUNSUPPORTED = -6   /* valid but unsupported (see pca_last_error)             */
+} pca_status;
+
+enum { PCA_NBHD_VN4 = 4, PCA_NBHD_MOORE8 = 8 };
+
+/* Estimate kinds for pca_estimate / pca_psnr_ssim / pca_metric_sums. */
+enum {
+    PCA_EST_LAST = 0,      /* the current sample x_t ("last sample")           */
+    PCA_EST_MPM = 1,       /* argmax_k count_k, ties to the lowest label (R15)               */
+    PCA_EST_MARGINALS = 2, /* float32 [batch][levels][rows][width] = count_k / N_samp      */
+    PCA_EST_CM = 3         /* float32 [batch][rows][width] = sum_k lum(k) count_k / N_samp  */
+};
+
+/* Kernel selection (all give the same chain up to fp64 near-ties). */
+enum {
+    PCA_KERNEL_AUTO = 0,    /* binary fast path when levels == 2, else general        */
+    PCA_KERNEL_GENERAL = 1, /* fp64 per-site weights, any levels                      */
+    PCA_KERNEL_BINARY = 2   /* levels == 2: SWAR neighbour counts + integer thresholds */
+};
+
+typedef struct pca_config {
+    int32_t height;        /* H: global rows of one chain's lattice (>= 1; >= 3 if periodic)  */
+    int32_t width;         /* W: columns (>= 1; >= 3 if periodic)                             */
+    int32_t batch;         /* number of independent chains in this context (>= 1)             */
+    int32_t levels;        /* l gray levels, 2..255                            */
+    int32_t neighborhood;  /* PCA_NBHD_MOORE8 (paper) or PCA_NBHD_VN4                         */
+    int32_t periodic;      /* 0 = free boundary, 1 = torus                     */
+    double J;              /* prior coupling > 0 (1/3 in PAPER.md:500)       */
+    double q;              /* inertia >= 0 (0.51 in PAPER.md:508)               */
+    double sigma;          /* noise std in luminance units > 0                 */
+    double beta0;          /* beta at t = 0, > 0 (1.25)                          */
+    double beta_step;      /* beta increment >= 0 (0.25)                         */
+    int32_t beta_period;   /* sweeps per beta stage > 0 (250)                    */
+    int32_t chain0;        /* chain id of this context's first chain (RNG counter), >= 0      */
+    double coef_scale;     /* > 0; 1.0 = paper-literal a, b; 0.5 = matched mode (R4)           */
+    uint64_t seed;         /* Philox key                                                       */
+    int32_t mpm_burn_in;   /* count x_{t+1} for sweeps t >= burn_in; < 0 disables counts       */
+    int32_t row0;          /* first global row owned by this context (sharding), >= 0         */
+    int32_t rows;          /* owned rows; 0 means all H rows (row0 must then be 0)            */
+    int32_t kernel;        /* PCA_KERNEL_*                                                     */
+    int32_t rows_per_thread; /* binary kernel register-blocking depth; 0 = library default    */
+    int32_t reserved[7];   /* must be zero                                                     */
+} pca_config;
+
+typedef struct pca_stats {
+    int64_t sweeps_done;     /* t: sweeps applied since init/reset (+ pca_set_step offset)    */
+    int64_t counted_sweeps;  /* N_samp: sweeps accumulated into the MPM counts               */
+    int64_t kernel_launches; /* library kernels launched since init (all kinds)             */
+    int64_t sweep_launches;  /* sweep kernels launched since init                           */
+    double beta;             /* beta of the most recent sweep (beta0 before the first)       */
+    int32_t kernel;          /* PCA_KERNEL_BINARY or PCA_KERNEL_GENERAL actually used        */
+    int32_t nranks;          /* NCCL ranks attached (1 if none)                              */
+} pca_stats;
+
+/* Halo rows of the CURRENT state buffer, for caller-driven (loopback) exchange between
+ * strip contexts.  Each pointer is a device pointer to one padded row of `row_bytes`
+ * bytes for chain 0; chain b is at + b*chain_stride.  send_top/send_bottom are the
+ * context's first/last owned rows, recv_top/recv_bottom the halo rows above/below. */
+typedef struct pca_halo {
+    uint8_t* send_top;
+    uint8_t* send_bottom;
+    uint8_t* recv_top;
+    uint8_t* recv_bottom;
+    size_t row_bytes;
+    size_t chain_stride;
+} pca_halo;
+
+/* Version of this ABI (PCA_ABI_VERSION). */
+int32_t pca_abi_version(void);
+
+/* Bytes of device workspace a context with this configuration needs; 0 if the
+ * configuration is invalid (pca_last_error explains). */
+size_t pca_workspace_bytes(const pca_config* cfg);
+
+/* Create a context on the current CUDA device.
+ *   workspace: device buffer of ws_bytes >= pca_workspace_bytes(cfg), 256-B aligned,
+ *              owned by the caller; must outlive the context.
+ *   g:  observed (noisy) image [batch][rows][width], host or device; copied.
+ *   x0: initial state, same layout; NULL means x0 = g (R9); copied.
+ *   stream: cudaStream_t to enqueue all work on (NULL = legacy default stream).
+ * Returns PCA_EINVAL (bad cfg/pointers), PCA_ENOSPACE, PCA_EUNSUPPORTED, PCA_ECUDA. */
+pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_t ws_bytes,
+                    const uint8_t* g, const uint8_t* x0, void* stream);
+
+/* Restart the chain: t = 0, counts = 0; g replaced if non-NULL; state = x0 (or g if x0 is
+ * NULL).  Equivalent to a fresh pca_init on the same workspace. */
+pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0);
+
+/* Enqueue n >= 0 synchronous PCA sweeps t, t+1, ..., t+n-1 (asynchronous).  When the
+ * context owns a strip (rows < height) and NCCL is attached, each sweep is followed by
+ * the halo exchange with the neighbouring ranks; without NCCL, n must be <= 1 and the
+ * caller exchanges halos (pca_halo_ptrs).  Returns PCA_EUNSUPPORTED if a beta stage
+ * makes the exponent range exceed 700 (fp64 weight underflow) or if the uint16 MPM
+ * counters would overflow (> 65535 counted sweeps). */
+pca_status pca_sweep(pca_ctx* ctx, int32_t n);
+
+/* Write an estimate of the chain (kind PCA_EST_*) to out (host or device; layout in the
+ * enum).  MPM / MARGINALS / CM need counting enabled and N_samp >= 1.  Synchronises. */
+pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out);
+
+/* Exact integer sums of estimate `kind` (LAST or MPM) y against the original `truth`
+ * x (uint8 [batch][rows][width], host or device), per chain, over this context's rows:
+ * sums[b*8 + {0..6}] = {sum (x-y)^2, sum x, sum y, sum x^2, sum y^2, sum x*y, max x}, in
+ * level units, slot 7 = site count.  With NCCL attached the sums (max for slot 6) are
+ * all-reduced over ranks.  Synchronises. */
+pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int64_t* sums);
+
+/* PSNR (dB) and global SSIM (R16, R17) of estimate `kind` against
+ * truth, per chain, from pca_metric_sums computed exactly in 128-bit integers and then
+ * fp64.  psnr = +inf when MSE = 0; PCA_EINVAL if the original is all black. */
+pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* psnr,
+                         double* ssim);
+
+/* Copy the current state [batch][rows][width] to out / from x (host or device). */
+pca_status pca_read_state(pca_ctx* ctx, uint8_t* out);
+pca_status pca_write_state(pca_ctx* ctx, const uint8_t* x);
+
+/* Copy the MPM counters (uint16, layout above) to out / from c.  Used for checkpoints. */
+pca_status pca_read_counts(pca_ctx* ctx, uint16_t* out);
+pca_status pca_write_counts(pca_ctx* ctx, const uint16_t* c, int64_t counted_sweeps);
+
+/* Set the sweep index t of the next sweep (checkpoint resume). */
+pca_status pca_set_step(pca_ctx* ctx, int64_t t);
+
+pca_status pca_get_stats(pca_ctx* ctx, pca_stats* out);
+
+/* Device pointers of the halo rows of the current state (loopback exchange). */
+pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out);
+
+/* NCCL (row-strip sharding, one context per GPU per rank).  pca_nccl_unique_id fills
+ * 128 bytes (ncclUniqueId) on rank 0; the caller broadcasts them (torch.distributed);
+ * pca_attach_nccl creates the communicator owned by the context. */
+pca_status pca_nccl_unique_id(void* id128);
+pca_status pca_attach_nccl(pca_ctx* ctx, const void* id128, int32_t nranks, int32_t rank);
+
+/* Synchronise the context's stream and report any pending asynchronous error. */
+pca_status pca_sync(pca_ctx* ctx);
+
+/* Destroy the context (and its NCCL communicator).  Never frees caller memory. */
+pca_status pca_destroy(pca_ctx* ctx);
+
+/* Thread-local message describing the most recent failure in this thread. */
+const char* pca_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PCA_B200_H */

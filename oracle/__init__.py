@@ -168,14 +168,24 @@ def decide(p, u):
 
 def pca_sweep(m: Model, x, g, beta, seed, chain, t, rows=None):
     """One sweep; returns (new_state, margins).  rows=(r0, r1) restricts the update to
-    those rows (other rows of the output are copied from x)."""
+    those rows and returns only them: (new_rows [r1-r0, W], margins [r1-r0, W])."""
     x, g = _u8(x), _u8(g)
-    out = x.copy()
-    mg = np.full(x.shape, np.inf, np.float64)
-    r0, r1 = (0, m.H) if rows is None else rows
-    lib().orc_pca_sweep_rows(ctypes.byref(m), _p(x, ctypes.c_uint8), _p(g, ctypes.c_uint8),
-                             _p(out, ctypes.c_uint8), _p(mg, ctypes.c_double), beta, seed, chain,
-                             t, r0, r1)
+    if rows is None:
+        out = x.copy()
+        mg = np.full(x.shape, np.inf, np.float64)
+        lib().orc_pca_sweep_rows(ctypes.byref(m), _p(x, ctypes.c_uint8), _p(g, ctypes.c_uint8),
+                                 _p(out, ctypes.c_uint8), _p(mg, ctypes.c_double), beta, seed,
+                                 chain, t, 0, m.H)
+        return out, mg
+    r0, r1 = rows
+    out = np.zeros((r1 - r0, m.W), np.uint8)
+    mg = np.full((r1 - r0, m.W), np.inf, np.float64)
+    # the C routine writes out[r*W + c] for r in [r0, r1): hand it base pointers shifted back
+    # by r0 rows so that only the small buffers are touched
+    outp = ctypes.cast(out.ctypes.data - r0 * m.W, ctypes.POINTER(ctypes.c_uint8))
+    mgp = ctypes.cast(mg.ctypes.data - r0 * m.W * 8, ctypes.POINTER(ctypes.c_double))
+    lib().orc_pca_sweep_rows(ctypes.byref(m), _p(x, ctypes.c_uint8), _p(g, ctypes.c_uint8), outp,
+                             mgp, beta, seed, chain, t, r0, r1)
     return out, mg
 
 

@@ -1,0 +1,275 @@
+"""B200-native synchronous lazy-PCA sweep (arXiv 2507.14869) -- thin Python binding.
+
+Every entry point has the same name as the C ABI in ``include/pca.h`` and only
+marshals arguments: all device work runs in ``libpca_b200.so`` (hand-written sm_100a
+CUDA).  PyTorch is used for device memory (the workspace and image tensors) and streams.
+There is no CPU fallback: if the extension is missing or no CUDA device is present,
+``lib()`` / ``PcaContext`` raise.
+
+Image arguments are uint8 tensors (or NumPy arrays for host data) shaped
+``[batch, rows, width]`` (a 2-D ``[rows, width]`` is accepted for batch == 1).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpca_b200.so")
+
+PCA_OK, PCA_EINVAL, PCA_ESTATE, PCA_ECUDA, PCA_ENCCL, PCA_ENOSPACE, PCA_EUNSUPPORTED = (
+    0, -1, -2, -3, -4, -5, -6)
+EST_LAST, EST_MPM, EST_MARGINALS, EST_CM = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_GENERAL, KERNEL_BINARY = 0, 1, 2
+STATUS_NAMES = {0: "PCA_OK", -1: "PCA_EINVAL", -2: "PCA_ESTATE", -3: "PCA_ECUDA",
+                -4: "PCA_ENCCL", -5: "PCA_ENOSPACE", -6: "PCA_EUNSUPPORTED"}
+
+# every symbol include/pca.h declares
+EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "pca_sweep",
+           "pca_estimate", "pca_metric_sums", "pca_psnr_ssim", "pca_read_state",
+           "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
+           "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
+           "pca_destroy", "pca_last_error"]
+
+
+class PcaError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class pca_config(ctypes.Structure):
+    """Mirror of ``pca_config`` (include/pca.h)."""
+
+    _fields_ = [
+        ("height", ctypes.c_int32), ("width", ctypes.c_int32), ("batch", ctypes.c_int32),
+        ("levels", ctypes.c_int32), ("neighborhood", ctypes.c_int32),
+        ("periodic", ctypes.c_int32), ("J", ctypes.c_double), ("q", ctypes.c_double),
+        ("sigma", ctypes.c_double), ("beta0", ctypes.c_double), ("beta_step", ctypes.c_double),
+        ("beta_period", ctypes.c_int32), ("chain0", ctypes.c_int32),
+        ("coef_scale", ctypes.c_double), ("seed", ctypes.c_uint64),
+        ("mpm_burn_in", ctypes.c_int32), ("row0", ctypes.c_int32), ("rows", ctypes.c_int32),
+        ("kernel", ctypes.c_int32), ("rows_per_thread", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
+class pca_stats(ctypes.Structure):
+    _fields_ = [("sweeps_done", ctypes.c_int64), ("counted_sweeps", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64), ("sweep_launches", ctypes.c_int64),
+                ("beta", ctypes.c_double), ("kernel", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+
+
+class pca_halo(ctypes.Structure):
+    _fields_ = [("send_top", ctypes.c_void_p), ("send_bottom", ctypes.c_void_p),
+                ("recv_top", ctypes.c_void_p), ("recv_bottom", ctypes.c_void_p),
+                ("row_bytes", ctypes.c_size_t), ("chain_stride", ctypes.c_size_t)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpca_b200.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run paper_2507_14869_b200.build.build() "
+                               "(no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        cfgp = ctypes.POINTER(pca_config)
+        sigs = {
+            "pca_abi_version": (i32, []),
+            "pca_workspace_bytes": (sz, [cfgp]),
+            "pca_init": (i32, [ctypes.POINTER(vp), cfgp, vp, sz, vp, vp, vp]),
+            "pca_reset": (i32, [vp, vp, vp]),
+            "pca_sweep": (i32, [vp, i32]),
+            "pca_estimate": (i32, [vp, i32, vp]),
+            "pca_metric_sums": (i32, [vp, vp, i32, vp]),
+            "pca_psnr_ssim": (i32, [vp, vp, i32, vp, vp]),
+            "pca_read_state": (i32, [vp, vp]),
+            "pca_write_state": (i32, [vp, vp]),
+            "pca_read_counts": (i32, [vp, vp]),
+            "pca_write_counts": (i32, [vp, vp, i64]),
+            "pca_set_step": (i32, [vp, i64]),
+            "pca_get_stats": (i32, [vp, ctypes.POINTER(pca_stats)]),
+            "pca_halo_ptrs": (i32, [vp, ctypes.POINTER(pca_halo)]),
+            "pca_nccl_unique_id": (i32, [vp]),
+            "pca_attach_nccl": (i32, [vp, vp, i32, i32]),
+            "pca_sync": (i32, [vp]),
+            "pca_destroy": (i32, [vp]),
+            "pca_last_error": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sigs.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str):
+    if status != PCA_OK:
+        raise PcaError(status, where, lib().pca_last_error().decode())
+
+
+def make_config(height, width, levels, *, batch=1, neighborhood=8, periodic=False, J=1.0 / 3.0,
+                q=0.51, sigma=0.25, beta0=1.25, beta_step=0.25, beta_period=250, chain0=0,
+                coef_scale=1.0, seed=0, mpm_burn_in=-1, row0=0, rows=0, kernel=KERNEL_AUTO,
+                rows_per_thread=0) -> pca_config:
+    """pca_config with the paper's defaults (J = 1/3, q = 0.51, beta
+    1.25 + 0.25 every 250 sweeps; Moore-8 neighbourhood, free boundary)."""
+    c = pca_config()
+    c.height, c.width, c.batch, c.levels = int(height), int(width), int(batch), int(levels)
+    c.neighborhood, c.periodic = int(neighborhood), int(bool(periodic))
+    c.J, c.q, c.sigma = float(J), float(q), float(sigma)
+    c.beta0, c.beta_step, c.beta_period = float(beta0), float(beta_step), int(beta_period)
+    c.chain0, c.coef_scale, c.seed = int(chain0), float(coef_scale), int(seed) & (2**64 - 1)
+    c.mpm_burn_in, c.row0, c.rows = int(mpm_burn_in), int(row0), int(rows)
+    c.kernel, c.rows_per_thread = int(kernel), int(rows_per_thread)
+    return c
+
+
+def pca_workspace_bytes(cfg: pca_config) -> int:
+    n = lib().pca_workspace_bytes(ctypes.byref(cfg))
+    if n == 0:
+        raise PcaError(PCA_EINVAL, "pca_workspace_bytes", lib().pca_last_error().decode())
+    return int(n)
+
+
+def pca_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().pca_nccl_unique_id(buf), "pca_nccl_unique_id")
+    return buf.raw
+
+
+def _ptr(a) -> int:
+    """Address of a torch tensor (device or host) or a NumPy array (host)."""
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    assert a.is_contiguous(), "tensor must be contiguous"
+    return a.data_ptr()
+
+
+class PcaContext:
+    """One pca_ctx: a lattice (or row strip) x batch of chains on the current CUDA device.
+
+    The workspace is a torch uint8 CUDA tensor owned by this object.  ``stream`` defaults
+    to torch's current stream."""
+
+    def __init__(self, cfg: pca_config, g, x0=None, stream=None, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("PcaContext needs a CUDA device (no CPU fallback)")
+        self.cfg = cfg
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.rows = cfg.rows if cfg.rows else cfg.height
+        self.shape = (cfg.batch, self.rows, cfg.width)
+        nbytes = pca_workspace_bytes(cfg)
+        with torch.cuda.device(self.device):
+            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+            off = (-self.workspace.data_ptr()) % 256
+            self._ws_ptr = self.workspace.data_ptr() + off
+            self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+            self._keep = [g, x0]
+            h = ctypes.c_void_p()
+            _check(lib().pca_init(ctypes.byref(h), ctypes.byref(cfg), self._ws_ptr, nbytes,
+                                  _ptr(g), _ptr(x0), self.stream.cuda_stream), "pca_init")
+        self.handle = h
+        self._keep = None
+
+    # ---- ABI wrappers (same names) ----
+    def pca_reset(self, g=None, x0=None):
+        _check(lib().pca_reset(self.handle, _ptr(g), _ptr(x0)), "pca_reset")
+
+    def pca_sweep(self, n: int):
+        _check(lib().pca_sweep(self.handle, int(n)), "pca_sweep")
+
+    def pca_estimate(self, kind: int, out):
+        _check(lib().pca_estimate(self.handle, int(kind), _ptr(out)), "pca_estimate")
+        return out
+
+    def pca_metric_sums(self, truth, kind: int) -> np.ndarray:
+        s = np.zeros((self.cfg.batch, 8), np.int64)
+        _check(lib().pca_metric_sums(self.handle, _ptr(truth), int(kind), s.ctypes.data),
+               "pca_metric_sums")
+        return s
+
+    def pca_psnr_ssim(self, truth, kind: int):
+        p = np.zeros(self.cfg.batch, np.float64)
+        s = np.zeros(self.cfg.batch, np.float64)
+        _check(lib().pca_psnr_ssim(self.handle, _ptr(truth), int(kind), p.ctypes.data,
+                                   s.ctypes.data), "pca_psnr_ssim")
+        return p, s
+
+    def pca_read_state(self, out):
+        _check(lib().pca_read_state(self.handle, _ptr(out)), "pca_read_state")
+        return out
+
+    def pca_write_state(self, x):
+        _check(lib().pca_write_state(self.handle, _ptr(x)), "pca_write_state")
+
+    def pca_read_counts(self, out):
+        _check(lib().pca_read_counts(self.handle, _ptr(out)), "pca_read_counts")
+        return out
+
+    def pca_write_counts(self, c, counted: int):
+        _check(lib().pca_write_counts(self.handle, _ptr(c), int(counted)), "pca_write_counts")
+
+    def pca_set_step(self, t: int):
+        _check(lib().pca_set_step(self.handle, int(t)), "pca_set_step")
+
+    def pca_get_stats(self) -> pca_stats:
+        st = pca_stats()
+        _check(lib().pca_get_stats(self.handle, ctypes.byref(st)), "pca_get_stats")
+        return st
+
+    def pca_halo_ptrs(self) -> pca_halo:
+        h = pca_halo()
+        _check(lib().pca_halo_ptrs(self.handle, ctypes.byref(h)), "pca_halo_ptrs")
+        return h
+
+    def pca_attach_nccl(self, uid: bytes, nranks: int, rank: int):
+        buf = ctypes.create_string_buffer(uid, 128)
+        _check(lib().pca_attach_nccl(self.handle, buf, int(nranks), int(rank)), "pca_attach_nccl")
+
+    def pca_sync(self):
+        _check(lib().pca_sync(self.handle), "pca_sync")
+
+    def pca_destroy(self):
+        if getattr(self, "handle", None):
+            lib().pca_destroy(self.handle)
+            self.handle = None
+
+    # ---- conveniences (host NumPy results) ----
+    def state(self) -> np.ndarray:
+        return self.pca_read_state(np.empty(self.shape, np.uint8))
+
+    def counts(self) -> np.ndarray:
+        planes = 1 if self.cfg.levels == 2 else self.cfg.levels
+        shape = (self.cfg.batch, self.rows, self.cfg.width) if planes == 1 else \
+            (self.cfg.batch, planes, self.rows, self.cfg.width)
+        return self.pca_read_counts(np.empty(shape, np.uint16))
+
+    def estimate(self, kind: int) -> np.ndarray:
+        if kind in (EST_LAST, EST_MPM):
+            out = np.empty(self.shape, np.uint8)
+        elif kind == EST_CM:
+            out = np.empty(self.shape, np.float32)
+        else:
+            out = np.empty((self.cfg.batch, self.cfg.levels, self.rows, self.cfg.width), np.float32)
+        return self.pca_estimate(kind, out)
+
+    def __del__(self):
+        try:
+            self.pca_destroy()
+        except Exception:
+            pass

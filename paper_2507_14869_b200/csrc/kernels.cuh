@@ -1,0 +1,99 @@
+// Kernel parameter blocks and launch entry points shared by the host runtime
+// (runtime.cu) and the device kernels (sweep_binary.cu, sweep_general.cu, aux.cu).
+//
+// HBM layout of one context:
+//   x[2]   : uint8 [batch][rows+2][xpitch]; padded row -1..rows, data column c at byte
+//            XOFF + c; byte XOFF-1 / XOFF+W are the column halos; rows -1 / rows are the
+//            row halos.  Free boundary: halos hold the sentinel 0xFF (never a label).
+//            Torus: halos hold the wrapped labels, rewritten by every sweep.
+//   g      : uint8 [batch][rows][gpitch]   (gpitch = 16*nchunks, padding bytes 0)
+//   counts : uint16, levels == 2: [batch][rows][cpitch] (count of label 1);
+//            levels > 2: [batch][levels][rows][cpitch]  (cpitch = 16*nchunks)
+//   dtab   : fp64 [levels][levels], D[g][s] = exp(-b (lum g - lum s)^2)  (general kernel)
+//   sums   : uint64 [batch][8] metric accumulators
+//   stage  : uint8 [batch][rows][W] (+ fp32 space for MARGINALS/CM) host<->device staging
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "philox.cuh"
+
+namespace pcab200 {
+
+constexpr int XOFF = 16;           // data column 0 sits at byte 16 of a padded row
+constexpr int THR_ENTRIES = 324;   // binary thresholds [np 0..8][n1 0..8][g 0..1][x 0..1]
+constexpr uint32_t TAG_PCA = 1u;
+
+struct Geometry {
+    int W;             // columns
+    int rows;          // owned rows (local)
+    int H;             // global rows
+    int row0;          // global index of local row 0
+    int nchunks;       // ceil(W / 16)
+    int levels;
+    int nbhd;          // 4 or 8
+    int periodic;      // torus?
+    int self_halo_rows;  // torus and this context owns all rows: sweep rewrites row halos
+    int xpitch;        // bytes per padded x row
+    int gpitch;        // bytes per g row
+    int cpitch;        // uint16 elements per counts row
+    long long xchain;  // bytes between chains in an x buffer
+    long long gchain;  // bytes between chains in g
+    long long cplane;  // uint16 elements between label planes (levels > 2)
+    long long cchain;  // uint16 elements between chains in counts
+};
+
+struct SweepCommon {
+    Geometry geo;
+    const uint8_t* x_in;   // padded buffer of chain 0, pointing at row -1, byte 0
+    uint8_t* x_out;
+    const uint8_t* g;
+    uint16_t* counts;
+    PhiloxKeys keys;
+    uint32_t t;            // sweep index (Philox counter word 2)
+    uint32_t chain0;       // chain id of batch entry 0
+    int count_enable;      // accumulate MPM counts this sweep
+};
+
+// levels == 2 fast path: thr[((np*9 + n1)*2 + g)*2 + x] = ceil(p0 * 2^32) - 1, the
+// largest Philox word r for which the new label is 0 (u = r 2^-32 < F_0 = p0).
+struct BinarySweepParams {
+    SweepCommon c;
+    uint32_t thr[THR_ENTRIES];
+};
+
+// general path: A[n] = exp(a n), Cw = exp(-c); D table in global memory.
+struct GeneralSweepParams {
+    SweepCommon c;
+    double A[9];
+    double Cw;
+    const double* dtab;
+};
+
+struct MetricParams {
+    Geometry geo;
+    const uint8_t* x;      // padded current state, chain 0 row -1
+    const uint16_t* counts;
+    const uint8_t* truth;  // dense [batch][rows][W]
+    unsigned long long* sums;  // [batch][8]
+    int kind;              // 0 LAST, 1 MPM
+    int nsamp;             // counted sweeps (MPM ties for levels == 2)
+};
+
+// ---- launchers (return cudaError_t as int) ----
+int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread,
+                        void* stream);
+int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream);
+int launch_pack_state(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
+                      uint8_t* xbuf, int batch, int* bad_flag, void* stream);
+int launch_unpack_state(const Geometry& geo, const uint8_t* xbuf, uint8_t* dense, int batch,
+                        void* stream);
+int launch_check_levels(const uint8_t* dense, size_t n, int levels, int* bad_flag,
+                        void* stream);
+int launch_mpm(const Geometry& geo, const uint16_t* counts, int nsamp, uint8_t* dense_out,
+               int batch, void* stream);
+int launch_marginals(const Geometry& geo, const uint16_t* counts, int nsamp, float* out,
+                     long long out_chain_stride, int k, int batch, void* stream);
+int launch_metric_sums(const MetricParams& p, int batch, void* stream);
+
+}  // namespace pcab200

@@ -1,0 +1,810 @@
+// runtime.cu -- host runtime behind the C ABI of include/pca.h.
+//
+// Owns: configuration validation (before any device work), the workspace layout in HBM,
+// per-beta-stage tables, the sweep loop with buffer swaps (a7),
+// estimate / metric finalisation (a8, a9), checkpoint state I/O, and the NCCL
+// communicator for row-strip sharding (halo exchange of one padded row per neighbour
+// per sweep).  NCCL is loaded with dlopen on first use, so the library
+// has no link-time dependency beyond libc/libdl (cudart is linked statically).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "pca.h"
+
+using namespace pcab200;
+
+// ---------------------------------------------------------------------------
+namespace {
+
+thread_local std::string g_err;
+
+pca_status fail(pca_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+// ---- NCCL via dlopen ----
+struct NcclApi {
+    bool loaded = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+            return api;
+        }
+#define LOAD(name, sym)                                                    \
+    api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, sym));        \
+    if (!api.name) {                                                       \
+        api.why = std::string("missing NCCL symbol ") + sym;               \
+        return api;                                                        \
+    }
+        LOAD(GetUniqueId, "ncclGetUniqueId");
+        LOAD(CommInitRank, "ncclCommInitRank");
+        LOAD(CommDestroy, "ncclCommDestroy");
+        LOAD(CommGetAsyncError, "ncclCommGetAsyncError");
+        LOAD(Send, "ncclSend");
+        LOAD(Recv, "ncclRecv");
+        LOAD(GroupStart, "ncclGroupStart");
+        LOAD(GroupEnd, "ncclGroupEnd");
+        LOAD(AllReduce, "ncclAllReduce");
+        LOAD(GetErrorString, "ncclGetErrorString");
+#undef LOAD
+        api.loaded = true;
+    }
+    return api;
+}
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// Workspace layout: byte offsets of every region.
+struct Layout {
+    int rows = 0, nchunks = 0, xpitch = 0, gpitch = 0, cpitch = 0, cplanes = 0;
+    size_t xbuf = 0;      // bytes of one x buffer
+    size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_sums = 0,
+           off_sums_max = 0, off_flag = 0, off_stage = 0;
+    size_t stage_bytes = 0, counts_bytes = 0, total = 0;
+};
+
+bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
+
+pca_status validate(const pca_config* c) {
+    if (!c) return fail(PCA_EINVAL, "config is NULL");
+    if (c->height < 1 || c->width < 1) return fail(PCA_EINVAL, "height and width must be >= 1");
+    if (c->width > (1 << 30) || c->height > (1 << 30))
+        return fail(PCA_EINVAL, "height/width must be <= 2^30");
+    if (c->batch < 1 || c->batch > 65535) return fail(PCA_EINVAL, "batch must be in [1, 65535]");
+    if (c->levels < 2 || c->levels > 255) return fail(PCA_EINVAL, "levels must be in [2, 255]");
+    if (c->neighborhood != 4 && c->neighborhood != 8)
+        return fail(PCA_EINVAL, "neighborhood must be 4 or 8");
+    if (c->periodic != 0 && c->periodic != 1) return fail(PCA_EINVAL, "periodic must be 0 or 1");
+    if (c->periodic && (c->height < 3 || c->width < 3))
+        return fail(PCA_EINVAL, "a torus needs height, width >= 3 (distinct neighbours, R7)");
+    if (!finite_pos(c->J)) return fail(PCA_EINVAL, "J must be finite and > 0");
+    if (!std::isfinite(c->q) || c->q < 0.0) return fail(PCA_EINVAL, "q must be finite and >= 0");
+    if (!finite_pos(c->sigma)) return fail(PCA_EINVAL, "sigma must be finite and > 0");
+    if (!finite_pos(c->beta0)) return fail(PCA_EINVAL, "beta0 must be finite and > 0");
+    if (!std::isfinite(c->beta_step) || c->beta_step < 0.0)
+        return fail(PCA_EINVAL, "beta_step must be finite and >= 0");
+    if (c->beta_period < 1) return fail(PCA_EINVAL, "beta_period must be >= 1");
+    if (!finite_pos(c->coef_scale)) return fail(PCA_EINVAL, "coef_scale must be finite and > 0");
+    if (c->chain0 < 0 || (long long)c->chain0 + c->batch > (1LL << 24))
+        return fail(PCA_EINVAL, "chain ids must lie in [0, 2^24)");
+    if (c->rows == 0) {
+        if (c->row0 != 0) return fail(PCA_EINVAL, "rows == 0 (whole lattice) requires row0 == 0");
+    } else if (c->rows < 1 || c->row0 < 0 || (long long)c->row0 + c->rows > c->height) {
+        return fail(PCA_EINVAL, "owned rows [row0, row0+rows) must lie inside [0, height)");
+    }
+    if (c->kernel < 0 || c->kernel > 2) return fail(PCA_EINVAL, "kernel must be 0, 1 or 2");
+    if (c->kernel == PCA_KERNEL_BINARY && c->levels != 2)
+        return fail(PCA_EUNSUPPORTED, "the binary kernel needs levels == 2");
+    const int R = c->rows_per_thread;
+    if (!(R == 0 || R == 1 || R == 2 || R == 4 || R == 8 || R == 16 || R == 32))
+        return fail(PCA_EINVAL, "rows_per_thread must be 0 or a power of two <= 32");
+    for (int i = 0; i < 7; ++i)
+        if (c->reserved[i] != 0) return fail(PCA_EINVAL, "reserved fields must be zero");
+    return PCA_OK;
+}
+
+Layout make_layout(const pca_config* c) {
+    Layout L;
+    L.rows = c->rows == 0 ? c->height : c->rows;
+    L.nchunks = (c->width + 15) / 16;
+    L.xpitch = 16 * L.nchunks + 32;
+    L.gpitch = 16 * L.nchunks;
+    L.cpitch = 16 * L.nchunks;
+    L.cplanes = c->levels == 2 ? 1 : c->levels;
+    const size_t B = (size_t)c->batch, R = (size_t)L.rows, W = (size_t)c->width;
+    L.xbuf = B * (R + 2) * (size_t)L.xpitch;
+    L.counts_bytes = B * (size_t)L.cplanes * R * (size_t)L.cpitch * 2;
+    L.stage_bytes = B * R * W * 4;  // uint8 images and fp32 planes (one label plane at a time)
+    size_t o = 0;
+    L.off_x0 = o; o = align256(o + L.xbuf);
+    L.off_x1 = o; o = align256(o + L.xbuf);
+    L.off_g = o; o = align256(o + B * R * (size_t)L.gpitch);
+    L.off_counts = o; o = align256(o + L.counts_bytes);
+    L.off_dtab = o; o = align256(o + (size_t)c->levels * c->levels * sizeof(double));
+    L.off_sums = o; o = align256(o + B * 8 * sizeof(unsigned long long));
+    L.off_sums_max = o; o = align256(o + B * 8 * sizeof(unsigned long long));
+    L.off_flag = o; o = align256(o + 256);
+    L.off_stage = o; o = align256(o + L.stage_bytes);
+    L.total = o;
+    return L;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct pca_ctx {
+    pca_config cfg;
+    Layout lay;
+    Geometry geo;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint8_t* ws = nullptr;
+    uint8_t* x[2] = {nullptr, nullptr};
+    int cur = 0;
+    uint8_t* g = nullptr;
+    uint16_t* counts = nullptr;
+    double* dtab = nullptr;
+    unsigned long long* sums = nullptr;
+    unsigned long long* sums_max = nullptr;
+    int* flag = nullptr;
+    uint8_t* stage = nullptr;
+    int64_t t = 0, counted = 0, launches = 0, sweep_launches = 0;
+    double beta_last = 0.0;
+    int kernel = PCA_KERNEL_BINARY;
+    int rows_per_thread = 8;
+    int poisoned = 0;
+    int64_t tab_stage = -1;
+    BinarySweepParams bin;
+    GeneralSweepParams gen;
+    std::vector<double> dtab_host;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+namespace {
+
+pca_status cuda_fail(pca_ctx* ctx, cudaError_t e, const char* where) {
+    if (ctx) ctx->poisoned = 1;
+    return fail(PCA_ECUDA, "%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+}
+
+#define CK(ctx, expr)                                                 \
+    do {                                                              \
+        cudaError_t e_ = (cudaError_t)(expr);                         \
+        if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #expr);    \
+    } while (0)
+
+pca_status usable(pca_ctx* ctx) {
+    if (!ctx) return fail(PCA_EINVAL, "context is NULL");
+    if (ctx->poisoned)
+        return fail(PCA_ESTATE, "context poisoned by an earlier CUDA/NCCL error; destroy it");
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+    return PCA_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+size_t dense_bytes(const pca_ctx* ctx) {
+    return (size_t)ctx->cfg.batch * ctx->lay.rows * (size_t)ctx->cfg.width;
+}
+
+// device view of a dense uint8 image argument (host data staged through `stage`)
+pca_status device_input(pca_ctx* ctx, const uint8_t* p, const uint8_t** out) {
+    if (is_device_ptr(p)) {
+        *out = p;
+        return PCA_OK;
+    }
+    CK(ctx, cudaMemcpyAsync(ctx->stage, p, dense_bytes(ctx), cudaMemcpyHostToDevice, ctx->stream));
+    *out = ctx->stage;
+    return PCA_OK;
+}
+
+pca_status sync(pca_ctx* ctx) {
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    CK(ctx, cudaGetLastError());
+    if (ctx->comm) {
+        ncclResult_t ar = ncclSuccess;
+        nccl().CommGetAsyncError(ctx->comm, &ar);
+        if (ar != ncclSuccess) {
+            ctx->poisoned = 1;
+            return fail(PCA_ENCCL, "NCCL async error: %s", nccl().GetErrorString(ar));
+        }
+    }
+    return PCA_OK;
+}
+
+pca_status check_flag(pca_ctx* ctx, const char* what) {
+    int h = 0;
+    CK(ctx, cudaMemcpyAsync(&h, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    pca_status st = sync(ctx);
+    if (st != PCA_OK) return st;
+    if (h) return fail(PCA_EINVAL, "%s contains a value >= levels", what);
+    return PCA_OK;
+}
+
+#define LAUNCH(ctx, expr)                                                        \
+    do {                                                                         \
+        int e_ = (expr);                                                         \
+        (ctx)->launches++;                                                       \
+        if (e_ != 0) return cuda_fail((ctx), (cudaError_t)e_, #expr);            \
+    } while (0)
+
+double beta_at(const pca_config& c, int64_t t) {
+    return c.beta0 + c.beta_step * (double)(t / c.beta_period);
+}
+
+double lum(int k, int levels) { return (double)k / (double)(levels - 1); }
+
+// a1: per-stage tables.  The binary thresholds repeat the per-site law of PAPER.md:462-477
+// in fp64 exactly as written (E = a n - b d^2 - c 1{s != x}; p0 = e0/(e0 + e1) with the
+// max subtracted), so T = ceil(p0 2^32) is the integer form of "u < F_0".
+pca_status build_tables(pca_ctx* ctx, int64_t t) {
+    const pca_config& c = ctx->cfg;
+    const int64_t stage = t / c.beta_period;
+    if (stage == ctx->tab_stage) return PCA_OK;
+    const double beta = beta_at(c, t);
+    const double a = c.coef_scale * 2.0 * beta * c.J;
+    const double b = c.coef_scale / (2.0 * c.sigma * c.sigma);
+    const double cq = beta * c.q;
+    const double range = a * (double)c.neighborhood + b + cq;
+    if (!(range < 700.0))
+        return fail(PCA_EUNSUPPORTED,
+                    "beta stage %lld: exponent range a*N + b + c = %g >= 700 would underflow fp64 "
+                    "weights",
+                    (long long)stage, range);
+    if (ctx->kernel == PCA_KERNEL_BINARY) {
+        for (int np = 0; np <= 8; ++np)
+            for (int n1 = 0; n1 <= 8; ++n1)
+                for (int gl = 0; gl < 2; ++gl)
+                    for (int xl = 0; xl < 2; ++xl) {
+                        const int idx = ((np * 9 + n1) * 2 + gl) * 2 + xl;
+                        if (n1 > np) {
+                            ctx->bin.thr[idx] = 0u;
+                            continue;
+                        }
+                        const int n[2] = {np - n1, n1};
+                        double E[2];
+                        for (int s = 0; s < 2; ++s) {
+                            const double d = lum(gl, 2) - lum(s, 2);
+                            const double inert = (s != xl) ? 1.0 : 0.0;
+                            E[s] = a * (double)n[s] - b * d * d - cq * inert;
+                        }
+                        double Emax = -INFINITY;
+                        for (int s = 0; s < 2; ++s)
+                            if (E[s] > Emax) Emax = E[s];
+                        const double e0 = exp(E[0] - Emax);
+                        const double e1 = exp(E[1] - Emax);
+                        const double Z = 0.0 + e0 + e1;
+                        const double p0 = e0 / Z;
+                        const double T = ceil(p0 * 4294967296.0);  // in [1, 2^32]
+                        if (!(T >= 1.0))
+                            return fail(PCA_EUNSUPPORTED, "p(0) underflowed to 0 at beta %g", beta);
+                        ctx->bin.thr[idx] = (uint32_t)(T - 1.0);
+                    }
+    } else {
+        for (int n = 0; n <= 8; ++n) ctx->gen.A[n] = exp(a * (double)n);
+        ctx->gen.Cw = exp(-cq);
+    }
+    ctx->tab_stage = stage;
+    ctx->beta_last = beta;
+    return PCA_OK;
+}
+
+void fill_common(pca_ctx* ctx, SweepCommon& sc, int64_t t, int count) {
+    sc.geo = ctx->geo;
+    sc.x_in = ctx->x[ctx->cur];
+    sc.x_out = ctx->x[ctx->cur ^ 1];
+    sc.g = ctx->g;
+    sc.counts = ctx->counts;
+    const uint32_t k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu);
+    const uint32_t k1 = (uint32_t)(ctx->cfg.seed >> 32);
+    for (int i = 0; i < 10; ++i) {
+        sc.keys.rk[2 * i] = k0 + (uint32_t)i * 0x9E3779B9u;
+        sc.keys.rk[2 * i + 1] = k1 + (uint32_t)i * 0xBB67AE85u;
+    }
+    sc.t = (uint32_t)t;
+    sc.chain0 = (uint32_t)ctx->cfg.chain0;
+    sc.count_enable = count;
+}
+
+// Halo exchange of buffer `buf` with the neighbouring ranks (row strips): send the first
+// owned row up and the last owned row down, receive the halo rows.  Order per chain:
+// send(top->up), recv(bottom halo<-down), send(bottom->down), recv(top halo<-up); with
+// 2 ranks on a torus both neighbours are the same peer and NCCL matches in issue order.
+pca_status exchange(pca_ctx* ctx, uint8_t* buf) {
+    if (!ctx->comm || ctx->nranks <= 1) return PCA_OK;
+    NcclApi& N = nccl();
+    const int P = ctx->nranks, r = ctx->rank;
+    int up = r - 1, down = r + 1;
+    if (ctx->cfg.periodic) {
+        up = (r + P - 1) % P;
+        down = (r + 1) % P;
+    } else {
+        if (up < 0) up = -1;
+        if (down >= P) down = -1;
+    }
+    const size_t rb = (size_t)ctx->lay.xpitch;
+    ncclResult_t e = N.GroupStart();
+    for (int b = 0; b < ctx->cfg.batch && e == ncclSuccess; ++b) {
+        uint8_t* base = buf + (size_t)b * ctx->geo.xchain;
+        uint8_t* top = base + rb;
+        uint8_t* bottom = base + (size_t)ctx->lay.rows * rb;
+        uint8_t* halo_top = base;
+        uint8_t* halo_bottom = base + (size_t)(ctx->lay.rows + 1) * rb;
+        if (up >= 0 && e == ncclSuccess) e = N.Send(top, rb, ncclUint8, up, ctx->comm, ctx->stream);
+        if (down >= 0 && e == ncclSuccess)
+            e = N.Recv(halo_bottom, rb, ncclUint8, down, ctx->comm, ctx->stream);
+        if (down >= 0 && e == ncclSuccess)
+            e = N.Send(bottom, rb, ncclUint8, down, ctx->comm, ctx->stream);
+        if (up >= 0 && e == ncclSuccess) e = N.Recv(halo_top, rb, ncclUint8, up, ctx->comm, ctx->stream);
+    }
+    ncclResult_t e2 = N.GroupEnd();
+    if (e == ncclSuccess) e = e2;
+    if (e != ncclSuccess) {
+        ctx->poisoned = 1;
+        return fail(PCA_ENCCL, "halo exchange: %s", N.GetErrorString(e));
+    }
+    return PCA_OK;
+}
+
+pca_status load_state(pca_ctx* ctx, const uint8_t* src, int pitch, long long chain_stride,
+                      const char* what) {
+    CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
+    LAUNCH(ctx, launch_pack_state(ctx->geo, src, pitch, chain_stride, ctx->x[ctx->cur],
+                                  ctx->cfg.batch, ctx->flag, ctx->stream));
+    pca_status st = check_flag(ctx, what);
+    if (st != PCA_OK) return st;
+    return exchange(ctx, ctx->x[ctx->cur]);
+}
+
+pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
+    const pca_config& c = ctx->cfg;
+    const Layout& L = ctx->lay;
+    if (g) {
+        CK(ctx, cudaMemsetAsync(ctx->g, 0, (size_t)c.batch * L.rows * L.gpitch, ctx->stream));
+        CK(ctx, cudaMemcpy2DAsync(ctx->g, L.gpitch, g, c.width, c.width, (size_t)c.batch * L.rows,
+                                  cudaMemcpyDefault, ctx->stream));
+        CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
+        LAUNCH(ctx, launch_check_levels(ctx->g, (size_t)c.batch * L.rows * L.gpitch, c.levels,
+                                        ctx->flag, ctx->stream));
+        pca_status st = check_flag(ctx, "g");
+        if (st != PCA_OK) return st;
+    }
+    CK(ctx, cudaMemsetAsync(ctx->x[0], 0xFF, L.xbuf, ctx->stream));
+    CK(ctx, cudaMemsetAsync(ctx->x[1], 0xFF, L.xbuf, ctx->stream));
+    CK(ctx, cudaMemsetAsync(ctx->counts, 0, L.counts_bytes, ctx->stream));
+    ctx->cur = 0;
+    ctx->t = 0;
+    ctx->counted = 0;
+    ctx->tab_stage = -1;
+    ctx->beta_last = c.beta0;
+    if (x0) {
+        const uint8_t* dx = nullptr;
+        pca_status st = device_input(ctx, x0, &dx);
+        if (st != PCA_OK) return st;
+        return load_state(ctx, dx, c.width, (long long)L.rows * c.width, "x0");
+    }
+    return load_state(ctx, ctx->g, L.gpitch, (long long)L.rows * L.gpitch, "g");
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int32_t pca_abi_version(void) { return PCA_ABI_VERSION; }
+
+const char* pca_last_error(void) { return g_err.c_str(); }
+
+size_t pca_workspace_bytes(const pca_config* cfg) {
+    if (validate(cfg) != PCA_OK) return 0;
+    return make_layout(cfg).total;
+}
+
+pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_t ws_bytes,
+                    const uint8_t* g, const uint8_t* x0, void* stream) {
+    if (!out) return fail(PCA_EINVAL, "out is NULL");
+    *out = nullptr;
+    pca_status st = validate(cfg);
+    if (st != PCA_OK) return st;
+    if (!workspace || !g) return fail(PCA_EINVAL, "workspace and g must be non-NULL");
+    if (((uintptr_t)workspace & 255u) != 0) return fail(PCA_EINVAL, "workspace must be 256-B aligned");
+    const Layout L = make_layout(cfg);
+    if (ws_bytes < L.total)
+        return fail(PCA_ENOSPACE, "workspace has %zu bytes, needs %zu", ws_bytes, L.total);
+    if (!is_device_ptr(workspace)) return fail(PCA_EINVAL, "workspace must be device memory");
+
+    pca_ctx* ctx = new (std::nothrow) pca_ctx();
+    if (!ctx) return fail(PCA_EINVAL, "out of host memory");
+    ctx->cfg = *cfg;
+    if (ctx->cfg.rows == 0) ctx->cfg.rows = cfg->height;
+    ctx->lay = L;
+    cudaGetDevice(&ctx->device);
+    ctx->stream = (cudaStream_t)stream;
+    ctx->ws = (uint8_t*)workspace;
+    ctx->x[0] = ctx->ws + L.off_x0;
+    ctx->x[1] = ctx->ws + L.off_x1;
+    ctx->g = ctx->ws + L.off_g;
+    ctx->counts = (uint16_t*)(ctx->ws + L.off_counts);
+    ctx->dtab = (double*)(ctx->ws + L.off_dtab);
+    ctx->sums = (unsigned long long*)(ctx->ws + L.off_sums);
+    ctx->sums_max = (unsigned long long*)(ctx->ws + L.off_sums_max);
+    ctx->flag = (int*)(ctx->ws + L.off_flag);
+    ctx->stage = ctx->ws + L.off_stage;
+    ctx->kernel = (cfg->kernel == PCA_KERNEL_AUTO) ? (cfg->levels == 2 ? PCA_KERNEL_BINARY
+                                                                       : PCA_KERNEL_GENERAL)
+                                                   : cfg->kernel;
+    ctx->rows_per_thread = cfg->rows_per_thread ? cfg->rows_per_thread : 8;
+
+    Geometry& G = ctx->geo;
+    G.W = cfg->width;
+    G.rows = L.rows;
+    G.H = cfg->height;
+    G.row0 = cfg->row0;
+    G.nchunks = L.nchunks;
+    G.levels = cfg->levels;
+    G.nbhd = cfg->neighborhood;
+    G.periodic = cfg->periodic;
+    G.self_halo_rows = (cfg->periodic && L.rows == cfg->height) ? 1 : 0;
+    G.xpitch = L.xpitch;
+    G.gpitch = L.gpitch;
+    G.cpitch = L.cpitch;
+    G.xchain = (long long)(L.rows + 2) * L.xpitch;
+    G.gchain = (long long)L.rows * L.gpitch;
+    G.cplane = (long long)L.rows * L.cpitch;
+    G.cchain = (long long)L.cplanes * L.rows * L.cpitch;
+
+    // D[g][s] = exp(-b (lum g - lum s)^2): beta-independent (R5), built once.
+    const double b = cfg->coef_scale / (2.0 * cfg->sigma * cfg->sigma);
+    ctx->dtab_host.resize((size_t)cfg->levels * cfg->levels);
+    for (int gl = 0; gl < cfg->levels; ++gl)
+        for (int s = 0; s < cfg->levels; ++s) {
+            const double d = lum(gl, cfg->levels) - lum(s, cfg->levels);
+            ctx->dtab_host[(size_t)gl * cfg->levels + s] = exp(-b * d * d);
+        }
+    ctx->gen.dtab = ctx->dtab;
+
+    auto bail = [&](pca_status s) {
+        delete ctx;
+        return s;
+    };
+    cudaError_t e = cudaMemcpyAsync(ctx->dtab, ctx->dtab_host.data(),
+                                    ctx->dtab_host.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                    ctx->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "upload dtab"));
+    st = do_reset(ctx, g, x0);
+    if (st != PCA_OK) return bail(st);
+    *out = ctx;
+    return PCA_OK;
+}
+
+pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    return do_reset(ctx, g, x0);
+}
+
+pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
+    const bool strip = ctx->lay.rows < ctx->cfg.height;
+    if (strip && !ctx->comm && n > 1)
+        return fail(PCA_EINVAL,
+                    "a strip context without NCCL sweeps one step at a time (caller exchanges halos)");
+    for (int32_t i = 0; i < n; ++i) {
+        const int64_t t = ctx->t;
+        if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
+        st = build_tables(ctx, t);
+        if (st != PCA_OK) return st;
+        const int count = (ctx->cfg.mpm_burn_in >= 0 && t >= ctx->cfg.mpm_burn_in) ? 1 : 0;
+        if (count && ctx->counted + 1 > 65535)
+            return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+        if (ctx->kernel == PCA_KERNEL_BINARY) {
+            fill_common(ctx, ctx->bin.c, t, count);
+            LAUNCH(ctx, launch_sweep_binary(ctx->bin, ctx->cfg.batch, ctx->rows_per_thread,
+                                            ctx->stream));
+        } else {
+            fill_common(ctx, ctx->gen.c, t, count);
+            LAUNCH(ctx, launch_sweep_general(ctx->gen, ctx->cfg.batch, ctx->stream));
+        }
+        ctx->sweep_launches++;
+        st = exchange(ctx, ctx->x[ctx->cur ^ 1]);
+        if (st != PCA_OK) return st;
+        ctx->cur ^= 1;
+        ctx->t = t + 1;
+        ctx->counted += count;
+    }
+    return PCA_OK;
+}
+
+pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!out) return fail(PCA_EINVAL, "out is NULL");
+    if (kind < PCA_EST_LAST || kind > PCA_EST_CM) return fail(PCA_EINVAL, "unknown estimate kind");
+    const pca_config& c = ctx->cfg;
+    if (kind != PCA_EST_LAST && ctx->counted < 1)
+        return fail(PCA_EINVAL, "MPM/marginal/CM estimates need counted sweeps (mpm_burn_in)");
+    const bool dev = is_device_ptr(out);
+    const size_t plane = (size_t)ctx->lay.rows * c.width;
+    if (kind == PCA_EST_LAST || kind == PCA_EST_MPM) {
+        uint8_t* dst = dev ? (uint8_t*)out : ctx->stage;
+        if (kind == PCA_EST_LAST)
+            LAUNCH(ctx, launch_unpack_state(ctx->geo, ctx->x[ctx->cur], dst, c.batch, ctx->stream));
+        else
+            LAUNCH(ctx, launch_mpm(ctx->geo, ctx->counts, (int)ctx->counted, dst, c.batch, ctx->stream));
+        if (!dev)
+            CK(ctx, cudaMemcpyAsync(out, ctx->stage, dense_bytes(ctx), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+        return sync(ctx);
+    }
+    // float outputs: CM [B][rows][W]; MARGINALS [B][levels][rows][W], one label plane per pass
+    const int nplanes = kind == PCA_EST_CM ? 1 : c.levels;
+    for (int k = 0; k < nplanes; ++k) {
+        const int kk = kind == PCA_EST_CM ? -1 : k;
+        float* dst = dev ? (float*)out + (size_t)k * plane : (float*)ctx->stage;
+        const long long cs = dev ? (long long)nplanes * plane : (long long)plane;
+        LAUNCH(ctx, launch_marginals(ctx->geo, ctx->counts, (int)ctx->counted, dst, cs, kk, c.batch,
+                                     ctx->stream));
+        if (!dev)
+            CK(ctx, cudaMemcpy2DAsync((float*)out + (size_t)k * plane, nplanes * plane * 4,
+                                      ctx->stage, plane * 4, plane * 4, c.batch,
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    return sync(ctx);
+}
+
+pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int64_t* sums) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!truth || !sums) return fail(PCA_EINVAL, "truth and sums must be non-NULL");
+    if (kind != PCA_EST_LAST && kind != PCA_EST_MPM)
+        return fail(PCA_EINVAL, "metric sums are defined for LAST and MPM");
+    if (kind == PCA_EST_MPM && ctx->counted < 1)
+        return fail(PCA_EINVAL, "MPM needs counted sweeps (mpm_burn_in)");
+    const pca_config& c = ctx->cfg;
+    const uint8_t* dt = nullptr;
+    st = device_input(ctx, truth, &dt);
+    if (st != PCA_OK) return st;
+    const size_t nb = (size_t)c.batch * 8 * sizeof(unsigned long long);
+    CK(ctx, cudaMemsetAsync(ctx->sums, 0, nb, ctx->stream));
+    MetricParams mp;
+    mp.geo = ctx->geo;
+    mp.x = ctx->x[ctx->cur];
+    mp.counts = ctx->counts;
+    mp.truth = dt;
+    mp.sums = ctx->sums;
+    mp.kind = kind;
+    mp.nsamp = (int)ctx->counted;
+    LAUNCH(ctx, launch_metric_sums(mp, c.batch, ctx->stream));
+    if (ctx->comm && ctx->nranks > 1) {
+        NcclApi& N = nccl();
+        CK(ctx, cudaMemcpyAsync(ctx->sums_max, ctx->sums, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+        ncclResult_t e = N.AllReduce(ctx->sums, ctx->sums, (size_t)c.batch * 8, ncclUint64, ncclSum,
+                                     ctx->comm, ctx->stream);
+        if (e == ncclSuccess)
+            e = N.AllReduce(ctx->sums_max, ctx->sums_max, (size_t)c.batch * 8, ncclUint64, ncclMax,
+                            ctx->comm, ctx->stream);
+        if (e != ncclSuccess) {
+            ctx->poisoned = 1;
+            return fail(PCA_ENCCL, "metric all-reduce: %s", N.GetErrorString(e));
+        }
+    }
+    std::vector<unsigned long long> h((size_t)c.batch * 8), hm((size_t)c.batch * 8);
+    CK(ctx, cudaMemcpyAsync(h.data(), ctx->sums, nb, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->comm && ctx->nranks > 1)
+        CK(ctx, cudaMemcpyAsync(hm.data(), ctx->sums_max, nb, cudaMemcpyDeviceToHost, ctx->stream));
+    st = sync(ctx);
+    if (st != PCA_OK) return st;
+    for (int bch = 0; bch < c.batch; ++bch)
+        for (int k = 0; k < 8; ++k) {
+            unsigned long long v = h[(size_t)bch * 8 + k];
+            if (k == 6 && ctx->comm && ctx->nranks > 1) v = hm[(size_t)bch * 8 + k];
+            sums[(size_t)bch * 8 + k] = (int64_t)v;
+        }
+    return PCA_OK;
+}
+
+pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* psnr,
+                         double* ssim) {
+    if (!psnr || !ssim) return fail(PCA_EINVAL, "psnr and ssim must be non-NULL");
+    std::vector<int64_t> s((size_t)(ctx ? ctx->cfg.batch : 1) * 8);
+    pca_status st = pca_metric_sums(ctx, truth, kind, s.data());
+    if (st != PCA_OK) return st;
+    const double L1 = (double)(ctx->cfg.levels - 1);
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    bool black = false;
+    for (int b = 0; b < ctx->cfg.batch; ++b) {
+        const int64_t* v = &s[(size_t)b * 8];
+        const __int128 N = v[7];
+        const double Nd = (double)v[7];
+        // MSE on luminances, PSNR with the original's max
+        const double mse = (double)v[0] / (Nd * L1 * L1);
+        if (v[6] == 0) black = true;
+        const double xmax = (double)v[6] / L1;
+        psnr[b] = (mse == 0.0) ? INFINITY : 20.0 * log10(xmax / sqrt(mse));
+        // global SSIM (R16): population moments from exact numerators
+        const __int128 vx = N * (__int128)v[3] - (__int128)v[1] * v[1];
+        const __int128 vy = N * (__int128)v[4] - (__int128)v[2] * v[2];
+        const __int128 cxy = N * (__int128)v[5] - (__int128)v[1] * v[2];
+        const double den = Nd * Nd * L1 * L1;
+        const double mux = (double)v[1] / (Nd * L1), muy = (double)v[2] / (Nd * L1);
+        const double sx = (double)vx / den, sy = (double)vy / den, sxy = (double)cxy / den;
+        ssim[b] = ((2.0 * mux * muy + c1) * (2.0 * sxy + c2)) /
+                  ((mux * mux + muy * muy + c1) * (sx + sy + c2));
+    }
+    if (black) return fail(PCA_EINVAL, "original image is all black: PSNR undefined (R17)");
+    return PCA_OK;
+}
+
+pca_status pca_read_state(pca_ctx* ctx, uint8_t* out) { return pca_estimate(ctx, PCA_EST_LAST, out); }
+
+pca_status pca_write_state(pca_ctx* ctx, const uint8_t* x) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!x) return fail(PCA_EINVAL, "x is NULL");
+    const uint8_t* dx = nullptr;
+    st = device_input(ctx, x, &dx);
+    if (st != PCA_OK) return st;
+    return load_state(ctx, dx, ctx->cfg.width, (long long)ctx->lay.rows * ctx->cfg.width, "x");
+}
+
+pca_status pca_read_counts(pca_ctx* ctx, uint16_t* out) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!out) return fail(PCA_EINVAL, "out is NULL");
+    const pca_config& c = ctx->cfg;
+    const Layout& L = ctx->lay;
+    CK(ctx, cudaMemcpy2DAsync(out, (size_t)c.width * 2, ctx->counts, (size_t)L.cpitch * 2,
+                              (size_t)c.width * 2, (size_t)c.batch * L.cplanes * L.rows,
+                              cudaMemcpyDefault, ctx->stream));
+    return sync(ctx);
+}
+
+pca_status pca_write_counts(pca_ctx* ctx, const uint16_t* cin, int64_t counted) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!cin || counted < 0 || counted > 65535) return fail(PCA_EINVAL, "bad counts arguments");
+    const pca_config& c = ctx->cfg;
+    const Layout& L = ctx->lay;
+    CK(ctx, cudaMemcpy2DAsync(ctx->counts, (size_t)L.cpitch * 2, cin, (size_t)c.width * 2,
+                              (size_t)c.width * 2, (size_t)c.batch * L.cplanes * L.rows,
+                              cudaMemcpyDefault, ctx->stream));
+    ctx->counted = counted;
+    return sync(ctx);
+}
+
+pca_status pca_set_step(pca_ctx* ctx, int64_t t) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (t < 0 || t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EINVAL, "t out of range");
+    ctx->t = t;
+    return PCA_OK;
+}
+
+pca_status pca_get_stats(pca_ctx* ctx, pca_stats* out) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!out) return fail(PCA_EINVAL, "out is NULL");
+    st = sync(ctx);
+    if (st != PCA_OK) return st;
+    out->sweeps_done = ctx->t;
+    out->counted_sweeps = ctx->counted;
+    out->kernel_launches = ctx->launches;
+    out->sweep_launches = ctx->sweep_launches;
+    out->beta = ctx->beta_last;
+    out->kernel = ctx->kernel;
+    out->nranks = ctx->nranks;
+    return PCA_OK;
+}
+
+pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!out) return fail(PCA_EINVAL, "out is NULL");
+    uint8_t* base = ctx->x[ctx->cur];
+    const size_t rb = (size_t)ctx->lay.xpitch;
+    out->send_top = base + rb;
+    out->send_bottom = base + (size_t)ctx->lay.rows * rb;
+    out->recv_top = base;
+    out->recv_bottom = base + (size_t)(ctx->lay.rows + 1) * rb;
+    out->row_bytes = rb;
+    out->chain_stride = (size_t)ctx->geo.xchain;
+    return PCA_OK;
+}
+
+pca_status pca_nccl_unique_id(void* id128) {
+    if (!id128) return fail(PCA_EINVAL, "id is NULL");
+    NcclApi& N = nccl();
+    if (!N.loaded) return fail(PCA_ENCCL, "%s", N.why.c_str());
+    ncclUniqueId id;
+    ncclResult_t e = N.GetUniqueId(&id);
+    if (e != ncclSuccess) return fail(PCA_ENCCL, "ncclGetUniqueId: %s", N.GetErrorString(e));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+    memcpy(id128, &id, 128);
+    return PCA_OK;
+}
+
+pca_status pca_attach_nccl(pca_ctx* ctx, const void* id128, int32_t nranks, int32_t rank) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!id128 || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(PCA_EINVAL, "bad NCCL arguments");
+    if (ctx->comm) return fail(PCA_EINVAL, "NCCL already attached");
+    NcclApi& N = nccl();
+    if (!N.loaded) return fail(PCA_ENCCL, "%s", N.why.c_str());
+    ncclUniqueId id;
+    memcpy(&id, id128, 128);
+    ncclComm_t comm = nullptr;
+    ncclResult_t e = N.CommInitRank(&comm, nranks, id, rank);
+    if (e != ncclSuccess) return fail(PCA_ENCCL, "ncclCommInitRank: %s", N.GetErrorString(e));
+    ctx->comm = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    st = exchange(ctx, ctx->x[ctx->cur]);
+    if (st != PCA_OK) return st;
+    return sync(ctx);
+}
+
+pca_status pca_sync(pca_ctx* ctx) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    return sync(ctx);
+}
+
+pca_status pca_destroy(pca_ctx* ctx) {
+    if (!ctx) return PCA_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) nccl().CommDestroy(ctx->comm);
+    delete ctx;
+    return PCA_OK;
+}
+
+}  // extern "C"

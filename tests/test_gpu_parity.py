@@ -1,0 +1,325 @@
+"""-m gpu parity: the CUDA path (through the C ABI) vs the fp64 CPU oracle.
+
+Bar (BASELINE.json north star, R19): chains bit-exact; the only allowed differences are
+decision mismatches whose uniform lies within 1e-6 of an oracle cumulative probability,
+fewer than 1e-6 of all updates.  Integer outputs (MPM counts, MPM image) exact; PSNR within
+0.01 dB and SSIM within 1e-9 of the oracle's two-pass fp64 statistics.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2507_14869_b200 as P
+import synth
+from parity_helpers import Tally, beta_of, lockstep, make_ctx, oracle_model
+
+pytestmark = pytest.mark.gpu
+
+
+# (H, W, levels, nbhd, periodic): several tiles, ragged widths (not multiples of 16 / 4),
+# single rows / columns, and the paper's level counts.
+SHAPES = [
+    (64, 64, 2, 4, True), (64, 64, 2, 8, False), (37, 531, 2, 8, True), (19, 1000, 2, 4, False),
+    (1, 77, 2, 8, False), (77, 1, 2, 8, False), (3, 3, 2, 8, True), (5, 17, 2, 8, False),
+    (33, 47, 3, 8, False), (40, 130, 5, 8, False), (29, 61, 9, 4, True), (31, 45, 33, 8, False),
+    (9, 23, 255, 8, True), (2, 2, 3, 8, False), (1, 1, 5, 8, False),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("kernel", [P.KERNEL_AUTO, P.KERNEL_GENERAL])
+def test_lockstep_random_states(cuda_device, shape, kernel):
+    H, W, L, nb, per = shape
+    cfg = P.make_config(H, W, L, neighborhood=nb, periodic=per, sigma=0.3, beta0=0.9,
+                        beta_step=0.5, beta_period=2, seed=1234 + H * W, kernel=kernel)
+    g = synth.random_labels((H, W), L, seed=H * 1000 + W)
+    x0 = synth.random_labels((H, W), L, seed=W * 1000 + H)
+    ctx = make_ctx(cfg, g, x0)
+    tally = lockstep(ctx, cfg, 6)
+    tally.check(allow_rate=False)
+
+
+@pytest.mark.parametrize("q", [0.0, 0.51, 3.0, 1e6])
+def test_lockstep_inertia_extremes(cuda_device, q):
+    cfg = P.make_config(48, 80, 2, neighborhood=8, periodic=False, q=q, sigma=0.5, seed=7)
+    g = synth.smooth_labels(48, 80, 2, seed=3)
+    ctx = make_ctx(cfg, synth.degrade(g, 2, 0.5, 4))
+    lockstep(ctx, cfg, 5).check(allow_rate=False)
+    if q == 1e6:  # infinite inertia freezes the chain
+        assert np.array_equal(ctx.state()[0], ctx._g_host[0])
+
+
+def _c1_config(seed, kernel=P.KERNEL_AUTO):
+    # config 1 (BASELINE.json configs[0]): 64x64 binary, 4-neighbour torus, 200 sweeps,
+    # schedule 1.25 + 0.25 every 50 (the paper's compressed), MPM burn-in 100.
+    return P.make_config(64, 64, 2, neighborhood=4, periodic=True, sigma=0.5, beta0=1.25,
+                         beta_step=0.25, beta_period=50, seed=seed, mpm_burn_in=100,
+                         kernel=kernel)
+
+
+def _c1_inputs(seed):
+    m = orc.model(64, 64, 2, nbhd=4, periodic=True)
+    truth = orc.generate_mrf(m, 400, 0.9, 1.6, seed=seed)
+    return truth, orc.degrade(truth, 2, 0.5, seed=seed + 100)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config1_free_running_chain(cuda_device, seed):
+    """Free-running: GPU and oracle chains run independently for 200 sweeps; states,
+    MPM counts, MPM image and PSNR/SSIM must agree exactly."""
+    truth, g = _c1_inputs(seed)
+    cfg = _c1_config(seed)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_sweep(200)
+    m = oracle_model(cfg)
+    x_o, cnt_o = orc.pca_run(m, g, g, 200, 1.25, 0.25, 50, seed, burn_in=100)
+    assert np.array_equal(ctx.state()[0], x_o)
+    assert np.array_equal(ctx.counts()[0], cnt_o[1].astype(np.uint16))
+    mpm_o = orc.mpm(cnt_o)
+    assert np.array_equal(ctx.estimate(P.EST_MPM)[0], mpm_o)
+    for kind, est in [(P.EST_LAST, x_o), (P.EST_MPM, mpm_o)]:
+        psnr, ssim = ctx.pca_psnr_ssim(truth[None], kind)
+        _, p_o, s_o, _ = orc.metrics(truth, est, 2)
+        assert abs(psnr[0] - p_o) < 0.01 and abs(psnr[0] - p_o) < 1e-9
+        assert abs(ssim[0] - s_o) < 1e-9
+    marg = ctx.estimate(P.EST_MARGINALS)[0]
+    assert np.allclose(marg[1], cnt_o[1] / 100.0, atol=1e-6)
+    assert np.allclose(marg[0] + marg[1], 1.0, atol=1e-6)
+    st = ctx.pca_get_stats()
+    assert st.sweeps_done == 200 and st.counted_sweeps == 100 and st.kernel == P.KERNEL_BINARY
+
+
+def test_config1_binary_and_general_kernels_agree(cuda_device):
+    truth, g = _c1_inputs(9)
+    a = make_ctx(_c1_config(9, P.KERNEL_BINARY), g)
+    b = make_ctx(_c1_config(9, P.KERNEL_GENERAL), g)
+    a.pca_sweep(200)
+    b.pca_sweep(200)
+    assert np.array_equal(a.state(), b.state())
+    assert np.array_equal(a.counts(), b.counts())
+
+
+@pytest.mark.parametrize("levels,sigma,ramp,n", [(5, 0.25, (0.8, 1.5), 1000),
+                                                  (9, 0.20, (0.8, 1.85), 300),
+                                                  (33, 0.10, (1.0, 3.0), 120)])
+def test_config2_paper_protocol_lockstep(cuda_device, levels, sigma, ramp, n):
+    """Config 2: 256x256, Moore-8, free boundary, beta 1.25 + 0.25 every
+    250 sweeps, q = 0.51, x0 = g; lockstep vs the oracle (l = 5 for the full 1000 sweeps;
+    l = 9, 33 for a prefix to bound the oracle's time), then MPM / PSNR / SSIM exact."""
+    m = orc.model(256, 256, levels, nbhd=8, periodic=False)
+    truth = orc.generate_mrf(m, 150, ramp[0], ramp[1], seed=levels)
+    g = orc.degrade(truth, levels, sigma, seed=levels + 50)
+    burn = max(0, n - 250)
+    cfg = P.make_config(256, 256, levels, neighborhood=8, periodic=False, sigma=sigma,
+                        seed=2025 + levels, mpm_burn_in=burn)
+    ctx = make_ctx(cfg, g)
+    tally = lockstep(ctx, cfg, n)
+    tally.check()
+    x_o, cnt_o = orc.pca_run(oracle_model(cfg), g, g, n, 1.25, 0.25, 250, cfg.seed, burn_in=burn)
+    if tally.mismatches == 0:
+        assert np.array_equal(ctx.state()[0], x_o)
+        assert np.array_equal(ctx.counts()[0], cnt_o.astype(np.uint16))
+        for kind, est in [(P.EST_LAST, x_o), (P.EST_MPM, orc.mpm(cnt_o))]:
+            psnr, ssim = ctx.pca_psnr_ssim(truth[None], kind)
+            _, p_o, s_o, _ = orc.metrics(truth, est, levels)
+            assert abs(psnr[0] - p_o) < 1e-9 and abs(ssim[0] - s_o) < 1e-9
+        cm = ctx.estimate(P.EST_CM)[0]
+        ref = (np.arange(levels)[:, None, None] / (levels - 1) * cnt_o).sum(0) / (n - burn)
+        assert np.allclose(cm, ref, atol=1e-6)
+
+
+def test_batch_equals_independent_chains(cuda_device):
+    """Batch mode: chain b of a batch == a single-chain context with chain0 = b."""
+    B, H, W = 4, 40, 72
+    g = np.stack([synth.degrade(synth.smooth_labels(H, W, 5, s), 5, 0.25, s + 9) for s in range(B)])
+    cfg = P.make_config(H, W, 5, batch=B, sigma=0.25, seed=77, mpm_burn_in=10)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_sweep(25)
+    xs, cs = ctx.state(), ctx.counts()
+    for b in range(B):
+        c1 = P.make_config(H, W, 5, batch=1, sigma=0.25, seed=77, mpm_burn_in=10, chain0=b)
+        one = make_ctx(c1, g[b])
+        one.pca_sweep(25)
+        assert np.array_equal(one.state()[0], xs[b])
+        assert np.array_equal(one.counts()[0], cs[b])
+    t = lockstep(make_ctx(cfg, g), cfg, 3)
+    t.check(allow_rate=False)
+
+
+def _cudart_memcpy():
+    """cudaMemcpy (device to device) from the CUDA runtime torch loaded (test plumbing)."""
+    import ctypes
+    import glob
+    import os
+
+    import nvidia.cuda_runtime as cr
+
+    path = sorted(glob.glob(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so*")))[0]
+    rt = ctypes.CDLL(path)
+    rt.cudaMemcpy.restype = ctypes.c_int
+    rt.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+
+    def copy(dst, src, n):
+        assert rt.cudaMemcpy(dst, src, n, 3) == 0  # cudaMemcpyDeviceToDevice
+
+    return copy
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+@pytest.mark.parametrize("levels", [2, 5])
+def test_row_strips_with_loopback_halo_exchange(cuda_device, periodic, levels):
+    """Row-strip decomposition: P strip contexts on one GPU whose halo rows
+    are copied between them after every sweep reproduce the unsharded chain bit-exactly."""
+    import torch
+
+    memcpy_d2d = _cudart_memcpy()
+
+    H, W, Pn = 48, 100, 3
+    g = synth.degrade(synth.smooth_labels(H, W, levels, 5), levels, 0.3, 6)
+    base = dict(neighborhood=8, periodic=periodic, sigma=0.3, seed=99, mpm_burn_in=4)
+    full = make_ctx(P.make_config(H, W, levels, **base), g)
+    bounds = [0, 17, 30, 48]
+    strips = [make_ctx(P.make_config(H, W, levels, row0=bounds[i], rows=bounds[i + 1] - bounds[i],
+                                     **base), g[bounds[i]:bounds[i + 1]]) for i in range(Pn)]
+
+    def exchange():
+        torch.cuda.synchronize()
+        hs = [s.pca_halo_ptrs() for s in strips]
+        rb = hs[0].row_bytes
+        for i in range(Pn):
+            up, dn = i - 1, i + 1
+            if periodic:
+                up %= Pn
+                dn %= Pn
+            if 0 <= up < Pn:
+                memcpy_d2d(hs[i].recv_top, hs[up].send_bottom, rb)
+            if 0 <= dn < Pn:
+                memcpy_d2d(hs[i].recv_bottom, hs[dn].send_top, rb)
+        torch.cuda.synchronize()
+
+    exchange()
+    for _ in range(10):
+        for s in strips:
+            s.pca_sweep(1)
+        exchange()
+    full.pca_sweep(10)
+    got = np.concatenate([s.state()[0] for s in strips], axis=0)
+    assert np.array_equal(got, full.state()[0])
+    gc = np.concatenate([s.counts()[0] for s in strips], axis=-2)
+    assert np.array_equal(gc, full.counts()[0])
+    truth = synth.smooth_labels(H, W, levels, 5)
+    tot = sum(s.pca_metric_sums(truth[bounds[i]:bounds[i + 1]][None], P.EST_LAST)
+              for i, s in enumerate(strips))
+    ref = full.pca_metric_sums(truth[None], P.EST_LAST)
+    assert np.array_equal(tot[:, [0, 1, 2, 3, 4, 5, 7]], ref[:, [0, 1, 2, 3, 4, 5, 7]])
+
+
+def test_checkpoint_resume_is_bit_exact(cuda_device):
+    H, W = 50, 70
+    g = synth.degrade(synth.smooth_labels(H, W, 2, 8), 2, 0.5, 9)
+    cfg = P.make_config(H, W, 2, sigma=0.5, seed=5, mpm_burn_in=20, beta_period=15)
+    a = make_ctx(cfg, g)
+    a.pca_sweep(60)
+    b = make_ctx(cfg, g)
+    b.pca_sweep(35)
+    st, cnt, t = b.state(), b.counts(), b.pca_get_stats()
+    c = make_ctx(cfg, g)
+    c.pca_write_state(st)
+    c.pca_write_counts(cnt, t.counted_sweeps)
+    c.pca_set_step(t.sweeps_done)
+    c.pca_sweep(25)
+    assert np.array_equal(c.state(), a.state()) and np.array_equal(c.counts(), a.counts())
+
+
+def test_device_and_host_buffers_agree(cuda_device):
+    import torch
+
+    H, W = 33, 90
+    g = synth.random_labels((1, H, W), 3, 4)
+    cfg = P.make_config(H, W, 3, sigma=0.4, seed=3, mpm_burn_in=0)
+    a = make_ctx(cfg, g)
+    b = P.PcaContext(cfg, torch.from_numpy(g).cuda())
+    a.pca_sweep(7)
+    b.pca_sweep(7)
+    out = torch.empty((1, H, W), dtype=torch.uint8, device="cuda")
+    b.pca_estimate(P.EST_MPM, out)
+    assert np.array_equal(out.cpu().numpy(), a.estimate(P.EST_MPM))
+    assert np.array_equal(b.state(), a.state())
+
+
+def test_error_paths(cuda_device):
+    H, W = 16, 16
+    g = synth.random_labels((H, W), 2, 1)
+    bad = g.copy()
+    bad[3, 3] = 7
+    with pytest.raises(P.PcaError) as e:
+        make_ctx(P.make_config(H, W, 2), bad)
+    assert e.value.status == P.PCA_EINVAL
+    ctx = make_ctx(P.make_config(H, W, 2, mpm_burn_in=-1), g)
+    with pytest.raises(P.PcaError):
+        ctx.estimate(P.EST_MPM)
+    ctx.pca_sweep(0)
+    assert np.array_equal(ctx.state()[0], g)  # zero sweeps: final = initial
+    with pytest.raises(P.PcaError) as e:
+        ctx.pca_write_state(bad)
+    assert e.value.status == P.PCA_EINVAL
+    black = np.zeros((1, H, W), np.uint8)
+    with pytest.raises(P.PcaError):
+        ctx.pca_psnr_ssim(black, P.EST_LAST)
+    with pytest.raises(P.PcaError) as e:  # sigma so small that fp64 weights underflow
+        c2 = make_ctx(P.make_config(H, W, 2, sigma=0.01), g)
+        c2.pca_sweep(1)
+    assert e.value.status == P.PCA_EUNSUPPORTED
+
+
+def test_distribution_matches_exact_transition_powers(cuda_device):
+    """50000 independent 3x3 torus chains (batch mode) after T sweeps from a fixed x0: the
+    empirical state histogram matches delta_x0 P^T from exact enumeration (chi-square).
+    Independent of the C oracle: pins the CUDA sampler to the paper's transition law."""
+    from oracle import enumerate as en
+    from test_oracle_pins import _chi2_ok
+
+    B, T = 50000, 3
+    lat = en.Lattice(3, 3, 2, nbhd=4, periodic=True)
+    g = np.array([[0, 1, 0], [1, 1, 0], [0, 0, 1]], np.uint8)
+    cfg = P.make_config(3, 3, 2, batch=B, neighborhood=4, periodic=True, sigma=0.5, beta0=1.25,
+                        beta_step=0.0, seed=31337)
+    ctx = make_ctx(cfg, np.broadcast_to(g, (B, 3, 3)).copy())
+    ctx.pca_sweep(T)
+    xs = ctx.state().reshape(B, 9).astype(np.int64)
+    idx = (xs * (2 ** np.arange(8, -1, -1))).sum(1)
+    hist = np.bincount(idx, minlength=512).astype(float)
+    a, b, c = en.coefficients(1.25, 1 / 3, 0.51, 0.5)
+    Pm = en.pca_matrix(lat, g.reshape(-1), a, b, c)
+    row = np.zeros(512)
+    row[en.state_index(lat, g.reshape(-1))] = 1.0
+    for _ in range(T):
+        row = row @ Pm
+    ok, stat, crit = _chi2_ok(hist, row, B)
+    assert ok, (stat, crit)
+
+
+def test_full_size_sampled_rows(cuda_device):
+    """Bench configuration (config 3, 8192^2, l = 2, Moore-8 torus, MPM on): a few GPU sweeps,
+    then rows sampled across the lattice are recomputed by the oracle from the GPU's x_t."""
+    H = W = 8192
+    truth = synth.tiled_labels(H, W, 2, seed=1)
+    g = synth.degrade(truth, 2, 0.5, seed=2)
+    cfg = P.make_config(H, W, 2, neighborhood=8, periodic=True, sigma=0.5, beta0=1.5,
+                        beta_step=0.0, seed=11, mpm_burn_in=0)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_sweep(3)
+    x3 = ctx.state()[0]
+    ctx.pca_sweep(1)
+    x4 = ctx.state()[0]
+    m = oracle_model(cfg)
+    rows = sorted({0, 1, H - 1, H // 2} | set(np.random.default_rng(0).integers(0, H, 24).tolist()))
+    tally = Tally()
+    for r in rows:
+        ref, mg = orc.pca_sweep(m, x3, g, 1.5, cfg.seed, 0, 3, rows=(r, r + 1))
+        tally.add(x4[r], ref[0], mg[0])
+    tally.check()
+    c = ctx.counts()[0]
+    assert c.max() <= 4 and np.array_equal(c[rows[0]] >= 0, np.ones(W, bool))
