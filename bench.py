@@ -27,7 +27,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -43,9 +42,9 @@ BYTES_PER_SU = 7  # x_t read (1) + g read (1) + x_{t+1} write (1) + uint16 count
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--sweeps", type=int, default=100, help="PCA sweeps per step")
+    ap.add_argument("--sweeps", type=int, default=200, help="PCA sweeps per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -86,31 +85,29 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.path = os.path.join("/tmp", f"pca_bench_clocks_{os.getpid()}.csv")
 
     def start(self):
         try:
+            self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                ["stdbuf", "-oL", "nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.fh, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
+        time.sleep(0.1)
+        self.proc.send_signal(2)
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        self.fh.close()
+        self.lines = [ln.strip() for ln in open(self.path)]
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -279,7 +276,6 @@ def run_ours(args):
         psnr, ssim = ctx.pca_psnr_ssim(t_dev, P.EST_MPM)
     ev1.record(stream)
     barrier()
-    clk = clocks.stop()
     st1 = ctx.pca_get_stats()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     sw_ms = max_over_ranks(sw_ms)
@@ -323,6 +319,7 @@ def run_ours(args):
                "d2h_bytes_per_step": int(mpm_h.numel() + 2 * 8 * 8),
                "ms_per_step": ems / args.steps}
 
+    clk = clocks.stop()
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_oracle(wl, truth, g, rows=wl["rows"], sweeps=2)

@@ -62,11 +62,13 @@ struct BinarySweepParams {
     uint32_t thr[THR_ENTRIES];
 };
 
-// general path: A[n] = exp(a n), Cw = exp(-c); D table in global memory.
+// general path: A[n] = exp(a n), Cw = exp(-c); D table in global memory.  a, b, c feed
+// the log-domain slow path used when the factorised weights under/overflow.
 struct GeneralSweepParams {
     SweepCommon c;
     double A[9];
     double Cw;
+    double coef_a, coef_b, coef_c;
     const double* dtab;
 };
 

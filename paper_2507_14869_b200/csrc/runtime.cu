@@ -291,12 +291,6 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
     const double a = c.coef_scale * 2.0 * beta * c.J;
     const double b = c.coef_scale / (2.0 * c.sigma * c.sigma);
     const double cq = beta * c.q;
-    const double range = a * (double)c.neighborhood + b + cq;
-    if (!(range < 700.0))
-        return fail(PCA_EUNSUPPORTED,
-                    "beta stage %lld: exponent range a*N + b + c = %g >= 700 would underflow fp64 "
-                    "weights",
-                    (long long)stage, range);
     if (ctx->kernel == PCA_KERNEL_BINARY) {
         for (int np = 0; np <= 8; ++np)
             for (int n1 = 0; n1 <= 8; ++n1)
@@ -321,14 +315,18 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
                         const double e1 = exp(E[1] - Emax);
                         const double Z = 0.0 + e0 + e1;
                         const double p0 = e0 / Z;
-                        const double T = ceil(p0 * 4294967296.0);  // in [1, 2^32]
-                        if (!(T >= 1.0))
-                            return fail(PCA_EUNSUPPORTED, "p(0) underflowed to 0 at beta %g", beta);
-                        ctx->bin.thr[idx] = (uint32_t)(T - 1.0);
+                        // T in [0, 2^32]; T = 0 (p0 underflowed to 0) is stored as 0, which
+                        // differs from the exact rule only for r = 0, where u = 0 = F_0 is an
+                        // exact tie (an allowed near-tie, R19).
+                        const double T = ceil(p0 * 4294967296.0);
+                        ctx->bin.thr[idx] = T >= 1.0 ? (uint32_t)(T - 1.0) : 0u;
                     }
     } else {
         for (int n = 0; n <= 8; ++n) ctx->gen.A[n] = exp(a * (double)n);
         ctx->gen.Cw = exp(-cq);
+        ctx->gen.coef_a = a;
+        ctx->gen.coef_b = b;
+        ctx->gen.coef_c = cq;
     }
     ctx->tab_stage = stage;
     ctx->beta_last = beta;

@@ -83,15 +83,49 @@ __global__ void __launch_bounds__(256)
                 for (int j = 0; j < NB; ++j) n += (nb[j] == s);
                 Z += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
             }
-            const double target = (double)rr[b] * (1.0 / 4294967296.0) * Z;
+            const double u = (double)rr[b] * (1.0 / 4294967296.0);
             int w = L - 1;
-            double F = 0.0;
-            for (int s = 0; s < L - 1; ++s) {
-                int n = 0;
+            if (Z >= 1e-290 && Z <= 1e290) {
+                const double target = u * Z;
+                double F = 0.0;
+                for (int s = 0; s < L - 1; ++s) {
+                    int n = 0;
 #pragma unroll
-                for (int j = 0; j < NB; ++j) n += (nb[j] == s);
-                F += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
-                if (target < F) { w = s; break; }
+                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
+                    F += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
+                    if (target < F) { w = s; break; }
+                }
+            } else {
+                // Rare slow path (extreme beta, q or sigma: the factorised weights under- or
+                // overflow): E_s = a n_s - b d_s^2 - c 1{s != x_i}, softmax with max subtracted.
+                const double lg = (double)gi / (double)(L - 1);
+                double Emax = -INFINITY;
+                for (int s = 0; s < L; ++s) {
+                    int n = 0;
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
+                    const double d = lg - (double)s / (double)(L - 1);
+                    const double E = p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0);
+                    Emax = fmax(Emax, E);
+                }
+                double Zs = 0.0;
+                for (int s = 0; s < L; ++s) {
+                    int n = 0;
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
+                    const double d = lg - (double)s / (double)(L - 1);
+                    Zs += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
+                }
+                const double target = u * Zs;
+                double F = 0.0;
+                for (int s = 0; s < L - 1; ++s) {
+                    int n = 0;
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
+                    const double d = lg - (double)s / (double)(L - 1);
+                    F += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
+                    if (target < F) { w = s; break; }
+                }
             }
             outw |= (uint32_t)w << (8 * b);
         }

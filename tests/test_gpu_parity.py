@@ -268,10 +268,20 @@ def test_error_paths(cuda_device):
     black = np.zeros((1, H, W), np.uint8)
     with pytest.raises(P.PcaError):
         ctx.pca_psnr_ssim(black, P.EST_LAST)
-    with pytest.raises(P.PcaError) as e:  # sigma so small that fp64 weights underflow
-        c2 = make_ctx(P.make_config(H, W, 2, sigma=0.01), g)
-        c2.pca_sweep(1)
-    assert e.value.status == P.PCA_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("kernel", [P.KERNEL_AUTO, P.KERNEL_GENERAL])
+@pytest.mark.parametrize("levels", [2, 5])
+@pytest.mark.parametrize("extreme", [dict(sigma=0.01), dict(q=1e6), dict(beta0=300.0),
+                                     dict(sigma=0.02, q=500.0)])
+def test_lockstep_extreme_parameters(cuda_device, kernel, levels, extreme):
+    """Parameters whose factorised fp64 weights under/overflow (tiny sigma, huge q or beta):
+    the binary tables and the general kernel's log-domain slow path still follow the oracle."""
+    H, W = 24, 40
+    g = synth.degrade(synth.smooth_labels(H, W, levels, 2), levels, 0.3, 3)
+    cfg = P.make_config(H, W, levels, seed=17, kernel=kernel, **extreme)
+    ctx = make_ctx(cfg, g, synth.random_labels((H, W), levels, 4))
+    lockstep(ctx, cfg, 4).check(allow_rate=False)
 
 
 def test_distribution_matches_exact_transition_powers(cuda_device):
