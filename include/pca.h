@@ -101,7 +101,7 @@ typedef struct pca_config {
     int32_t row0;          /* first global row owned by this context (sharding), >= 0         */
     int32_t rows;          /* owned rows; 0 means all H rows (row0 must then be 0)            */
     int32_t kernel;        /* PCA_KERNEL_*                                                     */
-    int32_t rows_per_thread; /* binary kernel register-blocking depth; 0 = library default    */
+    int32_t rows_per_thread; /* binary kernel: rows per warp task; 0 = auto (one wave)       */
     int32_t reserved[7];   /* must be zero                                                     */
 } pca_config;
 

@@ -132,8 +132,8 @@ pca_status validate(const pca_config* c) {
     if (c->kernel == PCA_KERNEL_BINARY && c->levels != 2)
         return fail(PCA_EUNSUPPORTED, "the binary kernel needs levels == 2");
     const int R = c->rows_per_thread;
-    if (!(R == 0 || R == 1 || R == 2 || R == 4 || R == 8 || R == 16 || R == 32))
-        return fail(PCA_EINVAL, "rows_per_thread must be 0 or a power of two <= 32");
+    if (R < 0 || R > 65536)
+        return fail(PCA_EINVAL, "rows_per_thread must be in [0, 65536] (0 = auto)");
     for (int i = 0; i < 7; ++i)
         if (c->reserved[i] != 0) return fail(PCA_EINVAL, "reserved fields must be zero");
     return PCA_OK;
@@ -413,8 +413,11 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
         pca_status st = check_flag(ctx, "g");
         if (st != PCA_OK) return st;
     }
-    CK(ctx, cudaMemsetAsync(ctx->x[0], 0xFF, L.xbuf, ctx->stream));
-    CK(ctx, cudaMemsetAsync(ctx->x[1], 0xFF, L.xbuf, ctx->stream));
+    // free boundary: halos and padding hold the sentinel 0xFF; torus: halos are rewritten by
+    // every sweep and padding is 0 (a valid label, so SWAR sums need no masking)
+    const int fill = c.periodic ? 0 : 0xFF;
+    CK(ctx, cudaMemsetAsync(ctx->x[0], fill, L.xbuf, ctx->stream));
+    CK(ctx, cudaMemsetAsync(ctx->x[1], fill, L.xbuf, ctx->stream));
     CK(ctx, cudaMemsetAsync(ctx->counts, 0, L.counts_bytes, ctx->stream));
     ctx->cur = 0;
     ctx->t = 0;
@@ -477,7 +480,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->kernel = (cfg->kernel == PCA_KERNEL_AUTO) ? (cfg->levels == 2 ? PCA_KERNEL_BINARY
                                                                        : PCA_KERNEL_GENERAL)
                                                    : cfg->kernel;
-    ctx->rows_per_thread = cfg->rows_per_thread ? cfg->rows_per_thread : 8;
+    ctx->rows_per_thread = cfg->rows_per_thread;
 
     Geometry& G = ctx->geo;
     G.W = cfg->width;

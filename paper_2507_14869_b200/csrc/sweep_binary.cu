@@ -9,12 +9,17 @@
 // (324 entries) and the device decision is the integer compare r > T - 1 on the Philox
 // word r (u = r 2^-32): bit-exact with the fp64 oracle whenever the host's p0 equals it.
 //
-// Data path per thread: a 16-site row chunk (one 16-byte vector of x, g and the uint16
-// counts' 32 bytes) for `R` consecutive rows, walking down with a rolling 3-row window
-// in registers.  Neighbour counts are SWAR byte sums: vertical sum of the 3 rows, then
-// left/right byte shifts with funnel shifts; the words left/right of the chunk come from
-// the adjacent lanes by warp shuffle (lanes 0 and 31 load them).  One Philox4x32-10 call
-// serves 4 sites.  MPM counts of label 1 are updated in the same pass (R15).
+// Data movement (Blackwell-native): every warp owns a 512-column segment (16 sites per
+// lane) of a run of R rows and streams it through a private K-stage shared-memory ring
+// filled by 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on per-stage
+// mbarriers.  A stage holds one padded x row (544 B incl. the words left/right of the
+// segment), one g row (512 B) and one row of uint16 MPM counts (1 KiB), so the warp keeps
+// K-1 rows of loads in flight without spending registers.  The 3-row neighbourhood window
+// lives in registers; neighbour counts are SWAR byte sums
+// (vertical sum of 3 rows, then funnel-shifted left/right sums); the table index of each
+// site is one byte of a pre-scaled SWAR word, extracted with one PRMT.  One Philox4x32-10
+// call serves 4 sites.  The MPM count of label 1 (uint16) is updated in the same pass (R15)
+// and stored with x_{t+1}.
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -22,39 +27,84 @@
 namespace pcab200 {
 namespace {
 
-constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int KSTAGES = 4;                             // ring depth per warp (power of two)
+constexpr int MIN_CTAS = 22;                           // resident one-warp CTAs per SM
+constexpr int SEG_CHUNKS = 32;                         // 16-site chunks per warp segment
+constexpr int XROW_BYTES = 16 * SEG_CHUNKS + 32;       // 544: [col0-16, col0+528)
+constexpr int GROW_BYTES = 16 * SEG_CHUNKS;            // 512
+constexpr int CROW_BYTES = 32 * SEG_CHUNKS;            // 1024
+constexpr int STAGE_BYTES = XROW_BYTES + GROW_BYTES + CROW_BYTES;  // 2080
+constexpr int THR_BYTES = THR_ENTRIES * 4;             // 1296
 
-// Map label bytes to {0,1}: 0 -> 0, 1 -> 1, sentinel 0xFF -> 0 (b & ~(b >> 1) & 1).
+constexpr int align16(int v) { return (v + 15) & ~15; }
+constexpr int RING_OFFSET = align16(KSTAGES * 8);      // mbarriers first, then the ring
+constexpr int SMEM_BYTES = RING_OFFSET + KSTAGES * STAGE_BYTES;  // dynamic smem per CTA
+
+// ---- PTX wrappers: mbarrier + 1-D bulk copy global -> shared ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(pred));
+    return pred != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Map label bytes to {0,1}: 0 -> 0, 1 -> 1, free-boundary sentinel 0xFF -> 0.
 __device__ __forceinline__ uint32_t to01(uint32_t w) { return w & ~(w >> 1) & 0x01010101u; }
-
-__device__ __forceinline__ uint4 ldg16(const uint8_t* p) {
-    return __ldg(reinterpret_cast<const uint4*>(p));
-}
-__device__ __forceinline__ uint32_t ldg4(const uint8_t* p) {
-    return __ldg(reinterpret_cast<const uint32_t*>(p));
-}
-
-// bytes shifted one column right (byte j <- byte j-1 of the 8-byte window lo:hi)
+// bytes shifted one column right (byte j <- byte j-1 of lo:hi) / left (byte j <- byte j+1)
 __device__ __forceinline__ uint32_t from_left(uint32_t lo, uint32_t hi) {
     return __funnelshift_l(lo, hi, 8);
 }
-// bytes shifted one column left (byte j <- byte j+1)
 __device__ __forceinline__ uint32_t from_right(uint32_t lo, uint32_t hi) {
     return __funnelshift_r(lo, hi, 8);
 }
-
+// byte j (0..15, run-time) of the 16-byte chunk o, without a local-memory array copy
+__device__ __forceinline__ uint8_t out_byte(const uint32_t (&o)[4], int j) {
+    const uint32_t w = (j < 8) ? ((j < 4) ? o[0] : o[1]) : ((j < 12) ? o[2] : o[3]);
+    return (uint8_t)(w >> (8 * (j & 3)));
+}
 __device__ __forceinline__ void store_chunk(uint8_t* op, const uint32_t (&o)[4], int nvalid) {
     if (nvalid >= 16) {
         *reinterpret_cast<uint4*>(op) = make_uint4(o[0], o[1], o[2], o[3]);
     } else {
-        for (int j = 0; j < nvalid; ++j) op[j] = (uint8_t)(o[j >> 2] >> (8 * (j & 3)));
+        for (int j = 0; j < nvalid; ++j) op[j] = out_byte(o, j);
     }
 }
-
-__device__ __forceinline__ uint8_t out_byte(const uint32_t (&o)[4], int j) {
-    return (uint8_t)(o[j >> 2] >> (8 * (j & 3)));
-}
-
 template <int NB>
 __device__ __forceinline__ int neighbours_present(int grow, int H, int c, int W) {
     const int er = (grow == 0) + (grow == H - 1);
@@ -62,162 +112,232 @@ __device__ __forceinline__ int neighbours_present(int grow, int H, int c, int W)
     return NB == 8 ? (3 - er) * (3 - ec) - 1 : 4 - er - ec;
 }
 
-template <int R, int NB>
-__global__ void __launch_bounds__(128)
-    sweep_binary_kernel(const __grid_constant__ BinarySweepParams p) {
-    __shared__ uint32_t s_thr[THR_ENTRIES];
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    for (int i = tid; i < THR_ENTRIES; i += 128) s_thr[i] = p.thr[i];
-    __syncthreads();
+struct XRow {
+    uint32_t w[4];  // the lane's 16 labels
+    uint32_t l, r;  // the words left / right of the chunk
+};
+
+// One warp per CTA: every per-warp quantity (segment, row range, stage addresses) derives
+// from blockIdx and kernel parameters only, so the compiler keeps it in uniform registers and
+// the bulk-copy issue needs no per-lane address handling.
+template <int NB, bool PER>
+__global__ void __launch_bounds__(32, MIN_CTAS)
+    sweep_binary_kernel(const __grid_constant__ BinarySweepParams p, int R) {
+    __shared__ __align__(16) uint32_t s_thr[THR_ENTRIES];  // static: LDS [reg + imm]
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    uint8_t* ring = smem + RING_OFFSET;
+    const int lane = threadIdx.x;
+    for (int i = lane; i < THR_ENTRIES; i += 32) s_thr[i] = p.thr[i];
+    if (lane == 0) {
+        for (int s = 0; s < KSTAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
 
     const Geometry& G = p.c.geo;
-    const int lane = threadIdx.x;
-    const int k = blockIdx.x * 32 + lane;  // 16-site chunk index
+    const int seg = blockIdx.x;
     const int chain = blockIdx.z;
-    const int rbeg = (blockIdx.y * 4 + threadIdx.y) * R;
-    if (rbeg >= G.rows) return;  // warp-uniform
+    const int rbeg = blockIdx.y * R;
     const int rend = min(rbeg + R, G.rows);
-    const bool has_chunk = k <= G.nchunks;  // chunk nchunks is readable padding
-    const bool active = k < G.nchunks;
-    const int col0 = 16 * k;
-    const uint8_t* xin = p.c.x_in + chain * G.xchain + XOFF + col0;
-    const uint8_t* gin = p.c.g + chain * G.gchain + col0;
-    uint8_t* xout = p.c.x_out + chain * G.xchain + XOFF + col0;
-    uint16_t* cnt = p.c.counts + chain * G.cchain + col0;
+    if (rbeg >= rend) return;
+    const int nitems = rend - rbeg + 2;  // x rows rbeg-1 .. rend
+    const int nch = min(SEG_CHUNKS, G.nchunks - seg * SEG_CHUNKS);
+    const int col0 = 16 * SEG_CHUNKS * seg;
+    const int k = seg * SEG_CHUNKS + lane;  // this lane's chunk
+    const bool active = lane < nch;
+    const int ccol = col0 + 16 * lane;      // first column of the chunk
+    const uint32_t xbytes = 16 * nch + 32, gbytes = 16 * nch;
+    const uint32_t cbytes = p.c.count_enable ? 32 * nch : 0;
+    // padded x row j (-1..rows) starts at (j+1)*xpitch; byte col0 of it is column col0-16
+    const uint8_t* xin = p.c.x_in + chain * G.xchain + col0 + (long long)rbeg * G.xpitch;
+    const uint8_t* gin = p.c.g + chain * G.gchain + col0 + (long long)rbeg * G.gpitch;
+    uint16_t* cnt_issue = p.c.counts + chain * G.cchain + col0 + (long long)rbeg * G.cpitch;
+    uint8_t* xo = p.c.x_out + chain * G.xchain + XOFF + ccol + (long long)(rbeg + 1) * G.xpitch;
+    uint16_t* co = p.c.counts + chain * G.cchain + ccol + (long long)rbeg * G.cpitch;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
-    const bool col_edge = !G.periodic && (k == 0 || k == G.nchunks - 1);
+    const uint8_t* thr_b = reinterpret_cast<const uint8_t*>(s_thr);
 
-    auto load = [&](int r, uint32_t(&w)[4], uint32_t& e) {
-        const uint8_t* rp = xin + (long long)(r + 1) * G.xpitch;
-        if (has_chunk) {
-            const uint4 v = ldg16(rp);
-            w[0] = to01(v.x); w[1] = to01(v.y); w[2] = to01(v.z); w[3] = to01(v.w);
-        } else {
-            w[0] = w[1] = w[2] = w[3] = 0u;
+    // lane 0: load item `it` (x row rbeg-1+it; g / counts row rbeg+it-2 when it >= 2)
+    auto issue = [&](int it) {
+        const int s = it & (KSTAGES - 1);
+        uint8_t* st = ring + s * STAGE_BYTES;
+        const bool gc = it >= 2;
+        mbar_expect_tx(&bars[s], xbytes + (gc ? gbytes + cbytes : 0u));
+        bulk_g2s(st, xin + (long long)it * G.xpitch, xbytes, &bars[s]);
+        if (gc) {
+            bulk_g2s(st + XROW_BYTES, gin + (long long)(it - 2) * G.gpitch, gbytes, &bars[s]);
+            if (cbytes)
+                bulk_g2s(st + XROW_BYTES + GROW_BYTES, cnt_issue + (long long)(it - 2) * G.cpitch,
+                         cbytes, &bars[s]);
         }
-        e = 0u;
-        if (lane == 0) e = to01(ldg4(rp - 4));
-        else if (lane == 31 && active) e = to01(ldg4(rp + 16));
+    };
+    if (elect_one())
+        for (int it = 0; it < min(KSTAGES, nitems); ++it) issue(it);
+
+    // wait for item `it` and copy its x row into registers
+    auto fetch = [&](int it, XRow& x) {
+        const int s = it & (KSTAGES - 1);
+        mbar_wait(&bars[s], (uint32_t)((it / KSTAGES) & 1));
+        const uint8_t* st = ring + s * STAGE_BYTES;
+        const uint4 xv = *reinterpret_cast<const uint4*>(st + 16 + 16 * lane);
+        x.l = *reinterpret_cast<const uint32_t*>(st + 12 + 16 * lane);
+        x.r = *reinterpret_cast<const uint32_t*>(st + 32 + 16 * lane);
+        x.w[0] = xv.x; x.w[1] = xv.y; x.w[2] = xv.z; x.w[3] = xv.w;
+        if (!PER) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x.w[i] = to01(x.w[i]);
+            x.l = to01(x.l);
+            x.r = to01(x.r);
+        }
+    };
+    // every lane is done with item `it`'s stage: refill it with item it + KSTAGES
+    auto release = [&](int it) {
+        __syncwarp();
+        if (it + KSTAGES < nitems && elect_one()) {
+            fence_proxy_async();
+            issue(it + KSTAGES);
+        }
     };
 
-    uint32_t U[4], M[4], D[4], eU, eM, eD;
-    load(rbeg - 1, U, eU);
-    load(rbeg, M, eM);
-    for (int r = rbeg; r < rend; ++r) {
-        load(r + 1, D, eD);
+    // update local row r from the window (U = row r-1, M = row r, D = row r+1)
+    // (its g row and counts row are read straight from item `it`'s stage)
+    auto update = [&](int it, const XRow& U, const XRow& M, const XRow& D) {
+        if (!active) return;  // lanes past the last chunk of a partial segment hold no data
+        const int r = rbeg + it - 2;
         const int grow = G.row0 + r;
-        uint32_t Gw[4] = {0u, 0u, 0u, 0u};
-        if (has_chunk) {
-            const uint4 v = ldg16(gin + (long long)r * G.gpitch);
-            Gw[0] = v.x; Gw[1] = v.y; Gw[2] = v.z; Gw[3] = v.w;
-        }
+        const uint8_t* st = ring + (it & (KSTAGES - 1)) * STAGE_BYTES;
+        const uint4 gv = *reinterpret_cast<const uint4*>(st + XROW_BYTES + 16 * lane);
         // ---- n_i(1): SWAR neighbour counts, one byte per site ----
         uint32_t S[4];
         if (NB == 8) {
             uint32_t V[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) V[i] = U[i] + M[i] + D[i];
-            uint32_t VL = __shfl_up_sync(FULL, V[3], 1);
-            uint32_t VR = __shfl_down_sync(FULL, V[0], 1);
-            if (lane == 0) VL = eU + eM + eD;
-            if (lane == 31) VR = eU + eM + eD;
-            S[0] = from_left(VL, V[0]) + V[0] + from_right(V[0], V[1]) - M[0];
-            S[1] = from_left(V[0], V[1]) + V[1] + from_right(V[1], V[2]) - M[1];
-            S[2] = from_left(V[1], V[2]) + V[2] + from_right(V[2], V[3]) - M[2];
-            S[3] = from_left(V[2], V[3]) + V[3] + from_right(V[3], VR) - M[3];
+            for (int i = 0; i < 4; ++i) V[i] = U.w[i] + M.w[i] + D.w[i];
+            const uint32_t VL = U.l + M.l + D.l, VR = U.r + M.r + D.r;
+            S[0] = from_left(VL, V[0]) + V[0] + from_right(V[0], V[1]) - M.w[0];
+            S[1] = from_left(V[0], V[1]) + V[1] + from_right(V[1], V[2]) - M.w[1];
+            S[2] = from_left(V[1], V[2]) + V[2] + from_right(V[2], V[3]) - M.w[2];
+            S[3] = from_left(V[2], V[3]) + V[3] + from_right(V[3], VR) - M.w[3];
         } else {
-            uint32_t ML = __shfl_up_sync(FULL, M[3], 1);
-            uint32_t MR = __shfl_down_sync(FULL, M[0], 1);
-            if (lane == 0) ML = eM;
-            if (lane == 31) MR = eM;
-            S[0] = U[0] + D[0] + from_left(ML, M[0]) + from_right(M[0], M[1]);
-            S[1] = U[1] + D[1] + from_left(M[0], M[1]) + from_right(M[1], M[2]);
-            S[2] = U[2] + D[2] + from_left(M[1], M[2]) + from_right(M[2], M[3]);
-            S[3] = U[3] + D[3] + from_left(M[2], M[3]) + from_right(M[3], MR);
+            S[0] = U.w[0] + D.w[0] + from_left(M.l, M.w[0]) + from_right(M.w[0], M.w[1]);
+            S[1] = U.w[1] + D.w[1] + from_left(M.w[0], M.w[1]) + from_right(M.w[1], M.w[2]);
+            S[2] = U.w[2] + D.w[2] + from_left(M.w[1], M.w[2]) + from_right(M.w[2], M.w[3]);
+            S[3] = U.w[3] + D.w[3] + from_left(M.w[2], M.w[3]) + from_right(M.w[3], M.r);
         }
-        // table index byte = n1*4 + g*2 + x  (+ np*36 added per site)
-        uint32_t IDX[4];
+        // byte offset into the threshold table: 4 * (n1*4 + g*2 + x) <= 140, one byte per site
+        const uint32_t Gw[4] = {gv.x, gv.y, gv.z, gv.w};
+        uint32_t IDX4[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) IDX[i] = (S[i] << 2) | (Gw[i] << 1) | M[i];
-        const bool edge = col_edge || (!G.periodic && (grow == 0 || grow == G.H - 1));
+        for (int i = 0; i < 4; ++i) IDX4[i] = (S[i] << 4) | (Gw[i] << 3) | (M.w[i] << 2);
+        const bool edge = !PER && (k == 0 || k == G.nchunks - 1 || grow == 0 || grow == G.H - 1);
 
         // ---- Philox (one call per 4 sites) + integer-threshold decisions ----
         uint32_t O[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const uint4 rnd =
-                philox4x32_10(make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain),
-                              p.c.keys);
-            const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+            const uint4 rnd = philox4x32_10(
+                make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+            const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
             uint32_t o = 0u;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                uint32_t idx = (IDX[i] >> (8 * b)) & 0xFFu;
-                int np = NB;
-                if (edge) np = neighbours_present<NB>(grow, G.H, col0 + 4 * i + b, G.W);
-                idx += (uint32_t)np * 36u;
-                o |= (rr[b] > s_thr[idx] ? 1u : 0u) << (8 * b);
+                uint32_t off = __byte_perm(IDX4[i], 0u, 0x4440 + b);
+                if (PER) {
+                    off += NB * 36 * 4;
+                } else {
+                    const int np = edge ? neighbours_present<NB>(grow, G.H, ccol + 4 * i + b, G.W) : NB;
+                    off += (uint32_t)np * 144u;
+                }
+                const uint32_t T = *reinterpret_cast<const uint32_t*>(thr_b + off);
+                if (rw[b] > T) o += 1u << (8 * b);
             }
             O[i] = o;
         }
-
-        if (active) {
-            // ---- fused MPM counts of label 1 (uint16 per site) ----
-            if (p.c.count_enable) {
-                uint4* cp = reinterpret_cast<uint4*>(cnt + (long long)r * G.cpitch);
-                uint4 c0 = cp[0], c1 = cp[1];
-                c0.x += __byte_perm(O[0], 0u, 0x4140); c0.y += __byte_perm(O[0], 0u, 0x4342);
-                c0.z += __byte_perm(O[1], 0u, 0x4140); c0.w += __byte_perm(O[1], 0u, 0x4342);
-                c1.x += __byte_perm(O[2], 0u, 0x4140); c1.y += __byte_perm(O[2], 0u, 0x4342);
-                c1.z += __byte_perm(O[3], 0u, 0x4140); c1.w += __byte_perm(O[3], 0u, 0x4342);
-                cp[0] = c0;
-                cp[1] = c1;
-            }
-            // ---- store x_{t+1} (+ torus halos) ----
-            const int nvalid = G.W - col0;
-            uint8_t* op = xout + (long long)(r + 1) * G.xpitch;
-            store_chunk(op, O, nvalid);
-            if (G.periodic) {
-                if (k == 0) op[G.W] = out_byte(O, 0);                       // right halo
-                if (k == G.nchunks - 1) op[-col0 - 1] = out_byte(O, G.W - 1 - col0);  // left halo
-                if (G.self_halo_rows && (grow == 0 || grow == G.H - 1)) {
-                    uint8_t* hp = op + (grow == 0 ? 1LL : -1LL) * (long long)G.rows * G.xpitch;
-                    store_chunk(hp, O, nvalid);
-                    if (k == 0) hp[G.W] = out_byte(O, 0);
-                    if (k == G.nchunks - 1) hp[-col0 - 1] = out_byte(O, G.W - 1 - col0);
-                }
+        // ---- fused MPM counts of label 1 (uint16 per site) ----
+        if (cbytes) {
+            const uint4* cs = reinterpret_cast<const uint4*>(st + XROW_BYTES + GROW_BYTES + 32 * lane);
+            uint4 c0 = cs[0], c1 = cs[1];
+            c0.x += __byte_perm(O[0], 0u, 0x4140); c0.y += __byte_perm(O[0], 0u, 0x4342);
+            c0.z += __byte_perm(O[1], 0u, 0x4140); c0.w += __byte_perm(O[1], 0u, 0x4342);
+            c1.x += __byte_perm(O[2], 0u, 0x4140); c1.y += __byte_perm(O[2], 0u, 0x4342);
+            c1.z += __byte_perm(O[3], 0u, 0x4140); c1.w += __byte_perm(O[3], 0u, 0x4342);
+            uint4* cp = reinterpret_cast<uint4*>(co + (long long)(r - rbeg) * G.cpitch);
+            cp[0] = c0;
+            cp[1] = c1;
+        }
+        // ---- store x_{t+1} (+ torus halos) ----
+        const int nvalid = G.W - ccol;
+        uint8_t* op = xo + (long long)(r - rbeg) * G.xpitch;
+        store_chunk(op, O, nvalid);
+        if (PER) {
+            if (k == 0) op[G.W] = out_byte(O, 0);                                  // right halo
+            if (k == G.nchunks - 1) op[-ccol - 1] = out_byte(O, G.W - 1 - ccol);  // left halo
+            if (G.self_halo_rows && (grow == 0 || grow == G.H - 1)) {
+                uint8_t* hp = op + (grow == 0 ? 1LL : -1LL) * (long long)G.rows * G.xpitch;
+                store_chunk(hp, O, nvalid);
+                if (k == 0) hp[G.W] = out_byte(O, 0);
+                if (k == G.nchunks - 1) hp[-ccol - 1] = out_byte(O, G.W - 1 - ccol);
             }
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { U[i] = M[i]; M[i] = D[i]; }
-        eU = eM;
-        eM = eD;
+    };
+
+    // 3-row window U (row r-1), M (row r), D (row r+1)
+    XRow U, M, D;
+    fetch(0, M);
+    release(0);
+    fetch(1, D);
+    release(1);
+    for (int it = 2; it < nitems; ++it) {
+        U = M;
+        M = D;
+        fetch(it, D);
+        update(it, U, M, D);
+        release(it);
     }
 }
 
-template <int R>
-int launch_r(const BinarySweepParams& p, int batch, cudaStream_t s) {
+template <int NB, bool PER>
+int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     const Geometry& G = p.c.geo;
-    dim3 block(32, 4, 1);
-    dim3 grid((G.nchunks + 31) / 32, (G.rows + 4 * R - 1) / (4 * R), batch);
-    if (G.nbhd == 8) sweep_binary_kernel<R, 8><<<grid, block, 0, s>>>(p);
-    else sweep_binary_kernel<R, 4><<<grid, block, 0, s>>>(p);
+    static bool configured = false;
+    static int occ = 0, sms = 0;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (e != cudaSuccess) return (int)e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_binary_kernel<NB, PER>, 32,
+                                                      SMEM_BYTES);
+        if (occ < 1) occ = 1;
+        configured = true;
+    }
+    if (R <= 0) {
+        // size R so the grid is about one full wave of resident warps: every warp walks one
+        // contiguous run of rows with its pipeline primed once
+        const long long segs = (G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
+        const long long target = (long long)sms * occ;
+        const long long work = (long long)G.rows * segs * batch;
+        R = (int)((work + target - 1) / target);
+        if (R < 2) R = 2;
+    }
+    const int nrb = (G.rows + R - 1) / R;
+    if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
+    dim3 grid((G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS, nrb, batch);
+    sweep_binary_kernel<NB, PER><<<grid, 32, SMEM_BYTES, s>>>(p, R);
     return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread,
-                        void* stream) {
+int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    switch (rows_per_thread) {
-        case 1: return launch_r<1>(p, batch, s);
-        case 2: return launch_r<2>(p, batch, s);
-        case 4: return launch_r<4>(p, batch, s);
-        case 16: return launch_r<16>(p, batch, s);
-        case 32: return launch_r<32>(p, batch, s);
-        default: return launch_r<8>(p, batch, s);
-    }
+    const int R = rows_per_thread;  // 0 = auto (one wave)
+    if (p.c.geo.nbhd == 8)
+        return p.c.geo.periodic ? launch_t<8, true>(p, batch, R, s) : launch_t<8, false>(p, batch, R, s);
+    return p.c.geo.periodic ? launch_t<4, true>(p, batch, R, s) : launch_t<4, false>(p, batch, R, s);
 }
 
 }  // namespace pcab200
