@@ -7,6 +7,10 @@
 //  * metric_sums: one pass over truth and the LAST or MPM estimate, accumulating the exact
 //    integer sums of PAPER.md:516-534's statistics (sum (x-y)^2, sum x, sum y, sum x^2,
 //    sum y^2, sum xy, max x) per chain; block reduction, then one atomic per block per sum.
+//
+// All of them move 16 sites per thread with 16-byte vector accesses when the rows are
+// 16-byte aligned (W % 16 == 0), and fall back to per-byte access otherwise.  Grid: x over
+// 16-site chunks of a row, y over rows (grid-stride), z over chains.
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -14,70 +18,137 @@
 namespace pcab200 {
 namespace {
 
-__global__ void pack_state_kernel(Geometry G, const uint8_t* __restrict__ dense, int src_pitch,
-                                  long long src_chain, uint8_t* __restrict__ xbuf, int* bad) {
-    const int chain = blockIdx.z;
-    const uint8_t* src = dense + chain * src_chain;
-    for (int pr = (int)blockIdx.y - 1; pr <= G.rows; pr += gridDim.y) {  // padded row -1..rows
-        uint8_t* dst = xbuf + chain * G.xchain + (long long)(pr + 1) * G.xpitch + XOFF;
-        int sr = pr;
-        if (pr < 0 || pr >= G.rows) {
-            if (!(G.periodic && G.self_halo_rows)) continue;
-            sr = pr < 0 ? G.rows - 1 : 0;
-        }
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x - 1; c <= G.W;
-             c += gridDim.x * blockDim.x) {
-            int sc = c;
-            if (c < 0 || c >= G.W) {
-                if (!G.periodic) continue;
-                sc = c < 0 ? G.W - 1 : 0;
-            }
-            const uint8_t v = src[(long long)sr * src_pitch + sc];
-            if (v >= G.levels) atomicOr(bad, 1);
-            dst[c] = v;
-        }
-    }
+constexpr int TPB = 128;
+
+// any byte of w >= lv (levels replicated in every byte)?
+__device__ __forceinline__ bool any_ge(uint32_t w, uint32_t lv4) { return __vcmpgeu4(w, lv4) != 0; }
+
+__device__ __forceinline__ uint32_t byte_of(const uint4& v, int j) {
+    const uint32_t w = (j < 8) ? ((j < 4) ? v.x : v.y) : ((j < 12) ? v.z : v.w);
+    return (w >> (8 * (j & 3))) & 0xFFu;
 }
 
-__global__ void unpack_state_kernel(Geometry G, const uint8_t* __restrict__ xbuf,
-                                    uint8_t* __restrict__ dense) {
+// load 16 bytes of a row starting at column c0 (n valid bytes, rest 0)
+__device__ __forceinline__ uint4 load16(const uint8_t* row, int c0, int n, bool vec) {
+    if (vec && n == 16) return *reinterpret_cast<const uint4*>(row + c0);
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (int j = 0; j < n; ++j) w[j >> 2] |= (uint32_t)row[c0 + j] << (8 * (j & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ void store16(uint8_t* row, int c0, int n, bool vec, const uint4& v) {
+    if (vec && n == 16) {
+        *reinterpret_cast<uint4*>(row + c0) = v;
+        return;
+    }
+    for (int j = 0; j < n; ++j) row[c0 + j] = (uint8_t)byte_of(v, j);
+}
+
+__global__ void __launch_bounds__(TPB) pack_state_kernel(Geometry G, const uint8_t* __restrict__ src,
+                                                         int src_pitch, long long src_chain,
+                                                         uint8_t* __restrict__ xbuf, int* bad) {
     const int chain = blockIdx.z;
+    const int cx = blockIdx.x * TPB + threadIdx.x;
+    const int c0 = 16 * cx;
+    if (c0 >= G.W) return;
+    const int n = min(16, G.W - c0);
+    const bool vec = ((src_pitch | (int)((uintptr_t)src & 15)) & 15) == 0 && (src_chain & 15) == 0;
+    const uint32_t lv4 = 0x01010101u * (uint32_t)G.levels;
+    int found = 0;
     for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
-        const uint8_t* src = xbuf + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF;
-        uint8_t* dst = dense + ((long long)chain * G.rows + r) * G.W;
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < G.W; c += gridDim.x * blockDim.x)
-            dst[c] = src[c];
+        const uint8_t* s = src + chain * src_chain + (long long)r * src_pitch;
+        const uint4 v = load16(s, c0, n, vec);
+        uint32_t m[4] = {0, 0, 0, 0};  // valid-byte masks
+        for (int j = 0; j < n; ++j) m[j >> 2] |= 0xFFu << (8 * (j & 3));
+        found |= any_ge(v.x & m[0], lv4) | any_ge(v.y & m[1], lv4) | any_ge(v.z & m[2], lv4) |
+                 any_ge(v.w & m[3], lv4);
+        uint8_t* d = xbuf + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF;
+        store16(d, c0, n, true, v);
+        if (G.periodic) {
+            if (c0 == 0) d[G.W] = (uint8_t)byte_of(v, 0);                        // right halo
+            if (c0 + n == G.W) d[-1] = (uint8_t)byte_of(v, n - 1);               // left halo
+            if (G.self_halo_rows && (r == 0 || r == G.rows - 1)) {
+                uint8_t* h = d + (r == 0 ? 1LL : -1LL) * (long long)G.rows * G.xpitch;
+                store16(h, c0, n, true, v);
+                if (c0 == 0) h[G.W] = (uint8_t)byte_of(v, 0);
+                if (c0 + n == G.W) h[-1] = (uint8_t)byte_of(v, n - 1);
+            }
+        }
+    }
+    if (found) atomicOr(bad, 1);
+}
+
+__global__ void __launch_bounds__(TPB) unpack_state_kernel(Geometry G, const uint8_t* __restrict__ xbuf,
+                                                           uint8_t* __restrict__ dense) {
+    const int chain = blockIdx.z;
+    const int c0 = 16 * (blockIdx.x * TPB + threadIdx.x);
+    if (c0 >= G.W) return;
+    const int n = min(16, G.W - c0);
+    const bool vec = (G.W & 15) == 0 && ((uintptr_t)dense & 15) == 0;
+    for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
+        const uint8_t* s = xbuf + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF;
+        uint8_t* d = dense + ((long long)chain * G.rows + r) * G.W;
+        store16(d, c0, n, vec, load16(s, c0, n, true));
     }
 }
 
 __global__ void check_levels_kernel(const uint8_t* __restrict__ p, size_t n, int levels, int* bad) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-         i += (size_t)gridDim.x * blockDim.x)
-        if (p[i] >= levels) atomicOr(bad, 1);
-}
-
-__device__ __forceinline__ int mpm_label(const Geometry& G, const uint16_t* cchain, int r, int c,
-                                         int nsamp) {
-    const uint16_t* cp = cchain + (long long)r * G.cpitch + c;
-    if (G.levels == 2) return (2 * (int)cp[0] > nsamp) ? 1 : 0;
-    int best = 0;
-    int bc = cp[0];
-    for (int k = 1; k < G.levels; ++k) {
-        const int v = cp[(long long)k * G.cplane];
-        if (v > bc) { bc = v; best = k; }
+    const uint32_t lv4 = 0x01010101u * (uint32_t)levels;
+    int found = 0;
+    const size_t nv = n / 16;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nv;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 v = reinterpret_cast<const uint4*>(p)[i];
+        found |= any_ge(v.x, lv4) | any_ge(v.y, lv4) | any_ge(v.z, lv4) | any_ge(v.w, lv4);
     }
-    return best;
+    if (blockIdx.x == 0)
+        for (size_t i = nv * 16 + threadIdx.x; i < n; i += blockDim.x) found |= p[i] >= levels;
+    if (found) atomicOr(bad, 1);
 }
 
-__global__ void mpm_kernel(Geometry G, const uint16_t* __restrict__ counts, int nsamp,
-                           uint8_t* __restrict__ out) {
+// MPM labels of the 16 sites starting at column c0 of row r (ties -> lowest label)
+__device__ __forceinline__ uint4 mpm16(const Geometry& G, const uint16_t* cchain, int r, int c0,
+                                       int nsamp) {
+    const uint16_t* cp = cchain + (long long)r * G.cpitch + c0;  // cpitch = 16*nchunks: in bounds
+    uint32_t out[4] = {0, 0, 0, 0};
+    if (G.levels == 2) {
+        const uint4 a = reinterpret_cast<const uint4*>(cp)[0];
+        const uint4 b = reinterpret_cast<const uint4*>(cp)[1];
+        const uint32_t cw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int c1 = (int)((cw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+            out[j >> 2] |= (uint32_t)(2 * c1 > nsamp) << (8 * (j & 3));
+        }
+    } else {
+        uint32_t best[16], bestc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { best[j] = 0; bestc[j] = 0; }
+        for (int k = 0; k < G.levels; ++k) {
+            const uint4* pk = reinterpret_cast<const uint4*>(cp + (long long)k * G.cplane);
+            const uint4 a = pk[0], b = pk[1];
+            const uint32_t cw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t v = (cw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+                if (k == 0 || v > bestc[j]) { bestc[j] = v; best[j] = (uint32_t)k; }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[j >> 2] |= best[j] << (8 * (j & 3));
+    }
+    return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+__global__ void __launch_bounds__(TPB) mpm_kernel(Geometry G, const uint16_t* __restrict__ counts,
+                                                  int nsamp, uint8_t* __restrict__ out) {
     const int chain = blockIdx.z;
+    const int c0 = 16 * (blockIdx.x * TPB + threadIdx.x);
+    if (c0 >= G.W) return;
+    const int n = min(16, G.W - c0);
+    const bool vec = (G.W & 15) == 0 && ((uintptr_t)out & 15) == 0;
     const uint16_t* cc = counts + chain * G.cchain;
-    for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
-        uint8_t* dst = out + ((long long)chain * G.rows + r) * G.W;
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < G.W; c += gridDim.x * blockDim.x)
-            dst[c] = (uint8_t)mpm_label(G, cc, r, c, nsamp);
-    }
+    for (int r = blockIdx.y; r < G.rows; r += gridDim.y)
+        store16(out + ((long long)chain * G.rows + r) * G.W, c0, n, vec, mpm16(G, cc, r, c0, nsamp));
 }
 
 // One label plane k (or the conditional mean when k < 0) for every chain:
@@ -87,22 +158,22 @@ __global__ void marginals_kernel(Geometry G, const uint16_t* __restrict__ counts
     const int chain = blockIdx.z;
     const double inv = 1.0 / (double)nsamp;
     for (int r = blockIdx.y; r < G.rows; r += gridDim.y)
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < G.W; c += gridDim.x * blockDim.x) {
-        const uint16_t* cc = counts + chain * G.cchain + (long long)r * G.cpitch;
-        float* o = out + chain * out_chain_stride + (long long)r * G.W;
-        double v;
-        if (G.levels == 2) {
-            const int c1 = cc[c];
-            v = (k == 0) ? (double)(nsamp - c1) : (double)c1;  // CM = lum(1) * c1 for l = 2
-        } else if (k >= 0) {
-            v = (double)cc[(long long)k * G.cplane + c];
-        } else {
-            v = 0.0;
-            for (int s = 0; s < G.levels; ++s)
-                v += ((double)s / (double)(G.levels - 1)) * (double)cc[(long long)s * G.cplane + c];
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < G.W; c += gridDim.x * blockDim.x) {
+            const uint16_t* cc = counts + chain * G.cchain + (long long)r * G.cpitch;
+            float* o = out + chain * out_chain_stride + (long long)r * G.W;
+            double v;
+            if (G.levels == 2) {
+                const int c1 = cc[c];
+                v = (k == 0) ? (double)(nsamp - c1) : (double)c1;  // CM = lum(1) * c1 for l = 2
+            } else if (k >= 0) {
+                v = (double)cc[(long long)k * G.cplane + c];
+            } else {
+                v = 0.0;
+                for (int s = 0; s < G.levels; ++s)
+                    v += ((double)s / (double)(G.levels - 1)) * (double)cc[(long long)s * G.cplane + c];
+            }
+            o[c] = (float)(v * inv);
         }
-        o[c] = (float)(v * inv);
-    }
 }
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
@@ -111,45 +182,52 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) metric_sums_kernel(const MetricParams p) {
+__global__ void __launch_bounds__(TPB) metric_sums_kernel(const MetricParams p) {
     const Geometry& G = p.geo;
-    const int chain = blockIdx.y;
+    const int chain = blockIdx.z;
+    const int c0 = 16 * (blockIdx.x * TPB + threadIdx.x);
+    const int n = c0 < G.W ? min(16, G.W - c0) : 0;
+    const bool vec = (G.W & 15) == 0 && ((uintptr_t)p.truth & 15) == 0;
     const uint8_t* truth = p.truth + (long long)chain * G.rows * G.W;
     const uint8_t* xb = p.x + chain * G.xchain;
     const uint16_t* cc = p.counts + chain * G.cchain;
-    unsigned long long s[7] = {0, 0, 0, 0, 0, 0, 0};
-    const long long n = (long long)G.rows * G.W;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / G.W), c = (int)(i % G.W);
-        const unsigned long long x = truth[i];
-        const unsigned long long y =
-            p.kind == 0 ? xb[(long long)(r + 1) * G.xpitch + XOFF + c] : mpm_label(G, cc, r, c, p.nsamp);
-        const long long d = (long long)x - (long long)y;
-        s[0] += (unsigned long long)(d * d);
-        s[1] += x;
-        s[2] += y;
-        s[3] += x * x;
-        s[4] += y * y;
-        s[5] += x * y;
-        s[6] = x > s[6] ? x : s[6];
+    unsigned long long s[6] = {0, 0, 0, 0, 0, 0};
+    uint32_t mx = 0;
+    if (n > 0) {
+        for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
+            const uint4 tv = load16(truth + (long long)r * G.W, c0, n, vec);
+            const uint4 yv = p.kind == 0 ? load16(xb + (long long)(r + 1) * G.xpitch + XOFF, c0, n, true)
+                                         : mpm16(G, cc, r, c0, p.nsamp);
+            uint32_t t[6] = {0, 0, 0, 0, 0, 0};  // 16 sites: every partial sum < 2^21
+            for (int j = 0; j < n; ++j) {
+                const uint32_t x = byte_of(tv, j), y = byte_of(yv, j);
+                const int d = (int)x - (int)y;
+                t[0] += (uint32_t)(d * d);
+                t[1] += x;
+                t[2] += y;
+                t[3] += x * x;
+                t[4] += y * y;
+                t[5] += x * y;
+                mx = x > mx ? x : mx;
+            }
+#pragma unroll
+            for (int k = 0; k < 6; ++k) s[k] += t[k];
+        }
     }
-    __shared__ unsigned long long red[8][7];
+    __shared__ unsigned long long red[TPB / 32][7];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < 6; ++k) s[k] = warp_sum(s[k]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long v = __shfl_xor_sync(0xFFFFFFFFu, s[6], o);
-        s[6] = v > s[6] ? v : s[6];
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) {
+        for (int k = 0; k < 6; ++k) red[warp][k] = s[k];
+        red[warp][6] = mx;
     }
-    if (lane == 0)
-        for (int k = 0; k < 7; ++k) red[warp][k] = s[k];
     __syncthreads();
     if (threadIdx.x < 7) {
         unsigned long long acc = 0;
-        const int nw = blockDim.x >> 5;
-        for (int w = 0; w < nw; ++w) {
+        for (int w = 0; w < TPB / 32; ++w) {
             const unsigned long long v = red[w][threadIdx.x];
             acc = threadIdx.x == 6 ? (v > acc ? v : acc) : acc + v;
         }
@@ -157,34 +235,37 @@ __global__ void __launch_bounds__(256) metric_sums_kernel(const MetricParams p) 
         if (threadIdx.x == 6) atomicMax(dst + 6, acc);
         else atomicAdd(dst + threadIdx.x, acc);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.sums + chain * 8 + 7, (unsigned long long)n);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        atomicAdd(p.sums + chain * 8 + 7, (unsigned long long)G.rows * G.W);
 }
 
-inline dim3 row_grid(const Geometry& G, int rows, int batch, int threads) {
-    int gx = (G.W + 2 + threads - 1) / threads;
-    if (gx > 64) gx = 64;
-    return dim3(gx, rows < 65535 ? rows : 65535, batch);
+// x: 16-site chunks of a row; y: rows, grid-stride, sized for ~8 resident blocks per SM
+inline dim3 chunk_grid(const Geometry& G, int batch, int max_rows = 2048) {
+    const int nchunks = (G.W + 15) / 16;
+    const int gx = (nchunks + TPB - 1) / TPB;
+    int gy = G.rows < max_rows ? G.rows : max_rows;
+    if (gy < 1) gy = 1;
+    return dim3(gx, gy, batch);
 }
 
 }  // namespace
 
 int launch_pack_state(const Geometry& G, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad, void* stream) {
-    pack_state_kernel<<<row_grid(G, G.rows + 2, batch, 256), 256, 0, (cudaStream_t)stream>>>(
-        G, src, src_pitch, src_chain, xbuf, bad);
+    pack_state_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(G, src, src_pitch,
+                                                                             src_chain, xbuf, bad);
     return (int)cudaGetLastError();
 }
 
 int launch_unpack_state(const Geometry& G, const uint8_t* xbuf, uint8_t* dense, int batch,
                         void* stream) {
-    unpack_state_kernel<<<row_grid(G, G.rows, batch, 256), 256, 0, (cudaStream_t)stream>>>(G, xbuf,
-                                                                                         dense);
+    unpack_state_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(G, xbuf, dense);
     return (int)cudaGetLastError();
 }
 
 int launch_check_levels(const uint8_t* p, size_t n, int levels, int* bad, void* stream) {
-    size_t blocks = (n + 255) / 256;
-    if (blocks > 4096) blocks = 4096;
+    size_t blocks = (n / 16 + 255) / 256;
+    if (blocks > 2048) blocks = 2048;
     if (blocks == 0) blocks = 1;
     check_levels_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(p, n, levels, bad);
     return (int)cudaGetLastError();
@@ -192,24 +273,22 @@ int launch_check_levels(const uint8_t* p, size_t n, int levels, int* bad, void* 
 
 int launch_mpm(const Geometry& G, const uint16_t* counts, int nsamp, uint8_t* out, int batch,
                void* stream) {
-    mpm_kernel<<<row_grid(G, G.rows, batch, 256), 256, 0, (cudaStream_t)stream>>>(G, counts, nsamp,
-                                                                                out);
+    mpm_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(G, counts, nsamp, out);
     return (int)cudaGetLastError();
 }
 
 int launch_marginals(const Geometry& G, const uint16_t* counts, int nsamp, float* out,
                      long long out_chain_stride, int k, int batch, void* stream) {
-    marginals_kernel<<<row_grid(G, G.rows, batch, 256), 256, 0, (cudaStream_t)stream>>>(
-        G, counts, nsamp, out, out_chain_stride, k);
+    int gx = (G.W + 255) / 256;
+    if (gx > 64) gx = 64;
+    dim3 grid(gx, G.rows < 65535 ? G.rows : 65535, batch);
+    marginals_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(G, counts, nsamp, out,
+                                                             out_chain_stride, k);
     return (int)cudaGetLastError();
 }
 
 int launch_metric_sums(const MetricParams& p, int batch, void* stream) {
-    const long long n = (long long)p.geo.rows * p.geo.W;
-    long long blocks = (n + 255) / 256;
-    if (blocks > 1184) blocks = 1184;  // 8 per SM on 148 SMs
-    if (blocks < 1) blocks = 1;
-    metric_sums_kernel<<<dim3((unsigned)blocks, batch), 256, 0, (cudaStream_t)stream>>>(p);
+    metric_sums_kernel<<<chunk_grid(p.geo, batch, 512), TPB, 0, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

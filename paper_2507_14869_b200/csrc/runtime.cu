@@ -189,6 +189,7 @@ struct pca_ctx {
     int kernel = PCA_KERNEL_BINARY;
     int rows_per_thread = 8;
     int poisoned = 0;
+    int x_initialized = 0;
     int64_t tab_stage = -1;
     BinarySweepParams bin;
     GeneralSweepParams gen;
@@ -415,9 +416,13 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
     }
     // free boundary: halos and padding hold the sentinel 0xFF; torus: halos are rewritten by
     // every sweep and padding is 0 (a valid label, so SWAR sums need no masking)
-    const int fill = c.periodic ? 0 : 0xFF;
-    CK(ctx, cudaMemsetAsync(ctx->x[0], fill, L.xbuf, ctx->stream));
-    CK(ctx, cudaMemsetAsync(ctx->x[1], fill, L.xbuf, ctx->stream));
+    // (only once: no kernel ever writes a free-boundary halo or a padding byte)
+    if (!ctx->x_initialized) {
+        const int fill = c.periodic ? 0 : 0xFF;
+        CK(ctx, cudaMemsetAsync(ctx->x[0], fill, L.xbuf, ctx->stream));
+        CK(ctx, cudaMemsetAsync(ctx->x[1], fill, L.xbuf, ctx->stream));
+        ctx->x_initialized = 1;
+    }
     CK(ctx, cudaMemsetAsync(ctx->counts, 0, L.counts_bytes, ctx->stream));
     ctx->cur = 0;
     ctx->t = 0;

@@ -34,7 +34,6 @@ constexpr int XROW_BYTES = 16 * SEG_CHUNKS + 32;       // 544: [col0-16, col0+52
 constexpr int GROW_BYTES = 16 * SEG_CHUNKS;            // 512
 constexpr int CROW_BYTES = 32 * SEG_CHUNKS;            // 1024
 constexpr int STAGE_BYTES = XROW_BYTES + GROW_BYTES + CROW_BYTES;  // 2080
-constexpr int THR_BYTES = THR_ENTRIES * 4;             // 1296
 
 constexpr int align16(int v) { return (v + 15) & ~15; }
 constexpr int RING_OFFSET = align16(KSTAGES * 8);      // mbarriers first, then the ring
