@@ -216,22 +216,23 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
+    from paper_2507_14869_b200 import dist as pdist
+
     wl = workload(n)
     truth, g = make_inputs(wl, rank)
     rows, W = wl["rows"], wl["W"]
-    cfg = P.make_config(wl["H"], W, wl["levels"], neighborhood=wl["nbhd"], periodic=wl["periodic"],
-                        sigma=wl["sigma"], q=0.51, beta0=wl["beta"], beta_step=0.0,
-                        beta_period=1 << 30, seed=11, mpm_burn_in=0, row0=rank * rows,
-                        rows=rows if world > 1 else 0, rows_per_thread=args.rows_per_thread)
+    assert pdist.strip_rows(wl["H"], max(world, 1), rank)[1] == rows
     stream = torch.cuda.Stream(device=dev)
     g_dev = torch.from_numpy(g).to(dev).reshape(1, rows, W).contiguous()
     t_dev = torch.from_numpy(truth).to(dev).reshape(1, rows, W).contiguous()
     mpm_dev = torch.empty_like(g_dev)
-    ctx = P.PcaContext(cfg, g_dev, stream=stream)
-    if world > 1:
-        uid = [P.pca_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.pca_attach_nccl(uid[0], world, rank)
+    kw = dict(neighborhood=wl["nbhd"], periodic=wl["periodic"], sigma=wl["sigma"], q=0.51,
+              beta0=wl["beta"], beta_step=0.0, beta_period=1 << 30, seed=11, mpm_burn_in=0,
+              rows_per_thread=args.rows_per_thread)
+    if world > 1:  # this rank's row strip, NCCL attached (unique id broadcast by torch.distributed)
+        ctx = pdist.strip_context(kw, wl["H"], W, wl["levels"], g_dev, stream=stream)
+    else:
+        ctx = P.PcaContext(P.make_config(wl["H"], W, wl["levels"], **kw), g_dev, stream=stream)
     S = args.sweeps
 
     def step_device():

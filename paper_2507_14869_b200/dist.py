@@ -1,0 +1,63 @@
+"""Host-side logic of the row-strip decomposition and of batch sharding.
+
+* ``strip_rows``: balanced contiguous partition of the H global rows over the ranks.
+* ``ring_peers``: the ranks above/below a strip (a ring on the torus; -1 at free ends).
+* ``broadcast_unique_id``: rank 0 creates the NCCL unique id through the C ABI
+  (pca_nccl_unique_id) and torch.distributed broadcasts its 128 bytes.
+* ``strip_context``: a PcaContext for this rank's strip with NCCL attached.
+* ``chain_range``: the batch-mode partition of independent chains (replicas only).
+
+The per-sweep halo exchange itself runs inside the library (runtime.cu ``exchange``):
+after each sweep a rank sends its first owned row to ``up`` and its last to ``down`` and
+receives the two halo rows -- the same protocol ``tests/test_dist_cpu.py`` replays with gloo.
+"""
+from __future__ import annotations
+
+
+def strip_rows(H: int, world: int, rank: int) -> tuple[int, int]:
+    """(row0, rows) of `rank`: the first H % world ranks get one extra row."""
+    if world < 1 or not 0 <= rank < world or H < world:
+        raise ValueError("need 0 <= rank < world <= H")
+    base, extra = divmod(H, world)
+    rows = base + (1 if rank < extra else 0)
+    row0 = rank * base + min(rank, extra)
+    return row0, rows
+
+
+def ring_peers(rank: int, world: int, periodic: bool) -> tuple[int, int]:
+    """(up, down): the ranks owning the rows just above / below this strip, -1 if none."""
+    if periodic:
+        return (rank - 1) % world, (rank + 1) % world
+    return (rank - 1 if rank > 0 else -1), (rank + 1 if rank < world - 1 else -1)
+
+
+def chain_range(n_chains: int, world: int, rank: int) -> tuple[int, int]:
+    """(chain0, batch) of `rank` in batch mode: contiguous, balanced."""
+    return strip_rows(n_chains, world, rank)
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    import torch.distributed as dist
+
+    from . import pca_nccl_unique_id
+
+    obj = [pca_nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    assert isinstance(obj[0], bytes) and len(obj[0]) == 128
+    return obj[0]
+
+
+def strip_context(cfg_kwargs: dict, H: int, W: int, levels: int, g_strip, *, stream=None,
+                  group=None):
+    """Create this rank's strip context (rows from strip_rows) and attach NCCL."""
+    import torch.distributed as dist
+
+    from . import PcaContext, make_config
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    row0, rows = strip_rows(H, world, rank)
+    cfg = make_config(H, W, levels, row0=row0, rows=rows if world > 1 else 0, **cfg_kwargs)
+    ctx = PcaContext(cfg, g_strip, stream=stream)
+    if world > 1:
+        ctx.pca_attach_nccl(broadcast_unique_id(group), world, rank)
+    return ctx

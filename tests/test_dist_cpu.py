@@ -1,0 +1,124 @@
+"""Multi-process (gloo, world size 2, CPU) coverage of the N > 1 host logic.
+
+The row-strip protocol of paper_2507_14869_b200.dist (partition, ring peers, the NCCL
+unique-id broadcast) is replayed with the CPU oracle as the per-strip sweep and gloo
+send/recv as the halo transport: the gathered sharded chain must equal the unsharded
+oracle chain bit for bit (the RNG is keyed by global row/col).
+Rows a rank does not own are filled with random labels, so reading anything but the
+exchanged halo rows would break the equality.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as orc
+from paper_2507_14869_b200 import dist as pdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        uid = pdist.broadcast_unique_id()
+        ids = [None] * world
+        dist.all_gather_object(ids, uid)
+        assert all(i == ids[0] for i in ids)
+
+        row0, rows = pdist.strip_rows(H, world, rank)
+        up, down = pdist.ring_peers(rank, world, periodic)
+        rng = np.random.default_rng(100 + rank)
+        g = np.random.default_rng(7).integers(0, levels, (H, W), dtype=np.uint8)
+        m = orc.model(H, W, levels, nbhd=8, periodic=periodic, sigma=0.4)
+        x = rng.integers(0, levels, (H, W), dtype=np.uint8)  # poison: rows not owned
+        x[row0:row0 + rows] = g[row0:row0 + rows]            # x0 = g on the strip
+
+        def exchange(x):
+            # library order: send(top -> up), recv(bottom halo <- down),
+            #                send(bottom -> down), recv(top halo <- up)
+            reqs = []
+            top = torch.from_numpy(x[row0].copy())
+            bot = torch.from_numpy(x[row0 + rows - 1].copy())
+            halo_bot = torch.empty(W, dtype=torch.uint8)
+            halo_top = torch.empty(W, dtype=torch.uint8)
+            if up >= 0:
+                reqs.append(dist.isend(top, up, tag=0))
+            if down >= 0:
+                reqs.append(dist.irecv(halo_bot, down, tag=0))
+                reqs.append(dist.isend(bot, down, tag=1))
+            if up >= 0:
+                reqs.append(dist.irecv(halo_top, up, tag=1))
+            for r in reqs:
+                r.wait()
+            if up >= 0:
+                x[(row0 - 1) % H] = halo_top.numpy()
+            if down >= 0:
+                x[(row0 + rows) % H] = halo_bot.numpy()
+
+        exchange(x)
+        for t in range(nsweeps):
+            new, _ = orc.pca_sweep(m, x, g, 1.25, 99, 0, t, rows=(row0, row0 + rows))
+            x = rng.integers(0, levels, (H, W), dtype=np.uint8)  # fresh poison every sweep
+            x[row0:row0 + rows] = new
+            exchange(x)
+        strips = [None] * world
+        dist.all_gather_object(strips, (row0, x[row0:row0 + rows].copy()))
+        if rank == 0:
+            full = np.zeros((H, W), np.uint8)
+            for r0, s in strips:
+                full[r0:r0 + len(s)] = s
+            ref = g.copy()
+            for t in range(nsweeps):
+                ref, _ = orc.pca_sweep(m, ref, g, 1.25, 99, 0, t)
+            out_q.put(bool(np.array_equal(full, ref)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_two_rank_strip_exchange_reproduces_unsharded_chain(periodic):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 13, 11, 3, periodic, 6, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok
+
+
+def test_partition_and_peers():
+    for H in (3, 10, 4096 * 8, 17):
+        for world in (1, 2, 3, 8):
+            if world > H:
+                continue
+            spans = [pdist.strip_rows(H, world, r) for r in range(world)]
+            assert spans[0][0] == 0
+            for (a0, an), (b0, _) in zip(spans, spans[1:]):
+                assert a0 + an == b0
+            assert sum(n for _, n in spans) == H
+            assert max(n for _, n in spans) - min(n for _, n in spans) <= 1
+    assert pdist.ring_peers(0, 4, True) == (3, 1)
+    assert pdist.ring_peers(0, 4, False) == (-1, 1)
+    assert pdist.ring_peers(3, 4, False) == (2, -1)
+    assert pdist.ring_peers(0, 2, True) == (1, 1)
+    assert pdist.chain_range(1024, 8, 3) == (384, 128)
+    with pytest.raises(ValueError):
+        pdist.strip_rows(2, 3, 0)
