@@ -76,9 +76,10 @@ enum {
 
 /* Kernel selection (all give the same chain up to fp64 near-ties). */
 enum {
-    PCA_KERNEL_AUTO = 0,    /* binary fast path when levels == 2, else general        */
-    PCA_KERNEL_GENERAL = 1, /* fp64 per-site weights, any levels                      */
-    PCA_KERNEL_BINARY = 2   /* levels == 2: SWAR neighbour counts + integer thresholds */
+    PCA_KERNEL_AUTO = 0,    /* BINARY when levels == 2, else GENERAL                        */
+    PCA_KERNEL_GENERAL = 1, /* any levels: integer thresholds where all neighbours agree    */
+                            /* (levels <= 16), else fp64 per-site weights                   */
+    PCA_KERNEL_BINARY = 2   /* levels == 2: SWAR neighbour counts + integer thresholds      */
 };
 
 typedef struct pca_config {

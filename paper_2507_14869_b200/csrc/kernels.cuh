@@ -64,12 +64,15 @@ struct BinarySweepParams {
 
 // general path: A[n] = exp(a n), Cw = exp(-c); D table in global memory.  a, b, c feed
 // the log-domain slow path used when the factorised weights under/overflow.
+// uthr[((s*L + g)*L + x)*(L-1) + k] = ceil(F_k 2^32) - 1: the integer thresholds of a site
+// whose neighbours all carry s (nullptr when L > 16).
 struct GeneralSweepParams {
     SweepCommon c;
     double A[9];
     double Cw;
     double coef_a, coef_b, coef_c;
     const double* dtab;
+    const uint32_t* uthr;
 };
 
 struct MetricParams {

@@ -90,10 +90,15 @@ NcclApi& nccl() {
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+// uniform-neighbourhood integer threshold tables (multilevel kernel) up to 16 levels:
+// 16^3 * 15 entries = 240 KiB
+constexpr int UTHR_MAX_LEVELS = 16;
+
 // Workspace layout: byte offsets of every region.
 struct Layout {
     int rows = 0, nchunks = 0, xpitch = 0, gpitch = 0, cpitch = 0, cplanes = 0;
     size_t xbuf = 0;      // bytes of one x buffer
+    size_t off_uthr = 0, uthr_entries = 0;
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_sums = 0,
            off_sums_max = 0, off_flag = 0, off_stage = 0;
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
@@ -157,6 +162,9 @@ Layout make_layout(const pca_config* c) {
     L.off_g = o; o = align256(o + B * R * (size_t)L.gpitch);
     L.off_counts = o; o = align256(o + L.counts_bytes);
     L.off_dtab = o; o = align256(o + (size_t)c->levels * c->levels * sizeof(double));
+    L.uthr_entries = c->levels <= UTHR_MAX_LEVELS
+                         ? (size_t)c->levels * c->levels * c->levels * (c->levels - 1) : 0;
+    L.off_uthr = o; o = align256(o + L.uthr_entries * sizeof(uint32_t));
     L.off_sums = o; o = align256(o + B * 8 * sizeof(unsigned long long));
     L.off_sums_max = o; o = align256(o + B * 8 * sizeof(unsigned long long));
     L.off_flag = o; o = align256(o + 256);
@@ -194,6 +202,8 @@ struct pca_ctx {
     BinarySweepParams bin;
     GeneralSweepParams gen;
     std::vector<double> dtab_host;
+    std::vector<uint32_t> uthr_host;
+    uint32_t* uthr = nullptr;
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
 };
@@ -323,11 +333,49 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
                         ctx->bin.thr[idx] = T >= 1.0 ? (uint32_t)(T - 1.0) : 0u;
                     }
     } else {
-        for (int n = 0; n <= 8; ++n) ctx->gen.A[n] = exp(a * (double)n);
-        ctx->gen.Cw = exp(-cq);
-        ctx->gen.coef_a = a;
-        ctx->gen.coef_b = b;
-        ctx->gen.coef_c = cq;
+        GeneralSweepParams& m = ctx->gen;
+        for (int n = 0; n <= 8; ++n) m.A[n] = exp(a * (double)n);
+        m.Cw = exp(-cq);
+        m.coef_a = a;
+        m.coef_b = b;
+        m.coef_c = cq;
+        if (ctx->lay.uthr_entries) {
+            // uniform neighbourhood (all NB neighbours carry s*): the oracle's per-site law
+            // (max-subtracted softmax, ascending cumulative sum) in the same fp64 order, and
+            // T_k = ceil(F_k 2^32) - 1 so that "u < F_k" <=> "r <= T_k".
+            const int L = c.levels, NB = c.neighborhood;
+            std::vector<double> E(L), pr(L);
+            uint32_t* out = ctx->uthr_host.data();
+            for (int s0 = 0; s0 < L; ++s0)
+                for (int gl = 0; gl < L; ++gl)
+                    for (int xl = 0; xl < L; ++xl) {
+                        double Emax = -INFINITY;
+                        for (int s = 0; s < L; ++s) {
+                            const double d = lum(gl, L) - lum(s, L);
+                            const double inert = (s != xl) ? 1.0 : 0.0;
+                            const int n = (s == s0) ? NB : 0;
+                            E[s] = a * (double)n - b * d * d - cq * inert;
+                            if (E[s] > Emax) Emax = E[s];
+                        }
+                        double Z = 0.0;
+                        for (int s = 0; s < L; ++s) {
+                            pr[s] = exp(E[s] - Emax);
+                            Z += pr[s];
+                        }
+                        for (int s = 0; s < L; ++s) pr[s] = pr[s] / Z;
+                        double F = 0.0;
+                        for (int k = 0; k < L - 1; ++k) {
+                            F += pr[k];
+                            const double T = ceil(F * 4294967296.0);
+                            *out++ = T < 1.0 ? 0u : (T > 4294967296.0 ? 0xFFFFFFFFu : (uint32_t)(T - 1.0));
+                        }
+                    }
+            // pageable host -> device: the source is staged before the call returns, and the
+            // copy is stream-ordered after every sweep of the previous stage
+            CK(ctx, cudaMemcpyAsync(ctx->uthr, ctx->uthr_host.data(),
+                                    ctx->uthr_host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+        }
     }
     ctx->tab_stage = stage;
     ctx->beta_last = beta;
@@ -482,6 +530,8 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->sums_max = (unsigned long long*)(ctx->ws + L.off_sums_max);
     ctx->flag = (int*)(ctx->ws + L.off_flag);
     ctx->stage = ctx->ws + L.off_stage;
+    ctx->uthr = L.uthr_entries ? (uint32_t*)(ctx->ws + L.off_uthr) : nullptr;
+    ctx->uthr_host.resize(L.uthr_entries);
     ctx->kernel = (cfg->kernel == PCA_KERNEL_AUTO) ? (cfg->levels == 2 ? PCA_KERNEL_BINARY
                                                                        : PCA_KERNEL_GENERAL)
                                                    : cfg->kernel;
@@ -514,6 +564,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
             ctx->dtab_host[(size_t)gl * cfg->levels + s] = exp(-b * d * d);
         }
     ctx->gen.dtab = ctx->dtab;
+    ctx->gen.uthr = ctx->uthr;
 
     auto bail = [&](pca_status s) {
         delete ctx;

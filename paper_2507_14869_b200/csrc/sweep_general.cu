@@ -1,6 +1,12 @@
 // sweep_general.cu -- one synchronous lazy-PCA sweep for any number of levels (2..255).
 //
-// Per site i (PAPER.md:462-477 with R1), in fp64:
+// Uniform neighbourhood (all NB neighbours carry the same label s*, ~75-85% of the sites of
+// a restored MRF image): p_i depends only on (s*, g_i, x_i), so the host tabulates for the
+// current beta the integer thresholds T_k = ceil(F_k 2^32) - 1 of the cumulative
+// probabilities (fp64, accumulated exactly as the oracle does, levels <= 16) and the new
+// label is #{k : r > T_k} -- integer-exact, like the binary kernel.
+//
+// Otherwise, per site i (PAPER.md:462-477 with R1), in fp64:
 //   w_s = e^{a n_i(s)} * e^{-b (lum g_i - lum s)^2} * e^{-c 1{s != x_i}}
 //       = A[n_i(s)] * D[g_i][s] * (s == x_i ? 1 : Cw)
 // (the factorised form of exp(E_i(s)); A, D, Cw tabulated on the host in fp64),
@@ -75,6 +81,17 @@ __global__ void __launch_bounds__(256)
             }
             const int xi = win_byte(mid, pos);
             const int gi = (int)((gword >> (8 * b)) & 0xFFu);
+            bool uniform = p.uthr != nullptr && xi < L && nb[0] < L;
+#pragma unroll
+            for (int j = 1; j < NB; ++j) uniform = uniform && nb[j] == nb[0];
+            if (uniform) {
+                // every neighbour carries s* = nb[0] (so all NB exist): integer thresholds
+                const uint32_t* T = p.uthr + (size_t)((nb[0] * L + gi) * L + xi) * (L - 1);
+                int w = 0;
+                for (int k = 0; k < L - 1; ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
+                outw |= (uint32_t)w << (8 * b);
+                continue;
+            }
             const double* Drow = dtab + (size_t)(gi < L ? gi : 0) * L;
             double Z = 0.0;
             for (int s = 0; s < L; ++s) {

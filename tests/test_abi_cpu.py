@@ -46,7 +46,7 @@ def test_workspace_and_validation(lib):
         dict(levels=1), dict(levels=256), dict(neighborhood=6), dict(periodic=True, height=2),
         dict(J=0.0), dict(q=-1.0), dict(sigma=0.0), dict(beta0=0.0), dict(beta_step=-0.1),
         dict(beta_period=0), dict(coef_scale=0.0), dict(rows=10, row0=60), dict(batch=0),
-        dict(kernel=P.KERNEL_BINARY, levels=3), dict(rows_per_thread=-3), dict(batch=70000),
+        dict(kernel=P.KERNEL_BINARY, levels=3), dict(rows_per_thread=-3), dict(batch=70000), dict(kernel=3),
     ]
     for kw in bad:
         args = dict(height=64, width=64, levels=2)
