@@ -9,17 +9,17 @@
 // (324 entries) and the device decision is the integer compare r > T - 1 on the Philox
 // word r (u = r 2^-32): bit-exact with the fp64 oracle whenever the host's p0 equals it.
 //
-// Data movement (Blackwell-native): every warp owns a 512-column segment (16 sites per
-// lane) of a run of R rows and streams it through a private K-stage shared-memory ring
-// filled by 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on per-stage
-// mbarriers.  A stage holds one padded x row (544 B incl. the words left/right of the
-// segment), one g row (512 B) and one row of uint16 MPM counts (1 KiB), so the warp keeps
-// K-1 rows of loads in flight without spending registers.  The 3-row neighbourhood window
-// lives in registers; neighbour counts are SWAR byte sums
-// (vertical sum of 3 rows, then funnel-shifted left/right sums); the table index of each
-// site is one byte of a pre-scaled SWAR word, extracted with one PRMT.  One Philox4x32-10
-// call serves 4 sites.  The MPM count of label 1 (uint16) is updated in the same pass (R15)
-// and stored with x_{t+1}.
+// Data movement (Blackwell-native): one warp per CTA owns a 512-column segment (16 sites
+// per lane) of a run of R rows and streams it through a private KSTAGES-deep shared-memory
+// ring filled by 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) that complete on
+// per-stage mbarriers.  A stage carries TWO rows: two padded x rows (544 B each, incl. the
+// words left/right of the segment), two g rows (512 B) and two rows of uint16 MPM counts
+// (1 KiB), so the per-stage bookkeeping (wait, refill, fence, address arithmetic) is paid
+// once per two rows.  The 4-row neighbourhood window lives in registers; neighbour counts
+// are SWAR byte sums (vertical sum of 3 rows, then funnel-shifted left/right sums); the table
+// index of each site is one byte of a pre-scaled SWAR word, extracted with one PRMT.  One
+// Philox4x32-10 call serves 4 sites.  The MPM count of label 1 (uint16) is updated in the
+// same pass (R15) and stored with x_{t+1}.
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -28,21 +28,21 @@
 namespace pcab200 {
 namespace {
 
-constexpr int KSTAGES = 4;                             // ring depth per warp (power of two)
-constexpr int MIN_CTAS = 22;                           // resident one-warp CTAs per SM
+constexpr int KSTAGES = 3;                             // ring depth per warp (2 rows each)
+constexpr int MIN_CTAS = 16;                           // resident one-warp CTAs per SM
 constexpr int SEG_CHUNKS = 32;                         // 16-site chunks per warp segment
 constexpr int XROW_BYTES = 16 * SEG_CHUNKS + 32;       // 544: [col0-16, col0+528)
 constexpr int GROW_BYTES = 16 * SEG_CHUNKS;            // 512
 constexpr int CROW_BYTES = 32 * SEG_CHUNKS;            // 1024
-constexpr int STAGE_BYTES = XROW_BYTES + GROW_BYTES + CROW_BYTES;  // 2080
+constexpr int XOFS = 0, GOFS = 2 * XROW_BYTES, COFS = GOFS + 2 * GROW_BYTES;
+constexpr int STAGE_BYTES = COFS + 2 * CROW_BYTES;     // 4160
 
-constexpr int align16(int v) { return (v + 15) & ~15; }
-constexpr int RING_OFFSET = align16(KSTAGES * 8);      // mbarriers first, then the ring
+constexpr int RING_OFFSET = 64;                        // mbarriers first, then the ring
 constexpr int SMEM_BYTES = RING_OFFSET + KSTAGES * STAGE_BYTES;  // dynamic smem per CTA
 
 // Map label bytes to {0,1}: 0 -> 0, 1 -> 1, free-boundary sentinel 0xFF -> 0.
 __device__ __forceinline__ uint32_t to01(uint32_t w) { return w & ~(w >> 1) & 0x01010101u; }
-__device__ __forceinline__ uint8_t out_byte(const uint32_t (&o)[4], int j) { return chunk_byte(o, j); }
+
 template <int NB>
 __device__ __forceinline__ int neighbours_present(int grow, int H, int c, int W) {
     const int er = (grow == 0) + (grow == H - 1);
@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
     const int rbeg = blockIdx.y * R;
     const int rend = min(rbeg + R, G.rows);
     if (rbeg >= rend) return;
-    const int nitems = rend - rbeg + 2;  // x rows rbeg-1 .. rend
+    // item i carries x rows rbeg-1+2i, rbeg+2i and g / count rows rbeg+2i-2, rbeg+2i-1
+    const int nitems = (rend - rbeg + 3) >> 1;
     const int nch = min(SEG_CHUNKS, G.nchunks - seg * SEG_CHUNKS);
     const int col0 = 16 * SEG_CHUNKS * seg;
     const int k = seg * SEG_CHUNKS + lane;  // this lane's chunk
@@ -90,37 +91,37 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
     // padded x row j (-1..rows) starts at (j+1)*xpitch; byte col0 of it is column col0-16
     const uint8_t* xin = p.c.x_in + chain * G.xchain + col0 + (long long)rbeg * G.xpitch;
     const uint8_t* gin = p.c.g + chain * G.gchain + col0 + (long long)rbeg * G.gpitch;
-    uint16_t* cnt_issue = p.c.counts + chain * G.cchain + col0 + (long long)rbeg * G.cpitch;
+    const uint16_t* cin = p.c.counts + chain * G.cchain + col0 + (long long)rbeg * G.cpitch;
     uint8_t* xo = p.c.x_out + chain * G.xchain + XOFF + ccol + (long long)(rbeg + 1) * G.xpitch;
     uint16_t* co = p.c.counts + chain * G.cchain + ccol + (long long)rbeg * G.cpitch;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const uint8_t* thr_b = reinterpret_cast<const uint8_t*>(s_thr);
 
-    // lane 0: load item `it` (x row rbeg-1+it; g / counts row rbeg+it-2 when it >= 2)
-    auto issue = [&](int it) {
-        const int s = it & (KSTAGES - 1);
+    // elected lane: load item `it` into stage s (rows past the run are skipped)
+    auto issue = [&](int it, int s) {
         uint8_t* st = ring + s * STAGE_BYTES;
-        const bool gc = it >= 2;
-        mbar_expect_tx(&bars[s], xbytes + (gc ? gbytes + cbytes : 0u));
-        bulk_g2s(st, xin + (long long)it * G.xpitch, xbytes, &bars[s]);
-        if (gc) {
-            bulk_g2s(st + XROW_BYTES, gin + (long long)(it - 2) * G.gpitch, gbytes, &bars[s]);
+        const int jx = 2 * it;             // x row rbeg-1+jx relative to xin
+        const int nx = (rbeg - 1 + jx + 1 <= rend) ? 2 : 1;
+        const int jr = 2 * it - 2;         // g / count row rbeg+jr
+        const int nr = it == 0 ? 0 : min(2, rend - rbeg - jr);
+        mbar_expect_tx(&bars[s], nx * xbytes + nr * (gbytes + cbytes));
+        for (int q = 0; q < nx; ++q)
+            bulk_g2s(st + XOFS + q * XROW_BYTES, xin + (long long)(jx + q) * G.xpitch, xbytes, &bars[s]);
+        for (int q = 0; q < nr; ++q) {
+            bulk_g2s(st + GOFS + q * GROW_BYTES, gin + (long long)(jr + q) * G.gpitch, gbytes, &bars[s]);
             if (cbytes)
-                bulk_g2s(st + XROW_BYTES + GROW_BYTES, cnt_issue + (long long)(it - 2) * G.cpitch,
-                         cbytes, &bars[s]);
+                bulk_g2s(st + COFS + q * CROW_BYTES, cin + (long long)(jr + q) * G.cpitch, cbytes,
+                         &bars[s]);
         }
     };
     if (elect_one())
-        for (int it = 0; it < min(KSTAGES, nitems); ++it) issue(it);
+        for (int it = 0; it < min(KSTAGES, nitems); ++it) issue(it, it);
 
-    // wait for item `it` and copy its x row into registers
-    auto fetch = [&](int it, XRow& x) {
-        const int s = it & (KSTAGES - 1);
-        mbar_wait(&bars[s], (uint32_t)((it / KSTAGES) & 1));
-        const uint8_t* st = ring + s * STAGE_BYTES;
-        const uint4 xv = *reinterpret_cast<const uint4*>(st + 16 + 16 * lane);
-        x.l = *reinterpret_cast<const uint32_t*>(st + 12 + 16 * lane);
-        x.r = *reinterpret_cast<const uint32_t*>(st + 32 + 16 * lane);
+    auto read_x = [&](const uint8_t* st, int q, XRow& x) {
+        const uint8_t* xr = st + XOFS + q * XROW_BYTES;
+        const uint4 xv = *reinterpret_cast<const uint4*>(xr + 16 + 16 * lane);
+        x.l = *reinterpret_cast<const uint32_t*>(xr + 12 + 16 * lane);
+        x.r = *reinterpret_cast<const uint32_t*>(xr + 32 + 16 * lane);
         x.w[0] = xv.x; x.w[1] = xv.y; x.w[2] = xv.z; x.w[3] = xv.w;
         if (!PER) {
 #pragma unroll
@@ -129,23 +130,12 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
             x.r = to01(x.r);
         }
     };
-    // every lane is done with item `it`'s stage: refill it with item it + KSTAGES
-    auto release = [&](int it) {
-        __syncwarp();
-        if (it + KSTAGES < nitems && elect_one()) {
-            fence_proxy_async();
-            issue(it + KSTAGES);
-        }
-    };
 
-    // update local row r from the window (U = row r-1, M = row r, D = row r+1)
-    // (its g row and counts row are read straight from item `it`'s stage)
-    auto update = [&](int it, const XRow& U, const XRow& M, const XRow& D) {
-        if (!active) return;  // lanes past the last chunk of a partial segment hold no data
-        const int r = rbeg + it - 2;
+    // update local row r from the window (U = row r-1, M = row r, D = row r+1); its g row
+    // and counts row are slot q of stage st
+    auto update = [&](int r, const uint8_t* st, int q, const XRow& U, const XRow& M, const XRow& D) {
         const int grow = G.row0 + r;
-        const uint8_t* st = ring + (it & (KSTAGES - 1)) * STAGE_BYTES;
-        const uint4 gv = *reinterpret_cast<const uint4*>(st + XROW_BYTES + 16 * lane);
+        const uint4 gv = *reinterpret_cast<const uint4*>(st + GOFS + q * GROW_BYTES + 16 * lane);
         // ---- n_i(1): SWAR neighbour counts, one byte per site ----
         uint32_t S[4];
         if (NB == 8) {
@@ -194,7 +184,7 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
         }
         // ---- fused MPM counts of label 1 (uint16 per site) ----
         if (cbytes) {
-            const uint4* cs = reinterpret_cast<const uint4*>(st + XROW_BYTES + GROW_BYTES + 32 * lane);
+            const uint4* cs = reinterpret_cast<const uint4*>(st + COFS + q * CROW_BYTES + 32 * lane);
             uint4 c0 = cs[0], c1 = cs[1];
             c0.x += __byte_perm(O[0], 0u, 0x4140); c0.y += __byte_perm(O[0], 0u, 0x4342);
             c0.z += __byte_perm(O[1], 0u, 0x4140); c0.w += __byte_perm(O[1], 0u, 0x4342);
@@ -209,29 +199,45 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
         uint8_t* op = xo + (long long)(r - rbeg) * G.xpitch;
         store_chunk(op, O, nvalid);
         if (PER) {
-            if (k == 0) op[G.W] = out_byte(O, 0);                                  // right halo
-            if (k == G.nchunks - 1) op[-ccol - 1] = out_byte(O, G.W - 1 - ccol);  // left halo
+            if (k == 0) op[G.W] = chunk_byte(O, 0);                                  // right halo
+            if (k == G.nchunks - 1) op[-ccol - 1] = chunk_byte(O, G.W - 1 - ccol);  // left halo
             if (G.self_halo_rows && (grow == 0 || grow == G.H - 1)) {
                 uint8_t* hp = op + (grow == 0 ? 1LL : -1LL) * (long long)G.rows * G.xpitch;
                 store_chunk(hp, O, nvalid);
-                if (k == 0) hp[G.W] = out_byte(O, 0);
-                if (k == G.nchunks - 1) hp[-ccol - 1] = out_byte(O, G.W - 1 - ccol);
+                if (k == 0) hp[G.W] = chunk_byte(O, 0);
+                if (k == G.nchunks - 1) hp[-ccol - 1] = chunk_byte(O, G.W - 1 - ccol);
             }
         }
     };
 
-    // 3-row window U (row r-1), M (row r), D (row r+1)
-    XRow U, M, D;
-    fetch(0, M);
-    release(0);
-    fetch(1, D);
-    release(1);
-    for (int it = 2; it < nitems; ++it) {
-        U = M;
-        M = D;
-        fetch(it, D);
-        update(it, U, M, D);
-        release(it);
+    // window: A0 = x row r0-1, A1 = x row r0 (previous item), B0 = r0+1, B1 = r0+2 (current)
+    XRow A0, A1, B0, B1;
+    int s = 0;
+    uint32_t phase = 0;
+    for (int it = 0; it < nitems; ++it) {
+        mbar_wait(&bars[s], phase);
+        const uint8_t* st = ring + s * STAGE_BYTES;
+        if (active) {
+            read_x(st, 0, B0);
+            read_x(st, 1, B1);  // (stale data when past the run: then never used)
+            if (it > 0) {
+                const int r0 = rbeg + 2 * it - 2;
+                update(r0, st, 0, A0, A1, B0);
+                if (r0 + 1 < rend) update(r0 + 1, st, 1, A1, B0, B1);
+            }
+        }
+        // every lane is done with this stage: refill it with item it + KSTAGES
+        __syncwarp();
+        if (it + KSTAGES < nitems && elect_one()) {
+            fence_proxy_async();
+            issue(it + KSTAGES, s);
+        }
+        A0 = B0;
+        A1 = B1;
+        if (++s == KSTAGES) {
+            s = 0;
+            phase ^= 1u;
+        }
     }
 }
 
