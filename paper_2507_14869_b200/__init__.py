@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpca_b200.so")
+LIB_PATH = os.environ.get("PCA_B200_LIB_OVERRIDE") or os.path.join(_PKG, "libpca_b200.so")
 
 PCA_OK, PCA_EINVAL, PCA_ESTATE, PCA_ECUDA, PCA_ENCCL, PCA_ENOSPACE, PCA_EUNSUPPORTED = (
     0, -1, -2, -3, -4, -5, -6)

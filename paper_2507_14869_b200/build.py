@@ -54,11 +54,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile every csrc/*.cu into one shared library (default: the in-tree LIB).
+    `out`/`defines` build tuning variants (e.g. defines=("PCA_KSTAGES=2",))."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
+           *[f"-D{d}" for d in defines],
            "-Xcompiler", "-fPIC,-ffp-contract=off",
            "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(),
            "-o", tmp, *sources(), "-ldl"]
@@ -71,8 +75,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -28,8 +28,14 @@
 namespace pcab200 {
 namespace {
 
-constexpr int KSTAGES = 3;                             // ring depth per warp (2 rows each)
-constexpr int MIN_CTAS = 16;                           // resident one-warp CTAs per SM
+#ifndef PCA_KSTAGES
+#define PCA_KSTAGES 4  // measured on B200 (tools/tune_variants.py): 4 stages x 12 CTAs/SM
+#endif                 // beat 2x20, 3x16, 5x10, 6x8 and 8x6 at 8192^2
+#ifndef PCA_MIN_CTAS
+#define PCA_MIN_CTAS 12
+#endif
+constexpr int KSTAGES = PCA_KSTAGES;                   // ring depth per warp (2 rows each)
+constexpr int MIN_CTAS = PCA_MIN_CTAS;                 // resident one-warp CTAs per SM
 constexpr int SEG_CHUNKS = 32;                         // 16-site chunks per warp segment
 constexpr int XROW_BYTES = 16 * SEG_CHUNKS + 32;       // 544: [col0-16, col0+528)
 constexpr int GROW_BYTES = 16 * SEG_CHUNKS;            // 512
