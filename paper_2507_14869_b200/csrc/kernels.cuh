@@ -53,6 +53,7 @@ struct SweepCommon {
     uint32_t t;            // sweep index (Philox counter word 2)
     uint32_t chain0;       // chain id of batch entry 0
     int count_enable;      // accumulate MPM counts this sweep
+    int rlo, rhi;          // local rows [rlo, rhi) updated by this launch
 };
 
 // levels == 2 fast path: thr[((np*9 + n1)*2 + g)*2 + x] = ceil(p0 * 2^32) - 1, the

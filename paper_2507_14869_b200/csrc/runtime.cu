@@ -206,6 +206,8 @@ struct pca_ctx {
     uint32_t* uthr = nullptr;
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
+    cudaStream_t side = nullptr;  // interior rows of a strip, overlapping the halo exchange
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -602,17 +604,49 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
         const int count = (ctx->cfg.mpm_burn_in >= 0 && t >= ctx->cfg.mpm_burn_in) ? 1 : 0;
         if (count && ctx->counted + 1 > 65535)
             return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
-        if (ctx->kernel == PCA_KERNEL_BINARY) {
-            fill_common(ctx, ctx->bin.c, t, count);
-            LAUNCH(ctx, launch_sweep_binary(ctx->bin, ctx->cfg.batch, ctx->rows_per_thread,
-                                            ctx->stream));
+        fill_common(ctx, ctx->bin.c, t, count);
+        fill_common(ctx, ctx->gen.c, t, count);
+        // one sweep kernel over local rows [rlo, rhi) on stream s
+        auto launch_rows = [&](int rlo, int rhi, cudaStream_t s) -> int {
+            ctx->launches++;
+            ctx->sweep_launches++;
+            if (ctx->kernel == PCA_KERNEL_BINARY) {
+                ctx->bin.c.rlo = rlo;
+                ctx->bin.c.rhi = rhi;
+                return launch_sweep_binary(ctx->bin, ctx->cfg.batch, ctx->rows_per_thread, s);
+            }
+            ctx->gen.c.rlo = rlo;
+            ctx->gen.c.rhi = rhi;
+            return launch_sweep_general(ctx->gen, ctx->cfg.batch, s);
+        };
+        const int R = ctx->lay.rows;
+        int e = 0;
+        if (strip && R >= 3) {
+            // row strip: the two edge rows first, then their halo exchange on the main stream
+            // overlapping the interior rows on the side stream; the next sweep starts after
+            // both (the interior never reads the halo rows).
+            if (!ctx->side) {
+                CK(ctx, cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+                CK(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+                CK(ctx, cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+            }
+            CK(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+            CK(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            e = launch_rows(0, 1, ctx->stream);
+            if (!e) e = launch_rows(R - 1, R, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (edge rows)");
+            st = exchange(ctx, ctx->x[ctx->cur ^ 1]);
+            if (st != PCA_OK) return st;
+            e = launch_rows(1, R - 1, ctx->side);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (interior rows)");
+            CK(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+            CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
         } else {
-            fill_common(ctx, ctx->gen.c, t, count);
-            LAUNCH(ctx, launch_sweep_general(ctx->gen, ctx->cfg.batch, ctx->stream));
+            e = launch_rows(0, R, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep");
+            st = exchange(ctx, ctx->x[ctx->cur ^ 1]);
+            if (st != PCA_OK) return st;
         }
-        ctx->sweep_launches++;
-        st = exchange(ctx, ctx->x[ctx->cur ^ 1]);
-        if (st != PCA_OK) return st;
         ctx->cur ^= 1;
         ctx->t = t + 1;
         ctx->counted += count;
@@ -859,6 +893,12 @@ pca_status pca_destroy(pca_ctx* ctx) {
     if (!ctx) return PCA_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+        cudaEventDestroy(ctx->ev_fork);
+        cudaEventDestroy(ctx->ev_join);
+    }
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     delete ctx;
     return PCA_OK;

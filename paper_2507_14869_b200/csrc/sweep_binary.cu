@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
     const Geometry& G = p.c.geo;
     const int seg = blockIdx.x;
     const int chain = blockIdx.z;
-    const int rbeg = blockIdx.y * R;
-    const int rend = min(rbeg + R, G.rows);
+    const int rbeg = p.c.rlo + blockIdx.y * R;
+    const int rend = min(rbeg + R, p.c.rhi);
     if (rbeg >= rend) return;
     // item i carries x rows rbeg-1+2i, rbeg+2i and g / count rows rbeg+2i-2, rbeg+2i-1
     const int nitems = (rend - rbeg + 3) >> 1;
@@ -269,11 +269,12 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
         // contiguous run of rows with its pipeline primed once
         const long long segs = (G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
         const long long target = (long long)sms * occ;
-        const long long work = (long long)G.rows * segs * batch;
+        const long long work = (long long)(p.c.rhi - p.c.rlo) * segs * batch;
         R = (int)((work + target - 1) / target);
         if (R < 2) R = 2;
     }
-    const int nrb = (G.rows + R - 1) / R;
+    const int nrb = (p.c.rhi - p.c.rlo + R - 1) / R;
+    if (nrb <= 0) return 0;
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS, nrb, batch);
     sweep_binary_kernel<NB, PER><<<grid, 32, SMEM_BYTES, s>>>(p, R);

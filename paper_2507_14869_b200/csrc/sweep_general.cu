@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256)
     const double Cw = p.Cw;
     const double* __restrict__ dtab = p.dtab;
 
-    for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
+    for (int r = p.c.rlo + blockIdx.y; r < p.c.rhi; r += gridDim.y) {
         const int grow = G.row0 + r;
         const uint8_t* xr = p.c.x_in + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF +
                             4 * qd;
@@ -177,7 +177,9 @@ int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream) {
     const Geometry& G = p.c.geo;
     const int nquads = (G.W + 3) / 4;
     dim3 block(nquads >= 256 ? 256 : ((nquads + 31) / 32) * 32);
-    dim3 grid((nquads + block.x - 1) / block.x, G.rows < 65535 ? G.rows : 65535, batch);
+    const int nr = p.c.rhi - p.c.rlo;
+    if (nr <= 0) return 0;
+    dim3 grid((nquads + block.x - 1) / block.x, nr < 65535 ? nr : 65535, batch);
     cudaStream_t s = (cudaStream_t)stream;
     if (G.nbhd == 8) sweep_general_kernel<8><<<grid, block, 0, s>>>(p);
     else sweep_general_kernel<4><<<grid, block, 0, s>>>(p);
