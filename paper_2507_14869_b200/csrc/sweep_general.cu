@@ -13,10 +13,14 @@
 // Z = sum_s w_s; the new label is min{k < l-1 : u Z < sum_{s<=k} w_s}, else l-1 (R14),
 // with u = r 2^-32 from the site's Philox word.  Rounding differs from the oracle's
 // exp(E - max E)/Z only in the last bits, so decisions can differ only when u lies within
-// ~1e-15 of a cumulative probability (an allowed near-tie, R19).
+// ~1e-15 of a cumulative probability (an allowed near-tie, R19).  When the factorised
+// weights under/overflow (extreme beta, q, sigma) the site uses the oracle's log-domain form.
 //
 // One thread = 4 consecutive sites of a row (one Philox4x32-10 call).  The 3x12-byte
 // neighbourhood window is fetched as 9 aligned 32-bit loads (L1-resident across the warp).
+// Load balance: the fp64 sites of a warp are compacted into a per-warp shared-memory queue
+// (ballot + popc) and processed round-robin by all 32 lanes, so a warp pays
+// ceil(#fp64 sites / 32) fp64 evaluations instead of one per site slot that any lane needs.
 // The free-boundary sentinel 0xFF never equals a label, so n_i(s) needs no position test.
 #include <cuda_runtime.h>
 
@@ -24,6 +28,10 @@
 
 namespace pcab200 {
 namespace {
+
+constexpr int GEN_THREADS = 256;
+constexpr int GEN_WARPS = GEN_THREADS / 32;
+constexpr unsigned FULL = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t ldg4(const uint8_t* p) {
     return __ldg(reinterpret_cast<const uint32_t*>(p));
@@ -34,39 +42,154 @@ __device__ __forceinline__ int win_byte(const uint32_t (&w)[3], int pos) {
     return (int)((w[pos >> 2] >> (8 * (pos & 3))) & 0xFFu);
 }
 
+// a queued fp64 site: neighbour labels (NB <= 8 bytes), x_i, g_i, the Philox word
+struct SiteJob {
+    uint32_t nb_lo, nb_hi;
+    uint32_t xg;  // x_i | g_i << 8
+    uint32_t r;
+};
+
+// fp64 decision with L known at compile time (L <= 16): the neighbour histogram is built once
+// as 16 nibbles, the L weights stay in registers, and the CDF scan is branch-free.
+template <int NB, int L>
+__device__ __forceinline__ int decide_fp64_fixed(const GeneralSweepParams& p, const double* sA,
+                                                 const double* sD, const SiteJob& j) {
+    uint64_t hist = 0;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const uint32_t v = ((q < 4 ? j.nb_lo : j.nb_hi) >> (8 * (q & 3))) & 0xFFu;
+        hist += (v < (uint32_t)L) ? (1ull << (4 * v)) : 0ull;  // sentinel 0xFF never counts
+    }
+    const int xi = (int)(j.xg & 0xFFu), gi = (int)((j.xg >> 8) & 0xFFu);
+    const double Cw = p.Cw;
+    const double* Drow = sD + gi * L;
+    double w[L];
+    double Z = 0.0;
+#pragma unroll
+    for (int s = 0; s < L; ++s) {
+        const int n = (int)((hist >> (4 * s)) & 0xFull);
+        w[s] = sA[n] * Drow[s] * (s == xi ? 1.0 : Cw);
+        Z += w[s];
+    }
+    if (!(Z >= 1e-290 && Z <= 1e290)) return -1;  // caller takes the log-domain path
+    const double target = (double)j.r * (1.0 / 4294967296.0) * Z;
+    double F = 0.0;
+    int res = L - 1;
+#pragma unroll
+    for (int s = 0; s < L - 1; ++s) {
+        F += w[s];
+        res = (res == L - 1 && target < F) ? s : res;
+    }
+    return res;
+}
+
 template <int NB>
-__global__ void __launch_bounds__(256)
+__device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const SiteJob& j) {
+    const int L = p.c.geo.levels;
+    int nb[NB];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) nb[q] = (int)(((q < 4 ? j.nb_lo : j.nb_hi) >> (8 * (q & 3))) & 0xFFu);
+    const int xi = (int)(j.xg & 0xFFu), gi = (int)((j.xg >> 8) & 0xFFu);
+    const double Cw = p.Cw;
+    const double* Drow = p.dtab + (size_t)gi * L;
+    double Z = 0.0;
+    for (int s = 0; s < L; ++s) {
+        int n = 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) n += (nb[q] == s);
+        Z += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
+    }
+    const double u = (double)j.r * (1.0 / 4294967296.0);
+    if (Z >= 1e-290 && Z <= 1e290) {
+        const double target = u * Z;
+        double F = 0.0;
+        for (int s = 0; s < L - 1; ++s) {
+            int n = 0;
+#pragma unroll
+            for (int q = 0; q < NB; ++q) n += (nb[q] == s);
+            F += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
+            if (target < F) return s;
+        }
+        return L - 1;
+    }
+    // Rare slow path (extreme beta, q or sigma: the factorised weights under- or overflow):
+    // E_s = a n_s - b d_s^2 - c 1{s != x_i}, softmax with the max subtracted.
+    const double lg = (double)gi / (double)(L - 1);
+    double Emax = -INFINITY;
+    for (int s = 0; s < L; ++s) {
+        int n = 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) n += (nb[q] == s);
+        const double d = lg - (double)s / (double)(L - 1);
+        Emax = fmax(Emax, p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0));
+    }
+    double Zs = 0.0;
+    for (int s = 0; s < L; ++s) {
+        int n = 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) n += (nb[q] == s);
+        const double d = lg - (double)s / (double)(L - 1);
+        Zs += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
+    }
+    const double target = u * Zs;
+    double F = 0.0;
+    for (int s = 0; s < L - 1; ++s) {
+        int n = 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) n += (nb[q] == s);
+        const double d = lg - (double)s / (double)(L - 1);
+        F += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
+        if (target < F) return s;
+    }
+    return L - 1;
+}
+
+template <int NB, int LT>  // LT: levels known at compile time, 0 = any
+__global__ void __launch_bounds__(GEN_THREADS, 2)
     sweep_general_kernel(const __grid_constant__ GeneralSweepParams p) {
     __shared__ double sA[9];
+    __shared__ double sD[LT > 0 ? LT * LT : 1];
+    __shared__ SiteJob s_jobs[GEN_WARPS][128];
+    __shared__ uint8_t s_res[GEN_WARPS][128];
     if (threadIdx.x < 9) sA[threadIdx.x] = p.A[threadIdx.x];
+    if (LT > 0)
+        for (int i = threadIdx.x; i < LT * LT; i += GEN_THREADS) sD[i] = p.dtab[i];
     __syncthreads();
 
     const Geometry& G = p.c.geo;
     const int L = G.levels;
     const int nquads = (G.W + 3) >> 2;
     const int qd = blockIdx.x * blockDim.x + threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int chain = blockIdx.z;
-    if (qd >= nquads) return;
+    const bool active = qd < nquads;
+    if (__ballot_sync(FULL, active) == 0) return;  // warp-uniform exit
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
-    const double Cw = p.Cw;
-    const double* __restrict__ dtab = p.dtab;
+    const unsigned lt = (1u << lane) - 1u;
+    SiteJob* jobs = s_jobs[warp];
+    uint8_t* res = s_res[warp];
 
     for (int r = p.c.rlo + blockIdx.y; r < p.c.rhi; r += gridDim.y) {
         const int grow = G.row0 + r;
-        const uint8_t* xr = p.c.x_in + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF +
-                            4 * qd;
-        uint32_t up[3], mid[3], dn[3];
+        const int c0 = 4 * qd;
+        const int nvalid = active ? min(4, G.W - c0) : 0;
+        uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0}, gword = 0;
+        uint4 rnd = make_uint4(0, 0, 0, 0);
+        if (active) {
+            const uint8_t* xr = p.c.x_in + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF + c0;
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            up[j] = ldg4(xr - G.xpitch + 4 * (j - 1));
-            mid[j] = ldg4(xr + 4 * (j - 1));
-            dn[j] = ldg4(xr + G.xpitch + 4 * (j - 1));
+            for (int j = 0; j < 3; ++j) {
+                up[j] = ldg4(xr - G.xpitch + 4 * (j - 1));
+                mid[j] = ldg4(xr + 4 * (j - 1));
+                dn[j] = ldg4(xr + G.xpitch + 4 * (j - 1));
+            }
+            gword = ldg4(p.c.g + chain * G.gchain + (long long)r * G.gpitch + c0);
+            rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
         }
-        const uint32_t gword = ldg4(p.c.g + chain * G.gchain + (long long)r * G.gpitch + 4 * qd);
-        const uint4 rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain),
-                                        p.c.keys);
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
         uint32_t outw = 0u;
+        int qpos[4];
+        int qbase = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int pos = 4 + b;  // window position of this site
@@ -81,73 +204,51 @@ __global__ void __launch_bounds__(256)
             }
             const int xi = win_byte(mid, pos);
             const int gi = (int)((gword >> (8 * b)) & 0xFFu);
+            const bool valid = b < nvalid;
             bool uniform = p.uthr != nullptr && xi < L && nb[0] < L;
 #pragma unroll
             for (int j = 1; j < NB; ++j) uniform = uniform && nb[j] == nb[0];
-            if (uniform) {
+            const bool need = valid && !uniform;
+            if (valid && uniform) {
                 // every neighbour carries s* = nb[0] (so all NB exist): integer thresholds
                 const uint32_t* T = p.uthr + (size_t)((nb[0] * L + gi) * L + xi) * (L - 1);
                 int w = 0;
                 for (int k = 0; k < L - 1; ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
                 outw |= (uint32_t)w << (8 * b);
-                continue;
             }
-            const double* Drow = dtab + (size_t)(gi < L ? gi : 0) * L;
-            double Z = 0.0;
-            for (int s = 0; s < L; ++s) {
-                int n = 0;
+            // compact the fp64 sites of the warp into its queue
+            const unsigned m = __ballot_sync(FULL, need);
+            qpos[b] = qbase + __popc(m & lt);
+            if (need) {
+                SiteJob jb;
+                jb.nb_lo = jb.nb_hi = 0u;
 #pragma unroll
-                for (int j = 0; j < NB; ++j) n += (nb[j] == s);
-                Z += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
-            }
-            const double u = (double)rr[b] * (1.0 / 4294967296.0);
-            int w = L - 1;
-            if (Z >= 1e-290 && Z <= 1e290) {
-                const double target = u * Z;
-                double F = 0.0;
-                for (int s = 0; s < L - 1; ++s) {
-                    int n = 0;
-#pragma unroll
-                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
-                    F += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
-                    if (target < F) { w = s; break; }
+                for (int q = 0; q < NB; ++q) {
+                    if (q < 4) jb.nb_lo |= (uint32_t)nb[q] << (8 * q);
+                    else jb.nb_hi |= (uint32_t)nb[q] << (8 * (q - 4));
                 }
+                jb.xg = (uint32_t)xi | ((uint32_t)gi << 8);
+                jb.r = rr[b];
+                jobs[qpos[b]] = jb;
             } else {
-                // Rare slow path (extreme beta, q or sigma: the factorised weights under- or
-                // overflow): E_s = a n_s - b d_s^2 - c 1{s != x_i}, softmax with max subtracted.
-                const double lg = (double)gi / (double)(L - 1);
-                double Emax = -INFINITY;
-                for (int s = 0; s < L; ++s) {
-                    int n = 0;
-#pragma unroll
-                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
-                    const double d = lg - (double)s / (double)(L - 1);
-                    const double E = p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0);
-                    Emax = fmax(Emax, E);
-                }
-                double Zs = 0.0;
-                for (int s = 0; s < L; ++s) {
-                    int n = 0;
-#pragma unroll
-                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
-                    const double d = lg - (double)s / (double)(L - 1);
-                    Zs += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
-                }
-                const double target = u * Zs;
-                double F = 0.0;
-                for (int s = 0; s < L - 1; ++s) {
-                    int n = 0;
-#pragma unroll
-                    for (int j = 0; j < NB; ++j) n += (nb[j] == s);
-                    const double d = lg - (double)s / (double)(L - 1);
-                    F += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
-                    if (target < F) { w = s; break; }
-                }
+                qpos[b] = -1;
             }
-            outw |= (uint32_t)w << (8 * b);
+            qbase += __popc(m);
         }
-        const int c0 = 4 * qd;
-        const int nvalid = min(4, G.W - c0);
+        __syncwarp();
+        for (int i = lane; i < qbase; i += 32) {
+            int w = -1;
+            if (LT > 0) w = decide_fp64_fixed<NB, (LT > 0 ? LT : 2)>(p, sA, sD, jobs[i]);
+            if (w < 0) w = decide_fp64<NB>(p, sA, jobs[i]);
+            res[i] = (uint8_t)w;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if (qpos[b] >= 0) outw |= (uint32_t)res[qpos[b]] << (8 * b);
+        __syncwarp();
+        if (!active) continue;
+
         uint8_t* op = p.c.x_out + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF + c0;
         auto store = [&](uint8_t* dst) {
             if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
@@ -176,13 +277,23 @@ __global__ void __launch_bounds__(256)
 int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream) {
     const Geometry& G = p.c.geo;
     const int nquads = (G.W + 3) / 4;
-    dim3 block(nquads >= 256 ? 256 : ((nquads + 31) / 32) * 32);
     const int nr = p.c.rhi - p.c.rlo;
     if (nr <= 0) return 0;
-    dim3 grid((nquads + block.x - 1) / block.x, nr < 65535 ? nr : 65535, batch);
+    dim3 grid((nquads + GEN_THREADS - 1) / GEN_THREADS, nr < 65535 ? nr : 65535, batch);
     cudaStream_t s = (cudaStream_t)stream;
-    if (G.nbhd == 8) sweep_general_kernel<8><<<grid, block, 0, s>>>(p);
-    else sweep_general_kernel<4><<<grid, block, 0, s>>>(p);
+#define PCA_GEN_LAUNCH(LTV)                                                              \
+    do {                                                                                 \
+        if (G.nbhd == 8) sweep_general_kernel<8, LTV><<<grid, GEN_THREADS, 0, s>>>(p);   \
+        else sweep_general_kernel<4, LTV><<<grid, GEN_THREADS, 0, s>>>(p);               \
+    } while (0)
+    switch (G.levels) {  // the paper's level counts (and 3) get fully unrolled fp64 paths
+        case 3: PCA_GEN_LAUNCH(3); break;
+        case 5: PCA_GEN_LAUNCH(5); break;
+        case 9: PCA_GEN_LAUNCH(9); break;
+        case 16: PCA_GEN_LAUNCH(16); break;
+        default: PCA_GEN_LAUNCH(0); break;
+    }
+#undef PCA_GEN_LAUNCH
     return (int)cudaGetLastError();
 }
 
