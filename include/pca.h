@@ -117,9 +117,10 @@ typedef struct pca_stats {
 } pca_stats;
 
 /* Halo rows of the CURRENT state buffer, for caller-driven (loopback) exchange between
- * strip contexts.  Each pointer is a device pointer to one padded row of `row_bytes`
- * bytes for chain 0; chain b is at + b*chain_stride.  send_top/send_bottom are the
- * context's first/last owned rows, recv_top/recv_bottom the halo rows above/below. */
+ * strip contexts.  Each pointer is a device pointer to a block of `row_bytes` bytes (the
+ * halo depth, 2 padded rows) for chain 0; chain b is at + b*chain_stride.  send_top /
+ * send_bottom are the context's first / last two owned rows, recv_top / recv_bottom the
+ * two halo rows above / below: copy a neighbour's send block onto the matching recv. */
 typedef struct pca_halo {
     uint8_t* send_top;
     uint8_t* send_bottom;

@@ -43,12 +43,16 @@ __device__ __forceinline__ void store16(uint8_t* row, int c0, int n, bool vec, c
     for (int j = 0; j < n; ++j) row[c0 + j] = (uint8_t)byte_of(v, j);
 }
 
-__global__ void __launch_bounds__(TPB) pack_state_kernel(Geometry G, const uint8_t* __restrict__ src,
-                                                         int src_pitch, long long src_chain,
-                                                         uint8_t* __restrict__ xbuf, int* bad) {
+// Rows [0, rows) of a dense / pitched source -> a padded buffer (row j at (j+halo)*dpitch,
+// data column c at XOFF + c), checking every value < levels; on a torus also the column pads
+// and, when the context owns the whole torus, the `halo` wrapped rows (kernels.cuh layout).
+__global__ void __launch_bounds__(TPB) pack_padded_kernel(Geometry G, const uint8_t* __restrict__ src,
+                                                          int src_pitch, long long src_chain,
+                                                          uint8_t* __restrict__ dst, long long dpitch,
+                                                          long long dchain, int halo, int* bad) {
     const int chain = blockIdx.z;
-    const int cx = blockIdx.x * TPB + threadIdx.x;
-    const int c0 = 16 * cx;
+    const int k = blockIdx.x * TPB + threadIdx.x;  // chunk
+    const int c0 = 16 * k;
     if (c0 >= G.W) return;
     const int n = min(16, G.W - c0);
     const bool vec = ((src_pitch | (int)((uintptr_t)src & 15)) & 15) == 0 && (src_chain & 15) == 0;
@@ -61,17 +65,23 @@ __global__ void __launch_bounds__(TPB) pack_state_kernel(Geometry G, const uint8
         for (int j = 0; j < n; ++j) m[j >> 2] |= 0xFFu << (8 * (j & 3));
         found |= any_ge(v.x & m[0], lv4) | any_ge(v.y & m[1], lv4) | any_ge(v.z & m[2], lv4) |
                  any_ge(v.w & m[3], lv4);
-        uint8_t* d = xbuf + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF;
-        store16(d, c0, n, true, v);
-        if (G.periodic) {
-            if (c0 == 0) d[G.W] = (uint8_t)byte_of(v, 0);                        // right halo
-            if (c0 + n == G.W) d[-1] = (uint8_t)byte_of(v, n - 1);               // left halo
-            if (G.self_halo_rows && (r == 0 || r == G.rows - 1)) {
-                uint8_t* h = d + (r == 0 ? 1LL : -1LL) * (long long)G.rows * G.xpitch;
-                store16(h, c0, n, true, v);
-                if (c0 == 0) h[G.W] = (uint8_t)byte_of(v, 0);
-                if (c0 + n == G.W) h[-1] = (uint8_t)byte_of(v, n - 1);
+        uint8_t* rowp = dst + chain * dchain + (long long)(r + halo) * dpitch;
+        auto put = [&](uint8_t* rp) {
+            store16(rp + XOFF, c0, n, true, v);
+            if (G.periodic) {
+                if ((G.W & 15) == 0) {
+                    if (k == 0) *reinterpret_cast<uint4*>(rp + XOFF + G.W) = v;
+                    if (k == G.nchunks - 1) *reinterpret_cast<uint4*>(rp + XOFF - 16) = v;
+                } else {
+                    if (k == 0) rp[XOFF + G.W] = (uint8_t)byte_of(v, 0);
+                    if (k == G.nchunks - 1) rp[XOFF - 1] = (uint8_t)byte_of(v, n - 1);
+                }
             }
+        };
+        put(rowp);
+        if (G.periodic && G.self_halo_rows) {
+            if (r < halo) put(rowp + (long long)G.rows * dpitch);
+            if (r >= G.rows - halo) put(rowp - (long long)G.rows * dpitch);
         }
     }
     if (found) atomicOr(bad, 1);
@@ -85,7 +95,7 @@ __global__ void __launch_bounds__(TPB) unpack_state_kernel(Geometry G, const uin
     const int n = min(16, G.W - c0);
     const bool vec = (G.W & 15) == 0 && ((uintptr_t)dense & 15) == 0;
     for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
-        const uint8_t* s = xbuf + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF;
+        const uint8_t* s = xbuf + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF;
         uint8_t* d = dense + ((long long)chain * G.rows + r) * G.W;
         store16(d, c0, n, vec, load16(s, c0, n, true));
     }
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(TPB) metric_sums_kernel(const MetricParams p) 
     if (n > 0) {
         for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
             const uint4 tv = load16(truth + (long long)r * G.W, c0, n, vec);
-            const uint4 yv = p.kind == 0 ? load16(xb + (long long)(r + 1) * G.xpitch + XOFF, c0, n, true)
+            const uint4 yv = p.kind == 0 ? load16(xb + (long long)(r + HALO) * G.xpitch + XOFF, c0, n, true)
                                          : mpm16(G, cc, r, c0, p.nsamp);
             uint32_t t[6] = {0, 0, 0, 0, 0, 0};  // 16 sites: every partial sum < 2^21
             for (int j = 0; j < n; ++j) {
@@ -252,8 +262,15 @@ inline dim3 chunk_grid(const Geometry& G, int batch, int max_rows = 2048) {
 
 int launch_pack_state(const Geometry& G, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad, void* stream) {
-    pack_state_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(G, src, src_pitch,
-                                                                             src_chain, xbuf, bad);
+    pack_padded_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(
+        G, src, src_pitch, src_chain, xbuf, G.xpitch, G.xchain, HALO, bad);
+    return (int)cudaGetLastError();
+}
+
+int launch_pack_g(const Geometry& G, const uint8_t* src, int src_pitch, long long src_chain,
+                  uint8_t* gbuf, int batch, int* bad, void* stream) {
+    pack_padded_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(
+        G, src, src_pitch, src_chain, gbuf, G.gpitch, G.gchain, GHALO, bad);
     return (int)cudaGetLastError();
 }
 

@@ -2,11 +2,14 @@
 // (runtime.cu) and the device kernels (sweep_binary.cu, sweep_general.cu, aux.cu).
 //
 // HBM layout of one context:
-//   x[2]   : uint8 [batch][rows+2][xpitch]; padded row -1..rows, data column c at byte
-//            XOFF + c; byte XOFF-1 / XOFF+W are the column halos; rows -1 / rows are the
-//            row halos.  Free boundary: halos hold the sentinel 0xFF (never a label).
-//            Torus: halos hold the wrapped labels, rewritten by every sweep.
-//   g      : uint8 [batch][rows][gpitch]   (gpitch = 16*nchunks, padding bytes 0)
+//   x[2]   : uint8 [batch][rows+2*HALO][xpitch], xpitch = 16*nchunks + 32; padded row j in
+//            -HALO..rows+HALO-1 at (j+HALO)*xpitch, data column c at byte XOFF + c; bytes
+//            [0, XOFF) and [XOFF+W, XOFF+W+16) are the column pads.  Free boundary: halos
+//            and pads hold the sentinel 0xFF (never a label).  Torus: halo rows and pads hold
+//            the wrapped labels (16 columns each side when W % 16 == 0, else columns -1 and
+//            W), rewritten by every sweep; other padding bytes are 0.
+//   g      : uint8 [batch][rows+2*GHALO][gpitch], same column layout as x (pads wrapped on a
+//            torus, 0 otherwise); halo rows wrapped on a single-context torus, else 0
 //   counts : uint16, levels == 2: [batch][rows][cpitch] (count of label 1);
 //            levels > 2: [batch][levels][rows][cpitch]  (cpitch = 16*nchunks)
 //   dtab   : fp64 [levels][levels], D[g][s] = exp(-b (lum g - lum s)^2)  (general kernel)
@@ -21,6 +24,8 @@
 namespace pcab200 {
 
 constexpr int XOFF = 16;           // data column 0 sits at byte 16 of a padded row
+constexpr int HALO = 2;            // x halo rows above / below the owned rows
+constexpr int GHALO = 1;           // g halo rows above / below the owned rows
 constexpr int THR_ENTRIES = 324;   // binary thresholds [np 0..8][n1 0..8][g 0..1][x 0..1]
 constexpr uint32_t TAG_PCA = 1u;
 
@@ -92,6 +97,8 @@ int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thre
 int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream);
 int launch_pack_state(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad_flag, void* stream);
+int launch_pack_g(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
+                  uint8_t* gbuf, int batch, int* bad_flag, void* stream);
 int launch_unpack_state(const Geometry& geo, const uint8_t* xbuf, uint8_t* dense, int batch,
                         void* stream);
 int launch_check_levels(const uint8_t* dense, size_t n, int levels, int* bad_flag,

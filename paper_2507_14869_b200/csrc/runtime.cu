@@ -98,6 +98,7 @@ constexpr int UTHR_MAX_LEVELS = 16;
 struct Layout {
     int rows = 0, nchunks = 0, xpitch = 0, gpitch = 0, cpitch = 0, cplanes = 0;
     size_t xbuf = 0;      // bytes of one x buffer
+    size_t gbuf = 0;      // bytes of the g buffer
     size_t off_uthr = 0, uthr_entries = 0;
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_sums = 0,
            off_sums_max = 0, off_flag = 0, off_stage = 0;
@@ -132,6 +133,8 @@ pca_status validate(const pca_config* c) {
         if (c->row0 != 0) return fail(PCA_EINVAL, "rows == 0 (whole lattice) requires row0 == 0");
     } else if (c->rows < 1 || c->row0 < 0 || (long long)c->row0 + c->rows > c->height) {
         return fail(PCA_EINVAL, "owned rows [row0, row0+rows) must lie inside [0, height)");
+    } else if (c->rows < c->height && c->rows < HALO) {
+        return fail(PCA_EINVAL, "a row strip must own at least %d rows (halo depth)", HALO);
     }
     if (c->kernel < 0 || c->kernel > 2) return fail(PCA_EINVAL, "kernel must be 0, 1 or 2");
     if (c->kernel == PCA_KERNEL_BINARY && c->levels != 2)
@@ -149,17 +152,18 @@ Layout make_layout(const pca_config* c) {
     L.rows = c->rows == 0 ? c->height : c->rows;
     L.nchunks = (c->width + 15) / 16;
     L.xpitch = 16 * L.nchunks + 32;
-    L.gpitch = 16 * L.nchunks;
+    L.gpitch = 16 * L.nchunks + 32;
     L.cpitch = 16 * L.nchunks;
     L.cplanes = c->levels == 2 ? 1 : c->levels;
     const size_t B = (size_t)c->batch, R = (size_t)L.rows, W = (size_t)c->width;
-    L.xbuf = B * (R + 2) * (size_t)L.xpitch;
+    L.xbuf = B * (R + 2 * HALO) * (size_t)L.xpitch;
+    L.gbuf = B * (R + 2 * GHALO) * (size_t)L.gpitch;
     L.counts_bytes = B * (size_t)L.cplanes * R * (size_t)L.cpitch * 2;
     L.stage_bytes = B * R * W * 4;  // uint8 images and fp32 planes (one label plane at a time)
     size_t o = 0;
     L.off_x0 = o; o = align256(o + L.xbuf);
     L.off_x1 = o; o = align256(o + L.xbuf);
-    L.off_g = o; o = align256(o + B * R * (size_t)L.gpitch);
+    L.off_g = o; o = align256(o + L.gbuf);
     L.off_counts = o; o = align256(o + L.counts_bytes);
     L.off_dtab = o; o = align256(o + (size_t)c->levels * c->levels * sizeof(double));
     L.uthr_entries = c->levels <= UTHR_MAX_LEVELS
@@ -417,14 +421,15 @@ pca_status exchange(pca_ctx* ctx, uint8_t* buf) {
         if (up < 0) up = -1;
         if (down >= P) down = -1;
     }
-    const size_t rb = (size_t)ctx->lay.xpitch;
+    // HALO consecutive padded rows per message (rows are contiguous in the buffer)
+    const size_t pitch = (size_t)ctx->lay.xpitch, rb = HALO * pitch;
     ncclResult_t e = N.GroupStart();
     for (int b = 0; b < ctx->cfg.batch && e == ncclSuccess; ++b) {
-        uint8_t* base = buf + (size_t)b * ctx->geo.xchain;
-        uint8_t* top = base + rb;
-        uint8_t* bottom = base + (size_t)ctx->lay.rows * rb;
-        uint8_t* halo_top = base;
-        uint8_t* halo_bottom = base + (size_t)(ctx->lay.rows + 1) * rb;
+        uint8_t* base = buf + (size_t)b * ctx->geo.xchain;                       // row -HALO
+        uint8_t* top = base + HALO * pitch;                                       // rows 0..
+        uint8_t* bottom = base + (size_t)ctx->lay.rows * pitch;                   // rows R-HALO..
+        uint8_t* halo_top = base;                                                 // rows -HALO..
+        uint8_t* halo_bottom = base + (size_t)(ctx->lay.rows + HALO) * pitch;     // rows R..
         if (up >= 0 && e == ncclSuccess) e = N.Send(top, rb, ncclUint8, up, ctx->comm, ctx->stream);
         if (down >= 0 && e == ncclSuccess)
             e = N.Recv(halo_bottom, rb, ncclUint8, down, ctx->comm, ctx->stream);
@@ -455,13 +460,14 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
     const pca_config& c = ctx->cfg;
     const Layout& L = ctx->lay;
     if (g) {
-        CK(ctx, cudaMemsetAsync(ctx->g, 0, (size_t)c.batch * L.rows * L.gpitch, ctx->stream));
-        CK(ctx, cudaMemcpy2DAsync(ctx->g, L.gpitch, g, c.width, c.width, (size_t)c.batch * L.rows,
-                                  cudaMemcpyDefault, ctx->stream));
+        const uint8_t* dg = nullptr;
+        pca_status st = device_input(ctx, g, &dg);
+        if (st != PCA_OK) return st;
+        CK(ctx, cudaMemsetAsync(ctx->g, 0, L.gbuf, ctx->stream));
         CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
-        LAUNCH(ctx, launch_check_levels(ctx->g, (size_t)c.batch * L.rows * L.gpitch, c.levels,
-                                        ctx->flag, ctx->stream));
-        pca_status st = check_flag(ctx, "g");
+        LAUNCH(ctx, launch_pack_g(ctx->geo, dg, c.width, (long long)L.rows * c.width, ctx->g,
+                                  c.batch, ctx->flag, ctx->stream));
+        st = check_flag(ctx, "g");
         if (st != PCA_OK) return st;
     }
     // free boundary: halos and padding hold the sentinel 0xFF; torus: halos are rewritten by
@@ -485,7 +491,7 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
         if (st != PCA_OK) return st;
         return load_state(ctx, dx, c.width, (long long)L.rows * c.width, "x0");
     }
-    return load_state(ctx, ctx->g, L.gpitch, (long long)L.rows * L.gpitch, "g");
+    return load_state(ctx, ctx->g + (size_t)GHALO * L.gpitch + XOFF, L.gpitch, ctx->geo.gchain, "g");
 }
 
 }  // namespace
@@ -552,8 +558,8 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     G.xpitch = L.xpitch;
     G.gpitch = L.gpitch;
     G.cpitch = L.cpitch;
-    G.xchain = (long long)(L.rows + 2) * L.xpitch;
-    G.gchain = (long long)L.rows * L.gpitch;
+    G.xchain = (long long)(L.rows + 2 * HALO) * L.xpitch;
+    G.gchain = (long long)(L.rows + 2 * GHALO) * L.gpitch;
     G.cplane = (long long)L.rows * L.cpitch;
     G.cchain = (long long)L.cplanes * L.rows * L.cpitch;
 
@@ -840,12 +846,12 @@ pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out) {
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
     uint8_t* base = ctx->x[ctx->cur];
-    const size_t rb = (size_t)ctx->lay.xpitch;
-    out->send_top = base + rb;
-    out->send_bottom = base + (size_t)ctx->lay.rows * rb;
+    const size_t pitch = (size_t)ctx->lay.xpitch;
+    out->send_top = base + HALO * pitch;
+    out->send_bottom = base + (size_t)ctx->lay.rows * pitch;
     out->recv_top = base;
-    out->recv_bottom = base + (size_t)(ctx->lay.rows + 1) * rb;
-    out->row_bytes = rb;
+    out->recv_bottom = base + (size_t)(ctx->lay.rows + HALO) * pitch;
+    out->row_bytes = HALO * pitch;
     out->chain_stride = (size_t)ctx->geo.xchain;
     return PCA_OK;
 }

@@ -94,11 +94,12 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
     const int ccol = col0 + 16 * lane;      // first column of the chunk
     const uint32_t xbytes = 16 * nch + 32, gbytes = 16 * nch;
     const uint32_t cbytes = p.c.count_enable ? 32 * nch : 0;
-    // padded x row j (-1..rows) starts at (j+1)*xpitch; byte col0 of it is column col0-16
-    const uint8_t* xin = p.c.x_in + chain * G.xchain + col0 + (long long)rbeg * G.xpitch;
-    const uint8_t* gin = p.c.g + chain * G.gchain + col0 + (long long)rbeg * G.gpitch;
+    // padded x row j starts at (j+HALO)*xpitch; byte col0 of it is column col0-16; xin points
+    // at x row rbeg-1 (item 0)
+    const uint8_t* xin = p.c.x_in + chain * G.xchain + col0 + (long long)(rbeg - 1 + HALO) * G.xpitch;
+    const uint8_t* gin = p.c.g + chain * G.gchain + XOFF + col0 + (long long)(rbeg + GHALO) * G.gpitch;
     const uint16_t* cin = p.c.counts + chain * G.cchain + col0 + (long long)rbeg * G.cpitch;
-    uint8_t* xo = p.c.x_out + chain * G.xchain + XOFF + ccol + (long long)(rbeg + 1) * G.xpitch;
+    uint8_t* xo = p.c.x_out + chain * G.xchain + (long long)(rbeg + HALO) * G.xpitch;  // row rbeg
     uint16_t* co = p.c.counts + chain * G.cchain + ccol + (long long)rbeg * G.cpitch;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const uint8_t* thr_b = reinterpret_cast<const uint8_t*>(s_thr);
@@ -201,19 +202,8 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
             cp[1] = c1;
         }
         // ---- store x_{t+1} (+ torus halos) ----
-        const int nvalid = G.W - ccol;
-        uint8_t* op = xo + (long long)(r - rbeg) * G.xpitch;
-        store_chunk(op, O, nvalid);
-        if (PER) {
-            if (k == 0) op[G.W] = chunk_byte(O, 0);                                  // right halo
-            if (k == G.nchunks - 1) op[-ccol - 1] = chunk_byte(O, G.W - 1 - ccol);  // left halo
-            if (G.self_halo_rows && (grow == 0 || grow == G.H - 1)) {
-                uint8_t* hp = op + (grow == 0 ? 1LL : -1LL) * (long long)G.rows * G.xpitch;
-                store_chunk(hp, O, nvalid);
-                if (k == 0) hp[G.W] = chunk_byte(O, 0);
-                if (k == G.nchunks - 1) hp[-ccol - 1] = chunk_byte(O, G.W - 1 - ccol);
-            }
-        }
+        store_row_chunk<HALO, XOFF>(xo + (long long)(r - rbeg) * G.xpitch, O, ccol, G.W - ccol, k, r,
+                                    G.W, G.nchunks, G.rows, G.xpitch, PER, G.self_halo_rows);
     };
 
     // window: A0 = x row r0-1, A1 = x row r0 (previous item), B0 = r0+1, B1 = r0+2 (current)

@@ -176,14 +176,14 @@ __global__ void __launch_bounds__(GEN_THREADS, 2)
         uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0}, gword = 0;
         uint4 rnd = make_uint4(0, 0, 0, 0);
         if (active) {
-            const uint8_t* xr = p.c.x_in + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF + c0;
+            const uint8_t* xr = p.c.x_in + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 up[j] = ldg4(xr - G.xpitch + 4 * (j - 1));
                 mid[j] = ldg4(xr + 4 * (j - 1));
                 dn[j] = ldg4(xr + G.xpitch + 4 * (j - 1));
             }
-            gword = ldg4(p.c.g + chain * G.gchain + (long long)r * G.gpitch + c0);
+            gword = ldg4(p.c.g + chain * G.gchain + (long long)(r + GHALO) * G.gpitch + XOFF + c0);
             rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
         }
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
@@ -249,18 +249,25 @@ __global__ void __launch_bounds__(GEN_THREADS, 2)
         __syncwarp();
         if (!active) continue;
 
-        uint8_t* op = p.c.x_out + chain * G.xchain + (long long)(r + 1) * G.xpitch + XOFF + c0;
+        uint8_t* op = p.c.x_out + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
         auto store = [&](uint8_t* dst) {
             if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
             else for (int b = 0; b < nvalid; ++b) dst[b] = (uint8_t)(outw >> (8 * b));
-            if (G.periodic) {
-                if (c0 == 0) dst[G.W] = (uint8_t)outw;
-                if (c0 + nvalid == G.W) dst[-c0 - 1] = (uint8_t)(outw >> (8 * (nvalid - 1)));
+            if (G.periodic) {  // column pads (see kernels.cuh)
+                if ((G.W & 15) == 0) {
+                    if (c0 < 16) *reinterpret_cast<uint32_t*>(dst + G.W) = outw;
+                    if (c0 >= G.W - 16) *reinterpret_cast<uint32_t*>(dst - G.W) = outw;
+                } else {
+                    if (c0 == 0) dst[G.W] = (uint8_t)outw;
+                    if (c0 + nvalid == G.W) dst[-c0 - 1] = (uint8_t)(outw >> (8 * (nvalid - 1)));
+                }
             }
         };
         store(op);
-        if (G.periodic && G.self_halo_rows && (grow == 0 || grow == G.H - 1))
-            store(op + (grow == 0 ? 1LL : -1LL) * (long long)G.rows * G.xpitch);
+        if (G.periodic && G.self_halo_rows) {
+            if (r < HALO) store(op + (long long)G.rows * G.xpitch);
+            if (r >= G.rows - HALO) store(op - (long long)G.rows * G.xpitch);
+        }
         if (p.c.count_enable) {
             uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
             for (int b = 0; b < nvalid; ++b) {

@@ -70,4 +70,33 @@ __device__ __forceinline__ void store_chunk(uint8_t* op, const uint32_t (&o)[4],
     }
 }
 
+// Store the 16-site chunk o (first column ccol, nvalid sites, chunk index k) of local row r
+// into a padded state buffer whose row r starts at rowp, plus the torus halo copies: the
+// column pads (16 wrapped columns each side when W % 16 == 0, else columns -1 and W) and,
+// when this context owns the whole torus, the HALO wrapped rows above and below.
+template <int HALO_ROWS, int XOFFB>
+__device__ __forceinline__ void store_row_chunk(uint8_t* rowp, const uint32_t (&o)[4], int ccol,
+                                                int nvalid, int k, int r, int W, int nchunks,
+                                                int rows, long long pitch, bool periodic,
+                                                bool self_halo_rows) {
+    auto put = [&](uint8_t* rp) {
+        store_chunk(rp + XOFFB + ccol, o, nvalid);
+        if (periodic) {
+            if ((W & 15) == 0) {
+                const uint4 v = make_uint4(o[0], o[1], o[2], o[3]);
+                if (k == 0) *reinterpret_cast<uint4*>(rp + XOFFB + W) = v;       // cols 0..15
+                if (k == nchunks - 1) *reinterpret_cast<uint4*>(rp + XOFFB - 16) = v;  // W-16..W-1
+            } else {
+                if (k == 0) rp[XOFFB + W] = chunk_byte(o, 0);
+                if (k == nchunks - 1) rp[XOFFB - 1] = chunk_byte(o, W - 1 - ccol);
+            }
+        }
+    };
+    put(rowp);
+    if (periodic && self_halo_rows) {
+        if (r < HALO_ROWS) put(rowp + (long long)rows * pitch);
+        if (r >= rows - HALO_ROWS) put(rowp - (long long)rows * pitch);
+    }
+}
+
 }  // namespace pcab200
