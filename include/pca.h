@@ -103,7 +103,10 @@ typedef struct pca_config {
     int32_t rows;          /* owned rows; 0 means all H rows (row0 must then be 0)            */
     int32_t kernel;        /* PCA_KERNEL_*                                                     */
     int32_t rows_per_thread; /* binary kernel: rows per warp task; 0 = auto (one wave)       */
-    int32_t reserved[7];   /* must be zero                                                     */
+    int32_t sweeps_per_pass; /* 0 = auto (1); 1 = one sweep per kernel launch; 2 = two      */
+                           /* sweeps per HBM pass (temporal blocking; same chain) when       */
+                           /* levels == 2, W % 16 == 0 and the context owns the whole lattice */
+    int32_t reserved[6];   /* must be zero                                                     */
 } pca_config;
 
 typedef struct pca_stats {

@@ -68,6 +68,14 @@ struct BinarySweepParams {
     uint32_t thr[THR_ENTRIES];
 };
 
+// two sweeps (t, t+1) per pass: thr[0] for sweep t, thr[1] for sweep t+1; c.count_enable
+// counts sweep t, count2 sweep t+1.
+struct Binary2SweepParams {
+    SweepCommon c;
+    int count2;
+    uint32_t thr[2][THR_ENTRIES];
+};
+
 // general path: A[n] = exp(a n), Cw = exp(-c); D table in global memory.  a, b, c feed
 // the log-domain slow path used when the factorised weights under/overflow.
 // uthr[((s*L + g)*L + x)*(L-1) + k] = ceil(F_k 2^32) - 1: the integer thresholds of a site
@@ -95,6 +103,7 @@ struct MetricParams {
 int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread,
                         void* stream);
 int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream);
+int launch_sweep_binary2(const Binary2SweepParams& p, int batch, int rows_per_thread, void* stream);
 int launch_pack_state(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad_flag, void* stream);
 int launch_pack_g(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,

@@ -142,7 +142,9 @@ pca_status validate(const pca_config* c) {
     const int R = c->rows_per_thread;
     if (R < 0 || R > 65536)
         return fail(PCA_EINVAL, "rows_per_thread must be in [0, 65536] (0 = auto)");
-    for (int i = 0; i < 7; ++i)
+    if (c->sweeps_per_pass < 0 || c->sweeps_per_pass > 2)
+        return fail(PCA_EINVAL, "sweeps_per_pass must be 0, 1 or 2");
+    for (int i = 0; i < 6; ++i)
         if (c->reserved[i] != 0) return fail(PCA_EINVAL, "reserved fields must be zero");
     return PCA_OK;
 }
@@ -204,6 +206,7 @@ struct pca_ctx {
     int x_initialized = 0;
     int64_t tab_stage = -1;
     BinarySweepParams bin;
+    Binary2SweepParams bin2;
     GeneralSweepParams gen;
     std::vector<double> dtab_host;
     std::vector<uint32_t> uthr_host;
@@ -406,10 +409,10 @@ void fill_common(pca_ctx* ctx, SweepCommon& sc, int64_t t, int count) {
 }
 
 // Halo exchange of buffer `buf` with the neighbouring ranks (row strips): send the first
-// owned row up and the last owned row down, receive the halo rows.  Order per chain:
+// `depth` owned rows up and the last `depth` down, receive the halo rows.  Order per chain:
 // send(top->up), recv(bottom halo<-down), send(bottom->down), recv(top halo<-up); with
 // 2 ranks on a torus both neighbours are the same peer and NCCL matches in issue order.
-pca_status exchange(pca_ctx* ctx, uint8_t* buf) {
+pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
     if (!ctx->comm || ctx->nranks <= 1) return PCA_OK;
     NcclApi& N = nccl();
     const int P = ctx->nranks, r = ctx->rank;
@@ -421,15 +424,16 @@ pca_status exchange(pca_ctx* ctx, uint8_t* buf) {
         if (up < 0) up = -1;
         if (down >= P) down = -1;
     }
-    // HALO consecutive padded rows per message (rows are contiguous in the buffer)
-    const size_t pitch = (size_t)ctx->lay.xpitch, rb = HALO * pitch;
+    // `depth` consecutive padded rows per message (rows are contiguous in the buffer)
+    const size_t pitch = (size_t)ctx->lay.xpitch, rb = (size_t)depth * pitch;
+    const size_t R = (size_t)ctx->lay.rows;
     ncclResult_t e = N.GroupStart();
     for (int b = 0; b < ctx->cfg.batch && e == ncclSuccess; ++b) {
         uint8_t* base = buf + (size_t)b * ctx->geo.xchain;                       // row -HALO
         uint8_t* top = base + HALO * pitch;                                       // rows 0..
-        uint8_t* bottom = base + (size_t)ctx->lay.rows * pitch;                   // rows R-HALO..
-        uint8_t* halo_top = base;                                                 // rows -HALO..
-        uint8_t* halo_bottom = base + (size_t)(ctx->lay.rows + HALO) * pitch;     // rows R..
+        uint8_t* bottom = base + (HALO + R - depth) * pitch;                      // rows R-depth..
+        uint8_t* halo_top = base + (HALO - depth) * pitch;                        // rows -depth..
+        uint8_t* halo_bottom = base + (HALO + R) * pitch;                         // rows R..
         if (up >= 0 && e == ncclSuccess) e = N.Send(top, rb, ncclUint8, up, ctx->comm, ctx->stream);
         if (down >= 0 && e == ncclSuccess)
             e = N.Recv(halo_bottom, rb, ncclUint8, down, ctx->comm, ctx->stream);
@@ -602,12 +606,43 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     if (strip && !ctx->comm && n > 1)
         return fail(PCA_EINVAL,
                     "a strip context without NCCL sweeps one step at a time (caller exchanges halos)");
+    // two sweeps per HBM pass (sweep_binary2.cu, opt-in): levels == 2, whole lattice,
+    // W % 16 == 0.  Measured slower than one sweep per pass on B200.
+    const bool pairs = ctx->kernel == PCA_KERNEL_BINARY && !strip && (ctx->cfg.width % 16) == 0 &&
+                       ctx->cfg.sweeps_per_pass == 2;
+    auto counts_at = [&](int64_t t) {
+        return (ctx->cfg.mpm_burn_in >= 0 && t >= ctx->cfg.mpm_burn_in) ? 1 : 0;
+    };
     for (int32_t i = 0; i < n; ++i) {
         const int64_t t = ctx->t;
         if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
+        if (pairs && i + 1 < n && t + 1 < (int64_t)0xFFFFFFFFLL) {
+            const int c0 = counts_at(t), c1 = counts_at(t + 1);
+            if (ctx->counted + c0 + c1 > 65535)
+                return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+            st = build_tables(ctx, t);
+            if (st != PCA_OK) return st;
+            memcpy(ctx->bin2.thr[0], ctx->bin.thr, sizeof(ctx->bin.thr));
+            st = build_tables(ctx, t + 1);
+            if (st != PCA_OK) return st;
+            memcpy(ctx->bin2.thr[1], ctx->bin.thr, sizeof(ctx->bin.thr));
+            fill_common(ctx, ctx->bin2.c, t, c0);
+            ctx->bin2.count2 = c1;
+            ctx->bin2.c.rlo = 0;
+            ctx->bin2.c.rhi = ctx->lay.rows;
+            ctx->launches++;
+            ctx->sweep_launches++;
+            const int e = launch_sweep_binary2(ctx->bin2, ctx->cfg.batch, 0, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (two per pass)");
+            ctx->cur ^= 1;
+            ctx->t = t + 2;
+            ctx->counted += c0 + c1;
+            ++i;
+            continue;
+        }
         st = build_tables(ctx, t);
         if (st != PCA_OK) return st;
-        const int count = (ctx->cfg.mpm_burn_in >= 0 && t >= ctx->cfg.mpm_burn_in) ? 1 : 0;
+        const int count = counts_at(t);
         if (count && ctx->counted + 1 > 65535)
             return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
         fill_common(ctx, ctx->bin.c, t, count);
@@ -641,7 +676,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             e = launch_rows(0, 1, ctx->stream);
             if (!e) e = launch_rows(R - 1, R, ctx->stream);
             if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (edge rows)");
-            st = exchange(ctx, ctx->x[ctx->cur ^ 1]);
+            st = exchange(ctx, ctx->x[ctx->cur ^ 1], 1);  // only the finished edge rows
             if (st != PCA_OK) return st;
             e = launch_rows(1, R - 1, ctx->side);
             if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (interior rows)");

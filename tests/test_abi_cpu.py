@@ -34,9 +34,9 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_config_struct_layout_matches_header():
-    # 6 int32, 5 double, 2 int32, double, uint64, 5 int32, 7 int32 reserved (natural alignment)
+    # 6 int32, 5 double, 2 int32, double, uint64, 6 int32, 6 int32 reserved (natural alignment)
     assert ctypes.sizeof(P.pca_config) == 24 + 40 + 8 + 8 + 8 + 20 + 28
-    assert P.pca_config.seed.offset == 80 and P.pca_config.reserved.offset == 108
+    assert P.pca_config.seed.offset == 80 and P.pca_config.reserved.offset == 112
 
 
 def test_workspace_and_validation(lib):
@@ -54,6 +54,9 @@ def test_workspace_and_validation(lib):
         cfg = P.make_config(args.pop("height"), args.pop("width"), args.pop("levels"), **args)
         assert lib.pca_workspace_bytes(ctypes.byref(cfg)) == 0, kw
         assert lib.pca_last_error().decode(), kw
+    c = P.make_config(64, 64, 2)
+    c.sweeps_per_pass = 3
+    assert lib.pca_workspace_bytes(ctypes.byref(c)) == 0
     c = P.make_config(64, 64, 2)
     c.reserved[3] = 1
     assert lib.pca_workspace_bytes(ctypes.byref(c)) == 0
