@@ -50,14 +50,14 @@ class Model(ctypes.Structure):
         ("H", ctypes.c_int), ("W", ctypes.c_int), ("levels", ctypes.c_int),
         ("nbhd", ctypes.c_int), ("periodic", ctypes.c_int),
         ("J", ctypes.c_double), ("q", ctypes.c_double), ("sigma", ctypes.c_double),
-        ("coef_scale", ctypes.c_double),
+        ("coef_scale", ctypes.c_double), ("inertia_p", ctypes.c_int),
     ]
 
 
 def model(H, W, levels, nbhd=8, periodic=False, J=1.0 / 3.0, q=0.51, sigma=0.25,
-          coef_scale=1.0) -> Model:
+          coef_scale=1.0, inertia_p=0) -> Model:
     return Model(int(H), int(W), int(levels), int(nbhd), int(bool(periodic)), float(J),
-                 float(q), float(sigma), float(coef_scale))
+                 float(q), float(sigma), float(coef_scale), int(inertia_p))
 
 
 _lib = None

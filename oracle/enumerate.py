@@ -83,6 +83,15 @@ def _dist2(lat: Lattice, g: np.ndarray) -> np.ndarray:
     return (L[np.asarray(g).reshape(-1)][:, None] - L[None, :]) ** 2
 
 
+def inertia_penalty(lat: Lattice, p: int = 0) -> np.ndarray:
+    """pen[x, s] = |lum x - lum s|^p with 0^0 = 0 (p = 0 is the paper's L0)."""
+    L = luminance(lat.levels)
+    d = np.abs(L[:, None] - L[None, :])
+    pen = (d > 0).astype(float) if p == 0 else d ** p
+    np.fill_diagonal(pen, 0.0)
+    return pen
+
+
 def _ncount(lat: Lattice, nbrs, x) -> np.ndarray:
     """cnt[i, s] = n_i(s; x)."""
     cnt = np.zeros((lat.n, lat.levels))
@@ -92,26 +101,26 @@ def _ncount(lat: Lattice, nbrs, x) -> np.ndarray:
     return cnt
 
 
-def site_laws(lat: Lattice, x, g, a, b, c, inertia=True) -> np.ndarray:
-    """p[i, s] for every site: softmax_s(a n_i(s;x) - b d_i(s)^2 - c 1{s != x_i})."""
+def site_laws(lat: Lattice, x, g, a, b, c, inertia=True, p=0) -> np.ndarray:
+    """p[i, s] for every site: softmax_s(a n_i(s;x) - b d_i(s)^2 - c |x_i - s|^p)."""
     nbrs = lat.neighbours()
     x = np.asarray(x).reshape(-1)
     E = a * _ncount(lat, nbrs, x) - b * _dist2(lat, g)
     if inertia:
-        E = E - c * (np.arange(lat.levels)[None, :] != x[:, None])
+        E = E - c * inertia_penalty(lat, p)[x]
     E = E - E.max(axis=1, keepdims=True)
     p = np.exp(E)
     return p / p.sum(axis=1, keepdims=True)
 
 
-def pca_matrix(lat: Lattice, g, a, b, c) -> np.ndarray:
+def pca_matrix(lat: Lattice, g, a, b, c, p=0) -> np.ndarray:
     """P[x, w] = prod_i p_i(w_i; x)."""
     S = lat.states()
     P = np.empty((len(S), len(S)))
     idx = np.arange(lat.n)
     for k, x in enumerate(S):
-        p = site_laws(lat, x, g, a, b, c)
-        P[k] = np.prod(p[idx[None, :], S], axis=1)
+        laws = site_laws(lat, x, g, a, b, c, p=p)
+        P[k] = np.prod(laws[idx[None, :], S], axis=1)
     return P
 
 
@@ -141,26 +150,28 @@ def gibbs_posterior(lat: Lattice, g, a, b) -> np.ndarray:
     return w / w.sum()
 
 
-def pca_closed_form(lat: Lattice, g, a, b, c) -> np.ndarray:
-    """pi~(x) ∝ exp(-D(x)) prod_i Z_i(x), Z_i(x) = sum_s exp(a n_i(s;x) - b d_i(s)^2 - c 1{s!=x_i})."""
+def pca_closed_form(lat: Lattice, g, a, b, c, p=0) -> np.ndarray:
+    """pi~(x) ∝ exp(-D(x)) prod_i Z_i(x), Z_i(x) = sum_s exp(a n_i(s;x) - b d_i(s)^2 - c |x_i-s|^p)."""
     nbrs = lat.neighbours()
     S = lat.states()
     d2 = _dist2(lat, g)
+    pen = inertia_penalty(lat, p)
     logw = np.empty(len(S))
     for k, x in enumerate(S):
-        E = a * _ncount(lat, nbrs, x) - b * d2 - c * (np.arange(lat.levels)[None, :] != x[:, None])
+        E = a * _ncount(lat, nbrs, x) - b * d2 - c * pen[x]
         logZ = np.log(np.exp(E).sum(axis=1)).sum()
         logw[k] = -data_term(lat, x, g, b) + logZ
     w = np.exp(logw - logw.max())
     return w / w.sum()
 
 
-def pca_double_sum(lat: Lattice, g, a, b, c) -> np.ndarray:
+def pca_double_sum(lat: Lattice, g, a, b, c, p=0) -> np.ndarray:
     """pi(x) = sum_w exp(-H^(x,w)) / sum_{x,w} exp(-H^(x,w)) for
     H^(x, w) = -S(x, w) + D(x) + D(w),
-    S(x, w) = a sum_i sum_{j in N(i)} 1{w_i = x_j} - c sum_i 1{w_i != x_i}."""
+    S(x, w) = a sum_i sum_{j in N(i)} 1{w_i = x_j} - c sum_i |w_i - x_i|^p."""
     nbrs = lat.neighbours()
     S = lat.states()
+    pen = inertia_penalty(lat, p)
     D = np.array([data_term(lat, x, g, b) for x in S])
     Hm = np.empty((len(S), len(S)))
     for k, x in enumerate(S):
@@ -168,7 +179,7 @@ def pca_double_sum(lat: Lattice, g, a, b, c) -> np.ndarray:
         for i in range(lat.n):
             for j in nbrs[i]:
                 s_xw += a * (S[:, i] == x[j])
-            s_xw -= c * (S[:, i] != x[i])
+            s_xw -= c * pen[x[i], S[:, i]]
         Hm[k] = -s_xw + D[k] + D
     M = np.exp(-(Hm - Hm.min()))
     return M.sum(axis=1) / M.sum(), Hm

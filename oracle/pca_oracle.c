@@ -88,9 +88,20 @@ typedef struct {
     double q;          /* inertia, PAPER.md:455, 508 (q = 0.51)                     */
     double sigma;      /* noise std in luminance units            */
     double coef_scale; /* 1.0 = paper-literal a, b; 0.5 = matched mode (R4)        */
+    int inertia_p;     /* inertia norm exponent p in {0, 1, 2}  */
 } orc_model;
 
 static double lum(int k, int levels) { return (double)k / (double)(levels - 1); }
+
+/* Inertia penalty |x_i - s|^p on luminances with the convention 0^0 = 0 (PAPER.md:279:
+ * "q ||x - w|| = sum_i q |x_i - w_i|^p ... 0^0 = 0"; L0 is the paper's choice, PAPER.md:455,
+ * L1 / L2 the alternatives of PAPER.md:483-485).                                   */
+static double inertia_penalty(int p, int xi, int s, int levels) {
+    if (s == xi) return 0.0;
+    if (p == 0) return 1.0;
+    double d = lum(xi, levels) - lum(s, levels);
+    return p == 1 ? fabs(d) : d * d;
+}
 
 /* Is (p, q) in F(r, c)?  PAPER.md:356-357: max(|r-p|, |c-q|) = 1 (Moore), or the
  * 4-neighbour variant |r-p| + |c-q| = 1.  Offsets are tested one at a time.      */
@@ -136,7 +147,7 @@ static void site_probs(const orc_model* m, const uint8_t* x, const uint8_t* g, i
     double Emax = -INFINITY;
     for (int s = 0; s < m->levels; s++) {
         double d = lum(gi, m->levels) - lum(s, m->levels);
-        double inert = (with_inertia && s != xi) ? 1.0 : 0.0;
+        double inert = with_inertia ? inertia_penalty(m->inertia_p, xi, s, m->levels) : 0.0;
         E[s] = a * (double)n[s] - b * d * d - cq * inert;
         if (E[s] > Emax) Emax = E[s];
     }

@@ -171,3 +171,31 @@ def test_large_q_freezes():
 def test_tv_arithmetic():
     assert en.tv([0.5, 0.5], [0.9, 0.1]) == pytest.approx(0.4, abs=1e-15)
     assert en.tv([1, 0], [0, 1]) == 1.0
+
+
+@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("lat,g", [(en.Lattice(2, 2, 3, nbhd=8), np.array([0, 2, 1, 2])),
+                                   (en.Lattice(1, 3, 4, nbhd=8), np.array([3, 0, 2])),
+                                   (en.Lattice(2, 3, 3, nbhd=4), np.array([2, 0, 1, 1, 2, 0]))])
+def test_l1_l2_inertia_keep_the_closed_form(lat, g, p):
+    """PAPER.md:279 / 483-485: the inertia q sum_i |x_i - w_i|^p (p = 1, 2) is symmetric in
+    (x, w), so the stationary law is still exp(-D) prod_i Z_i."""
+    a, b, c = en.coefficients(1.25, 1 / 3, 0.9, 0.4)
+    P = en.pca_matrix(lat, g, a, b, c, p=p)
+    cf = en.pca_closed_form(lat, g, a, b, c, p=p)
+    assert en.tv(en.stationary(P), cf) < 1e-10
+    assert en.detailed_balance_residual(cf, P) < 1e-15
+    ds, Hm = en.pca_double_sum(lat, g, a, b, c, p=p)
+    assert np.abs(Hm - Hm.T).max() < 1e-12 and en.tv(ds, cf) < 1e-12
+    P0 = en.pca_matrix(lat, g, a, b, c, p=0)
+    assert np.abs(P - P0).max() > 1e-3  # the norm matters for l > 2
+
+
+def test_inertia_norm_irrelevant_for_two_levels():
+    """For l = 2 every change costs |1 - 0|^p = 1: L0, L1 and L2 inertia coincide."""
+    lat = en.Lattice(3, 3, 2, nbhd=8)
+    g = RNG.integers(0, 2, 9)
+    a, b, c = en.coefficients(1.25, 1 / 3, 0.51, 0.5)
+    P0 = en.pca_matrix(lat, g, a, b, c, p=0)
+    for p in (1, 2):
+        assert np.abs(en.pca_matrix(lat, g, a, b, c, p=p) - P0).max() == 0.0

@@ -90,16 +90,18 @@ CASES = [
 
 
 @pytest.mark.parametrize("case", CASES)
-def test_site_laws_match_enumeration(case):
-    """C per-site PCA and Gibbs conditionals == enumerate.site_laws (independent code)."""
+@pytest.mark.parametrize("pexp", [0, 1, 2])
+def test_site_laws_match_enumeration(case, pexp):
+    """C per-site PCA and Gibbs conditionals == enumerate.site_laws (independent code), for
+    the L0 inertia of the paper and the L1 / L2 alternatives."""
     rng = np.random.default_rng(7)
     lat = en.Lattice(case["H"], case["W"], case["levels"], case["nbhd"], case["periodic"])
-    m = orc.model(**case, J=1 / 3, q=0.51, sigma=0.3)
+    m = orc.model(**case, J=1 / 3, q=0.51, sigma=0.3, inertia_p=pexp)
     for beta in (0.7, 1.25, 2.0):
         x = rng.integers(0, case["levels"], (case["H"], case["W"]), dtype=np.uint8)
         g = rng.integers(0, case["levels"], (case["H"], case["W"]), dtype=np.uint8)
         a, b, c = en.coefficients(beta, 1 / 3, 0.51, 0.3)
-        ref = en.site_laws(lat, x.reshape(-1), g.reshape(-1), a, b, c)
+        ref = en.site_laws(lat, x.reshape(-1), g.reshape(-1), a, b, c, p=pexp)
         refg = en.site_laws(lat, x.reshape(-1), g.reshape(-1), a, b, c, inertia=False)
         for r in range(case["H"]):
             for cc in range(case["W"]):
