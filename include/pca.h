@@ -5,8 +5,10 @@
  * The library samples the lazy Probabilistic Cellular Automaton of PAPER.md section 5.2
  * (transition display PAPER.md:462-477): at every sweep t each site i
  * of the lattice independently draws its new gray level w_i with probability
- *     p_i(s; x) ∝ exp( a*n_i(s;x) - b*(lum g_i - lum s)^2 - c*1{s != x_i} ),
+ *     p_i(s; x) ∝ exp( a*n_i(s;x) - b*(lum g_i - lum s)^2 - c*pen(x_i, s) ),
  *     a = coef_scale*2*beta_t*J,  b = coef_scale/(2 sigma^2),  c = beta_t*q,
+ *     pen = 1{s != x_i} (L0, the paper's), or |lum x_i - lum s|^p for p = 1, 2 (the
+ *     L1 / L2 alternatives of PAPER.md:279 and 483-485; see inertia_p),
  *     beta_t = beta0 + beta_step*floor(t/beta_period),
  * from the PREVIOUS configuration x (double buffering), where n_i(s;x) is
  * the number of neighbours (Moore-8, or von Neumann-4) carrying s and
@@ -106,7 +108,10 @@ typedef struct pca_config {
     int32_t sweeps_per_pass; /* 0 = auto (1); 1 = one sweep per kernel launch; 2 = two      */
                            /* sweeps per HBM pass (temporal blocking; same chain) when       */
                            /* levels == 2, W % 16 == 0 and the context owns the whole lattice */
-    int32_t reserved[6];   /* must be zero                                                     */
+    int32_t inertia_p;     /* inertia norm p: 0 = L0 1{s != x_i} (paper), 1 = |lum x_i - lum s|,*/
+                           /* 2 = (lum x_i - lum s)^2; identical for   */
+                           /* levels == 2                                                      */
+    int32_t reserved[5];   /* must be zero                                                     */
 } pca_config;
 
 typedef struct pca_stats {

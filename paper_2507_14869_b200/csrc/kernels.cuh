@@ -76,7 +76,8 @@ struct Binary2SweepParams {
     uint32_t thr[2][THR_ENTRIES];
 };
 
-// general path: A[n] = exp(a n), Cw = exp(-c); D table in global memory.  a, b, c feed
+// general path: A[n] = exp(a n), Cw = exp(-c) (L0 inertia); D table in global memory;
+// itab[x][s] = exp(-c pen(x, s)) for the L1 / L2 inertia (inertia_p = 1, 2).  a, b, c feed
 // the log-domain slow path used when the factorised weights under/overflow.
 // uthr[((s*L + g)*L + x)*(L-1) + k] = ceil(F_k 2^32) - 1: the integer thresholds of a site
 // whose neighbours all carry s (nullptr when L > 16).
@@ -86,6 +87,8 @@ struct GeneralSweepParams {
     double Cw;
     double coef_a, coef_b, coef_c;
     const double* dtab;
+    const double* itab;
+    int inertia_p;
     const uint32_t* uthr;
 };
 

@@ -100,7 +100,7 @@ struct Layout {
     size_t xbuf = 0;      // bytes of one x buffer
     size_t gbuf = 0;      // bytes of the g buffer
     size_t off_uthr = 0, uthr_entries = 0;
-    size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_sums = 0,
+    size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
            off_sums_max = 0, off_flag = 0, off_stage = 0;
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
 };
@@ -144,7 +144,9 @@ pca_status validate(const pca_config* c) {
         return fail(PCA_EINVAL, "rows_per_thread must be in [0, 65536] (0 = auto)");
     if (c->sweeps_per_pass < 0 || c->sweeps_per_pass > 2)
         return fail(PCA_EINVAL, "sweeps_per_pass must be 0, 1 or 2");
-    for (int i = 0; i < 6; ++i)
+    if (c->inertia_p < 0 || c->inertia_p > 2)
+        return fail(PCA_EINVAL, "inertia_p must be 0 (L0), 1 (L1) or 2 (L2)");
+    for (int i = 0; i < 5; ++i)
         if (c->reserved[i] != 0) return fail(PCA_EINVAL, "reserved fields must be zero");
     return PCA_OK;
 }
@@ -168,6 +170,7 @@ Layout make_layout(const pca_config* c) {
     L.off_g = o; o = align256(o + L.gbuf);
     L.off_counts = o; o = align256(o + L.counts_bytes);
     L.off_dtab = o; o = align256(o + (size_t)c->levels * c->levels * sizeof(double));
+    L.off_itab = o; o = align256(o + (size_t)c->levels * c->levels * sizeof(double));
     L.uthr_entries = c->levels <= UTHR_MAX_LEVELS
                          ? (size_t)c->levels * c->levels * c->levels * (c->levels - 1) : 0;
     L.off_uthr = o; o = align256(o + L.uthr_entries * sizeof(uint32_t));
@@ -194,6 +197,7 @@ struct pca_ctx {
     uint8_t* g = nullptr;
     uint16_t* counts = nullptr;
     double* dtab = nullptr;
+    double* itab = nullptr;  // I[x][s] = exp(-c pen(x, s)), per beta stage (inertia_p > 0)
     unsigned long long* sums = nullptr;
     unsigned long long* sums_max = nullptr;
     int* flag = nullptr;
@@ -208,7 +212,7 @@ struct pca_ctx {
     BinarySweepParams bin;
     Binary2SweepParams bin2;
     GeneralSweepParams gen;
-    std::vector<double> dtab_host;
+    std::vector<double> dtab_host, itab_host;
     std::vector<uint32_t> uthr_host;
     uint32_t* uthr = nullptr;
     ncclComm_t comm = nullptr;
@@ -300,6 +304,15 @@ double beta_at(const pca_config& c, int64_t t) {
 
 double lum(int k, int levels) { return (double)k / (double)(levels - 1); }
 
+// inertia penalty pen(x, s): 0 when s == x, else 1 (L0, the paper's),
+// |lum x - lum s| (L1) or (lum x - lum s)^2 (L2)
+double inertia_pen(int p, int x, int s, int levels) {
+    if (s == x) return 0.0;
+    if (p == 0) return 1.0;
+    const double d = lum(x, levels) - lum(s, levels);
+    return p == 1 ? fabs(d) : d * d;
+}
+
 // a1: per-stage tables.  The binary thresholds repeat the per-site law of PAPER.md:462-477
 // in fp64 exactly as written (E = a n - b d^2 - c 1{s != x}; p0 = e0/(e0 + e1) with the
 // max subtracted), so T = ceil(p0 2^32) is the integer form of "u < F_0".
@@ -325,7 +338,7 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
                         double E[2];
                         for (int s = 0; s < 2; ++s) {
                             const double d = lum(gl, 2) - lum(s, 2);
-                            const double inert = (s != xl) ? 1.0 : 0.0;
+                            const double inert = inertia_pen(c.inertia_p, xl, s, 2);
                             E[s] = a * (double)n[s] - b * d * d - cq * inert;
                         }
                         double Emax = -INFINITY;
@@ -348,6 +361,15 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
         m.coef_a = a;
         m.coef_b = b;
         m.coef_c = cq;
+        if (c.inertia_p != 0) {
+            const int L = c.levels;
+            for (int xl = 0; xl < L; ++xl)
+                for (int s = 0; s < L; ++s)
+                    ctx->itab_host[(size_t)xl * L + s] = exp(-cq * inertia_pen(c.inertia_p, xl, s, L));
+            CK(ctx, cudaMemcpyAsync(ctx->itab, ctx->itab_host.data(),
+                                    ctx->itab_host.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+        }
         if (ctx->lay.uthr_entries) {
             // uniform neighbourhood (all NB neighbours carry s*): the oracle's per-site law
             // (max-subtracted softmax, ascending cumulative sum) in the same fp64 order, and
@@ -361,7 +383,7 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
                         double Emax = -INFINITY;
                         for (int s = 0; s < L; ++s) {
                             const double d = lum(gl, L) - lum(s, L);
-                            const double inert = (s != xl) ? 1.0 : 0.0;
+                            const double inert = inertia_pen(c.inertia_p, xl, s, L);
                             const int n = (s == s0) ? NB : 0;
                             E[s] = a * (double)n - b * d * d - cq * inert;
                             if (E[s] > Emax) Emax = E[s];
@@ -538,6 +560,8 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->g = ctx->ws + L.off_g;
     ctx->counts = (uint16_t*)(ctx->ws + L.off_counts);
     ctx->dtab = (double*)(ctx->ws + L.off_dtab);
+    ctx->itab = (double*)(ctx->ws + L.off_itab);
+    ctx->itab_host.resize((size_t)cfg->levels * cfg->levels);
     ctx->sums = (unsigned long long*)(ctx->ws + L.off_sums);
     ctx->sums_max = (unsigned long long*)(ctx->ws + L.off_sums_max);
     ctx->flag = (int*)(ctx->ws + L.off_flag);
@@ -576,6 +600,8 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
             ctx->dtab_host[(size_t)gl * cfg->levels + s] = exp(-b * d * d);
         }
     ctx->gen.dtab = ctx->dtab;
+    ctx->gen.itab = ctx->itab;
+    ctx->gen.inertia_p = cfg->inertia_p;
     ctx->gen.uthr = ctx->uthr;
 
     auto bail = [&](pca_status s) {

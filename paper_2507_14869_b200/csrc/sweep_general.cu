@@ -7,9 +7,10 @@
 // label is #{k : r > T_k} -- integer-exact, like the binary kernel.
 //
 // Otherwise, per site i (PAPER.md:462-477 with R1), in fp64:
-//   w_s = e^{a n_i(s)} * e^{-b (lum g_i - lum s)^2} * e^{-c 1{s != x_i}}
-//       = A[n_i(s)] * D[g_i][s] * (s == x_i ? 1 : Cw)
-// (the factorised form of exp(E_i(s)); A, D, Cw tabulated on the host in fp64),
+//   w_s = e^{a n_i(s)} * e^{-b (lum g_i - lum s)^2} * e^{-c pen(x_i, s)}
+//       = A[n_i(s)] * D[g_i][s] * I[x_i][s],   I[x][s] = (s == x ? 1 : Cw) for the paper's
+// L0 inertia, the host table exp(-c |lum x - lum s|^p) for L1 / L2
+// (the factorised form of exp(E_i(s)); A, D, Cw, I tabulated on the host in fp64),
 // Z = sum_s w_s; the new label is min{k < l-1 : u Z < sum_{s<=k} w_s}, else l-1 (R14),
 // with u = r 2^-32 from the site's Philox word.  Rounding differs from the oracle's
 // exp(E - max E)/Z only in the last bits, so decisions can differ only when u lies within
@@ -53,7 +54,8 @@ struct SiteJob {
 // as 16 nibbles, the L weights stay in registers, and the CDF scan is branch-free.
 template <int NB, int L>
 __device__ __forceinline__ int decide_fp64_fixed(const GeneralSweepParams& p, const double* sA,
-                                                 const double* sD, const SiteJob& j) {
+                                                 const double* sD, const double* sI,
+                                                 const SiteJob& j) {
     uint64_t hist = 0;
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
@@ -63,12 +65,14 @@ __device__ __forceinline__ int decide_fp64_fixed(const GeneralSweepParams& p, co
     const int xi = (int)(j.xg & 0xFFu), gi = (int)((j.xg >> 8) & 0xFFu);
     const double Cw = p.Cw;
     const double* Drow = sD + gi * L;
+    const double* Irow = sI + xi * L;
+    const bool l0 = p.inertia_p == 0;
     double w[L];
     double Z = 0.0;
 #pragma unroll
     for (int s = 0; s < L; ++s) {
         const int n = (int)((hist >> (4 * s)) & 0xFull);
-        w[s] = sA[n] * Drow[s] * (s == xi ? 1.0 : Cw);
+        w[s] = sA[n] * Drow[s] * (l0 ? (s == xi ? 1.0 : Cw) : Irow[s]);
         Z += w[s];
     }
     if (!(Z >= 1e-290 && Z <= 1e290)) return -1;  // caller takes the log-domain path
@@ -92,12 +96,14 @@ __device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const 
     const int xi = (int)(j.xg & 0xFFu), gi = (int)((j.xg >> 8) & 0xFFu);
     const double Cw = p.Cw;
     const double* Drow = p.dtab + (size_t)gi * L;
+    const double* Irow = p.itab + (size_t)xi * L;
+    const bool l0 = p.inertia_p == 0;
     double Z = 0.0;
     for (int s = 0; s < L; ++s) {
         int n = 0;
 #pragma unroll
         for (int q = 0; q < NB; ++q) n += (nb[q] == s);
-        Z += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
+        Z += sA[n] * __ldg(Drow + s) * (l0 ? (s == xi ? 1.0 : Cw) : __ldg(Irow + s));
     }
     const double u = (double)j.r * (1.0 / 4294967296.0);
     if (Z >= 1e-290 && Z <= 1e290) {
@@ -107,21 +113,28 @@ __device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const 
             int n = 0;
 #pragma unroll
             for (int q = 0; q < NB; ++q) n += (nb[q] == s);
-            F += sA[n] * __ldg(Drow + s) * (s == xi ? 1.0 : Cw);
+            F += sA[n] * __ldg(Drow + s) * (l0 ? (s == xi ? 1.0 : Cw) : __ldg(Irow + s));
             if (target < F) return s;
         }
         return L - 1;
     }
     // Rare slow path (extreme beta, q or sigma: the factorised weights under- or overflow):
-    // E_s = a n_s - b d_s^2 - c 1{s != x_i}, softmax with the max subtracted.
+    // E_s = a n_s - b d_s^2 - c pen(x_i, s), softmax with the max subtracted.
     const double lg = (double)gi / (double)(L - 1);
+    const double lx = (double)xi / (double)(L - 1);
+    auto pen = [&](int s) {
+        if (s == xi) return 0.0;
+        if (p.inertia_p == 0) return 1.0;
+        const double e = lx - (double)s / (double)(L - 1);
+        return p.inertia_p == 1 ? fabs(e) : e * e;
+    };
     double Emax = -INFINITY;
     for (int s = 0; s < L; ++s) {
         int n = 0;
 #pragma unroll
         for (int q = 0; q < NB; ++q) n += (nb[q] == s);
         const double d = lg - (double)s / (double)(L - 1);
-        Emax = fmax(Emax, p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0));
+        Emax = fmax(Emax, p.coef_a * n - p.coef_b * d * d - p.coef_c * pen(s));
     }
     double Zs = 0.0;
     for (int s = 0; s < L; ++s) {
@@ -129,7 +142,7 @@ __device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const 
 #pragma unroll
         for (int q = 0; q < NB; ++q) n += (nb[q] == s);
         const double d = lg - (double)s / (double)(L - 1);
-        Zs += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
+        Zs += exp(p.coef_a * n - p.coef_b * d * d - p.coef_c * pen(s) - Emax);
     }
     const double target = u * Zs;
     double F = 0.0;
@@ -138,7 +151,7 @@ __device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const 
 #pragma unroll
         for (int q = 0; q < NB; ++q) n += (nb[q] == s);
         const double d = lg - (double)s / (double)(L - 1);
-        F += exp(p.coef_a * n - p.coef_b * d * d - (s != xi ? p.coef_c : 0.0) - Emax);
+        F += exp(p.coef_a * n - p.coef_b * d * d - p.coef_c * pen(s) - Emax);
         if (target < F) return s;
     }
     return L - 1;
@@ -149,11 +162,15 @@ __global__ void __launch_bounds__(GEN_THREADS, 2)
     sweep_general_kernel(const __grid_constant__ GeneralSweepParams p) {
     __shared__ double sA[9];
     __shared__ double sD[LT > 0 ? LT * LT : 1];
+    __shared__ double sI[LT > 0 ? LT * LT : 1];
     __shared__ SiteJob s_jobs[GEN_WARPS][128];
     __shared__ uint8_t s_res[GEN_WARPS][128];
     if (threadIdx.x < 9) sA[threadIdx.x] = p.A[threadIdx.x];
     if (LT > 0)
-        for (int i = threadIdx.x; i < LT * LT; i += GEN_THREADS) sD[i] = p.dtab[i];
+        for (int i = threadIdx.x; i < LT * LT; i += GEN_THREADS) {
+            sD[i] = p.dtab[i];
+            sI[i] = p.inertia_p != 0 ? p.itab[i] : 0.0;
+        }
     __syncthreads();
 
     const Geometry& G = p.c.geo;
@@ -238,7 +255,7 @@ __global__ void __launch_bounds__(GEN_THREADS, 2)
         __syncwarp();
         for (int i = lane; i < qbase; i += 32) {
             int w = -1;
-            if (LT > 0) w = decide_fp64_fixed<NB, (LT > 0 ? LT : 2)>(p, sA, sD, jobs[i]);
+            if (LT > 0) w = decide_fp64_fixed<NB, (LT > 0 ? LT : 2)>(p, sA, sD, sI, jobs[i]);
             if (w < 0) w = decide_fp64<NB>(p, sA, jobs[i]);
             res[i] = (uint8_t)w;
         }

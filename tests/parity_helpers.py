@@ -14,7 +14,7 @@ RATE_TOL = 1e-6       # ... and fewer than 1e-6 of all updates
 def oracle_model(cfg: P.pca_config) -> orc.Model:
     return orc.model(cfg.height, cfg.width, cfg.levels, nbhd=cfg.neighborhood,
                      periodic=bool(cfg.periodic), J=cfg.J, q=cfg.q, sigma=cfg.sigma,
-                     coef_scale=cfg.coef_scale)
+                     coef_scale=cfg.coef_scale, inertia_p=cfg.inertia_p)
 
 
 def beta_of(cfg: P.pca_config, t: int) -> float:

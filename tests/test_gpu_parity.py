@@ -51,6 +51,24 @@ def test_lockstep_inertia_extremes(cuda_device, q):
         assert np.array_equal(ctx.state()[0], ctx._g_host[0])
 
 
+@pytest.mark.parametrize("inertia_p", [1, 2])
+@pytest.mark.parametrize("shape", [(40, 130, 5, 8, False), (29, 61, 9, 4, True),
+                                   (31, 45, 33, 8, False), (33, 47, 2, 8, True)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("q", [0.51, 4.0, 1e6])
+def test_lockstep_l1_l2_inertia(cuda_device, inertia_p, shape, q):
+    """L1 / L2 inertia norms, table (levels <= 16) and fp64 paths,
+    including the log-domain path (q = 1e6 under/overflows the factorised weights)."""
+    H, W, L, nb, per = shape
+    cfg = P.make_config(H, W, L, neighborhood=nb, periodic=per, q=q, sigma=0.3, beta0=0.9,
+                        beta_step=0.5, beta_period=2, seed=99 + L, inertia_p=inertia_p)
+    g = synth.smooth_labels(H, W, L, seed=5)
+    x0 = synth.smooth_labels(H, W, L, seed=6)  # smooth: the uniform-table path is exercised
+    x0[::3, ::2] = synth.random_labels(x0[::3, ::2].shape, L, seed=7)  # ... and the fp64 one
+    ctx = make_ctx(cfg, synth.degrade(g, L, 0.3, 8), x0)
+    lockstep(ctx, cfg, 6).check(allow_rate=False)
+
+
 def _c1_config(seed, kernel=P.KERNEL_AUTO):
     # config 1 (BASELINE.json configs[0]): 64x64 binary, 4-neighbour torus, 200 sweeps,
     # schedule 1.25 + 0.25 every 50 (the paper's compressed), MPM burn-in 100.
