@@ -184,6 +184,15 @@ pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int
 pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* psnr,
                          double* ssim);
 
+/* Windowed SSIM (R16's secondary metric, the form Table 1 of PAPER.md:703 appears to use):
+ * the mean over every 7x7 window position inside the image (stride 1, no padding) of
+ *   SSIM_w = (2 mx my + c1)(2 sxy + c2) / ((mx^2 + my^2 + c1)(sx^2 + sy^2 + c2)),
+ * uniform weights, sample (N-1) variances, c1 = 1e-4, c2 = 9e-4, luminance units.  Window
+ * moments are exact (integer sums); ssim[b] per chain.  kind = PCA_EST_LAST or PCA_EST_MPM;
+ * truth host or device [batch][height][width].  PCA_EINVAL if height or width < 7;
+ * PCA_EUNSUPPORTED for a row-strip context (windows would span ranks).  Synchronises. */
+pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* ssim);
+
 /* Copy the current state [batch][rows][width] to out / from x (host or device). */
 pca_status pca_read_state(pca_ctx* ctx, uint8_t* out);
 pca_status pca_write_state(pca_ctx* ctx, const uint8_t* x);

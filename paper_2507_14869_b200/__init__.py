@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "PCA_OK", -1: "PCA_EINVAL", -2: "PCA_ESTATE", -3: "PCA_ECUDA"
 
 # every symbol include/pca.h declares
 EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "pca_sweep",
-           "pca_estimate", "pca_metric_sums", "pca_psnr_ssim", "pca_read_state",
+           "pca_estimate", "pca_metric_sums", "pca_psnr_ssim", "pca_ssim_windowed", "pca_read_state",
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
            "pca_destroy", "pca_last_error"]
@@ -92,6 +92,7 @@ def lib():
             "pca_estimate": (i32, [vp, i32, vp]),
             "pca_metric_sums": (i32, [vp, vp, i32, vp]),
             "pca_psnr_ssim": (i32, [vp, vp, i32, vp, vp]),
+            "pca_ssim_windowed": (i32, [vp, vp, i32, vp]),
             "pca_read_state": (i32, [vp, vp]),
             "pca_write_state": (i32, [vp, vp]),
             "pca_read_counts": (i32, [vp, vp]),
@@ -212,6 +213,12 @@ class PcaContext:
         _check(lib().pca_psnr_ssim(self.handle, _ptr(truth), int(kind), p.ctypes.data,
                                    s.ctypes.data), "pca_psnr_ssim")
         return p, s
+
+    def pca_ssim_windowed(self, truth, kind: int):
+        s = np.zeros(self.cfg.batch, np.float64)
+        _check(lib().pca_ssim_windowed(self.handle, _ptr(truth), int(kind), s.ctypes.data),
+               "pca_ssim_windowed")
+        return s
 
     def pca_read_state(self, out):
         _check(lib().pca_read_state(self.handle, _ptr(out)), "pca_read_state")

@@ -7,6 +7,8 @@
 //  * metric_sums: one pass over truth and the LAST or MPM estimate, accumulating the exact
 //    integer sums of PAPER.md:516-534's statistics (sum (x-y)^2, sum x, sum y, sum x^2,
 //    sum y^2, sum xy, max x) per chain; block reduction, then one atomic per block per sum.
+//  * ssim_windowed: mean SSIM over every 7x7 window (R16's secondary metric): exact integer
+//    window sums, fp64 per window, deterministic fixed-order per-block partial sums.
 //
 // All of them move 16 sites per thread with 16-byte vector accesses when the rows are
 // 16-byte aligned (W % 16 == 0), and fall back to per-byte access otherwise.  Grid: x over
@@ -258,6 +260,65 @@ inline dim3 chunk_grid(const Geometry& G, int batch, int max_rows = 2048) {
     return dim3(gx, gy, batch);
 }
 
+// Windowed SSIM (Wang et al.; PAPER.md:527-534 read through R16): thread = one window
+// column c0, block = SSIM_TPB columns x SSIM_ROWS_PER_BLOCK window rows.  The 7x7 sums
+// (x, y, x^2, y^2, xy over level indices) slide down the rows: add the entering row's
+// 7-column sums, subtract the leaving row's; all integer, so every window's moments are
+// exact and only the per-window SSIM and the final mean round.
+struct WinSums {
+    int x, y, xx, yy, xy;
+};
+__device__ __forceinline__ void row7(const uint8_t* xr, const uint8_t* yr, int sign, WinSums& S) {
+    int x = 0, y = 0, xx = 0, yy = 0, xy = 0;
+#pragma unroll
+    for (int c = 0; c < SSIM_WIN; ++c) {
+        const int a = xr[c], b = yr[c];
+        x += a; y += b; xx += a * a; yy += b * b; xy += a * b;
+    }
+    S.x += sign * x; S.y += sign * y; S.xx += sign * xx; S.yy += sign * yy; S.xy += sign * xy;
+}
+
+__global__ void __launch_bounds__(SSIM_TPB) ssim_windowed_kernel(const WinSsimParams p) {
+    const int nwr = p.H - SSIM_WIN + 1, nwc = p.W - SSIM_WIN + 1;
+    const int c0 = blockIdx.x * SSIM_TPB + threadIdx.x;
+    const int rb = blockIdx.y * SSIM_ROWS_PER_BLOCK;
+    const int re = min(rb + SSIM_ROWS_PER_BLOCK, nwr);
+    const uint8_t* X = p.x + (long long)blockIdx.z * p.xchain + c0;
+    const uint8_t* Y = p.y + (long long)blockIdx.z * p.ychain + c0;
+    const double L1 = (double)(p.levels - 1);
+    const double n = (double)(SSIM_WIN * SSIM_WIN);
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    double acc = 0.0;
+    if (c0 < nwc) {
+        WinSums S = {0, 0, 0, 0, 0};
+        for (int r = rb; r < rb + SSIM_WIN; ++r)
+            row7(X + (long long)r * p.xpitch, Y + (long long)r * p.ypitch, 1, S);
+        for (int r0 = rb;;) {
+            // means S/(n L1); sample (co)variances (n S2 - S S')/(n (n-1) L1^2), exact numerators
+            const double mx = (double)S.x / (n * L1), my = (double)S.y / (n * L1);
+            const double den = n * (n - 1.0) * L1 * L1;
+            const double vx = (double)(SSIM_WIN * SSIM_WIN * (long long)S.xx - (long long)S.x * S.x) / den;
+            const double vy = (double)(SSIM_WIN * SSIM_WIN * (long long)S.yy - (long long)S.y * S.y) / den;
+            const double vxy = (double)(SSIM_WIN * SSIM_WIN * (long long)S.xy - (long long)S.x * S.y) / den;
+            acc += ((2.0 * mx * my + c1) * (2.0 * vxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
+            if (++r0 >= re) break;
+            row7(X + (long long)(r0 + SSIM_WIN - 1) * p.xpitch, Y + (long long)(r0 + SSIM_WIN - 1) * p.ypitch, 1, S);
+            row7(X + (long long)(r0 - 1) * p.xpitch, Y + (long long)(r0 - 1) * p.ypitch, -1, S);
+        }
+    }
+    // fixed-order reduction: warp butterfly, then warp 0 adds the warp totals in order
+    __shared__ double s_w[SSIM_TPB / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < SSIM_TPB / 32; ++w) t += s_w[w];
+        p.partial[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
 }  // namespace
 
 int launch_pack_state(const Geometry& G, const uint8_t* src, int src_pitch, long long src_chain,
@@ -306,6 +367,21 @@ int launch_marginals(const Geometry& G, const uint16_t* counts, int nsamp, float
 
 int launch_metric_sums(const MetricParams& p, int batch, void* stream) {
     metric_sums_kernel<<<chunk_grid(p.geo, batch, 512), TPB, 0, (cudaStream_t)stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+void ssim_windowed_grid(int H, int W, int* gx, int* gy) {
+    const int nwr = H - SSIM_WIN + 1, nwc = W - SSIM_WIN + 1;
+    *gx = nwc > 0 ? (nwc + SSIM_TPB - 1) / SSIM_TPB : 0;
+    *gy = nwr > 0 ? (nwr + SSIM_ROWS_PER_BLOCK - 1) / SSIM_ROWS_PER_BLOCK : 0;
+}
+
+int launch_ssim_windowed(const WinSsimParams& p, int batch, void* stream) {
+    int gx = 0, gy = 0;
+    ssim_windowed_grid(p.H, p.W, &gx, &gy);
+    if (gx == 0 || gy == 0) return 0;
+    dim3 grid(gx, gy, batch);
+    ssim_windowed_kernel<<<grid, SSIM_TPB, 0, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

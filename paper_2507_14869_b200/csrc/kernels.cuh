@@ -121,4 +121,19 @@ int launch_marginals(const Geometry& geo, const uint16_t* counts, int nsamp, flo
                      long long out_chain_stride, int k, int batch, void* stream);
 int launch_metric_sums(const MetricParams& p, int batch, void* stream);
 
+// windowed SSIM: 7x7 uniform windows at every position inside the image, sample moments
+constexpr int SSIM_WIN = 7, SSIM_TPB = 128, SSIM_ROWS_PER_BLOCK = 64;
+struct WinSsimParams {
+    const uint8_t* x;  // image 1, row 0 col 0 of chain 0
+    long long xchain;
+    int xpitch;
+    const uint8_t* y;  // image 2
+    long long ychain;
+    int ypitch;
+    int H, W, levels;
+    double* partial;   // [batch][gy][gx] per-block sums of window SSIMs
+};
+void ssim_windowed_grid(int H, int W, int* gx, int* gy);
+int launch_ssim_windowed(const WinSsimParams& p, int batch, void* stream);
+
 }  // namespace pcab200

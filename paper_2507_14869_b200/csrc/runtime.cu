@@ -163,7 +163,11 @@ Layout make_layout(const pca_config* c) {
     L.xbuf = B * (R + 2 * HALO) * (size_t)L.xpitch;
     L.gbuf = B * (R + 2 * GHALO) * (size_t)L.gpitch;
     L.counts_bytes = B * (size_t)L.cplanes * R * (size_t)L.cpitch * 2;
-    L.stage_bytes = B * R * W * 4;  // uint8 images and fp32 planes (one label plane at a time)
+    // uint8 images and fp32 planes (one label plane at a time); windowed SSIM: staged truth,
+    // MPM image and the per-block partial sums
+    int sgx = 0, sgy = 0;
+    ssim_windowed_grid(L.rows, c->width, &sgx, &sgy);
+    L.stage_bytes = std::max(B * R * W * 4, align256(B * R * W) * 2 + B * (size_t)sgx * sgy * 8);
     size_t o = 0;
     L.off_x0 = o; o = align256(o + L.xbuf);
     L.off_x1 = o; o = align256(o + L.xbuf);
@@ -838,6 +842,60 @@ pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, doubl
                   ((mux * mux + muy * muy + c1) * (sx + sy + c2));
     }
     if (black) return fail(PCA_EINVAL, "original image is all black: PSNR undefined (R17)");
+    return PCA_OK;
+}
+
+pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* ssim) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!truth || !ssim) return fail(PCA_EINVAL, "truth and ssim must be non-NULL");
+    if (kind != PCA_EST_LAST && kind != PCA_EST_MPM)
+        return fail(PCA_EINVAL, "windowed SSIM is defined for LAST and MPM");
+    if (kind == PCA_EST_MPM && ctx->counted < 1)
+        return fail(PCA_EINVAL, "MPM needs counted sweeps (mpm_burn_in)");
+    const pca_config& c = ctx->cfg;
+    if (ctx->lay.rows != c.height)
+        return fail(PCA_EUNSUPPORTED, "windowed SSIM needs the whole lattice (not a row strip)");
+    if (c.height < SSIM_WIN || c.width < SSIM_WIN)
+        return fail(PCA_EINVAL, "windowed SSIM needs height, width >= %d", SSIM_WIN);
+    const uint8_t* dt = nullptr;
+    st = device_input(ctx, truth, &dt);  // host truth -> stage[0, BRW)
+    if (st != PCA_OK) return st;
+    const size_t brw = dense_bytes(ctx);
+    WinSsimParams wp;
+    wp.y = dt;
+    wp.ychain = (long long)ctx->lay.rows * c.width;
+    wp.ypitch = c.width;
+    if (kind == PCA_EST_LAST) {
+        wp.x = ctx->x[ctx->cur] + (size_t)HALO * ctx->lay.xpitch + XOFF;
+        wp.xchain = ctx->geo.xchain;
+        wp.xpitch = ctx->lay.xpitch;
+    } else {
+        uint8_t* mpm = ctx->stage + align256(brw);
+        LAUNCH(ctx, launch_mpm(ctx->geo, ctx->counts, (int)ctx->counted, mpm, c.batch, ctx->stream));
+        wp.x = mpm;
+        wp.xchain = wp.ychain;
+        wp.xpitch = c.width;
+    }
+    wp.H = c.height;
+    wp.W = c.width;
+    wp.levels = c.levels;
+    wp.partial = (double*)(ctx->stage + 2 * align256(brw));
+    int gx = 0, gy = 0;
+    ssim_windowed_grid(c.height, c.width, &gx, &gy);
+    LAUNCH(ctx, launch_ssim_windowed(wp, c.batch, ctx->stream));
+    const size_t per = (size_t)gx * gy;
+    std::vector<double> h(per * c.batch);
+    CK(ctx, cudaMemcpyAsync(h.data(), wp.partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    st = sync(ctx);
+    if (st != PCA_OK) return st;
+    const double nwin = (double)(c.height - SSIM_WIN + 1) * (double)(c.width - SSIM_WIN + 1);
+    for (int b = 0; b < c.batch; ++b) {
+        double t = 0.0;
+        for (size_t i = 0; i < per; ++i) t += h[(size_t)b * per + i];
+        ssim[b] = t / nwin;
+    }
     return PCA_OK;
 }
 

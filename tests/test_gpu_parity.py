@@ -102,6 +102,8 @@ def test_config1_free_running_chain(cuda_device, seed):
         _, p_o, s_o, _ = orc.metrics(truth, est, 2)
         assert abs(psnr[0] - p_o) < 0.01 and abs(psnr[0] - p_o) < 1e-9
         assert abs(ssim[0] - s_o) < 1e-9
+        sw = ctx.pca_ssim_windowed(truth[None], kind)
+        assert abs(sw[0] - orc.ssim_windowed(truth, est, 2)) < 1e-12
     marg = ctx.estimate(P.EST_MARGINALS)[0]
     assert np.allclose(marg[1], cnt_o[1] / 100.0, atol=1e-6)
     assert np.allclose(marg[0] + marg[1], 1.0, atol=1e-6)
@@ -143,9 +145,38 @@ def test_config2_paper_protocol_lockstep(cuda_device, levels, sigma, ramp, n):
             psnr, ssim = ctx.pca_psnr_ssim(truth[None], kind)
             _, p_o, s_o, _ = orc.metrics(truth, est, levels)
             assert abs(psnr[0] - p_o) < 1e-9 and abs(ssim[0] - s_o) < 1e-9
+            sw = ctx.pca_ssim_windowed(truth[None], kind)
+            assert abs(sw[0] - orc.ssim_windowed(truth, est, levels)) < 1e-12
         cm = ctx.estimate(P.EST_CM)[0]
         ref = (np.arange(levels)[:, None, None] / (levels - 1) * cnt_o).sum(0) / (n - burn)
         assert np.allclose(cm, ref, atol=1e-6)
+
+
+@pytest.mark.parametrize("H,W,L", [(7, 7, 2), (8, 300, 5), (130, 9, 9), (71, 133, 255), (64, 64, 33)])
+def test_windowed_ssim_matches_oracle(cuda_device, H, W, L):
+    """pca_ssim_windowed (7x7 windows, sample moments, R16) == orc_ssim_windowed for LAST and
+    MPM, per chain of a batch, with ragged widths and heights that span several blocks."""
+    B = 3
+    truth = np.stack([synth.smooth_labels(H, W, L, seed=11 + b) for b in range(B)])
+    g = np.stack([synth.degrade(truth[b], L, 0.3, seed=b) for b in range(B)])
+    cfg = P.make_config(H, W, L, batch=B, sigma=0.3, seed=5, mpm_burn_in=2)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_sweep(6)
+    for kind in (P.EST_LAST, P.EST_MPM):
+        est = ctx.estimate(kind)
+        for t_arg in (truth, _to_device(truth)):
+            sw = ctx.pca_ssim_windowed(t_arg, kind)
+            for b in range(B):
+                assert abs(sw[b] - orc.ssim_windowed(truth[b], est[b], L)) < 1e-12
+    assert abs(ctx.pca_ssim_windowed(ctx.state(), P.EST_LAST)[0] - 1.0) < 1e-14
+    small = make_ctx(P.make_config(6, 40, 2, sigma=0.5), np.zeros((6, 40), np.uint8))
+    with pytest.raises(P.PcaError):
+        small.pca_ssim_windowed(np.zeros((1, 6, 40), np.uint8), P.EST_LAST)
+
+
+def _to_device(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
 def test_batch_equals_independent_chains(cuda_device):
@@ -232,6 +263,8 @@ def test_row_strips_with_loopback_halo_exchange(cuda_device, periodic, levels):
               for i, s in enumerate(strips))
     ref = full.pca_metric_sums(truth[None], P.EST_LAST)
     assert np.array_equal(tot[:, [0, 1, 2, 3, 4, 5, 7]], ref[:, [0, 1, 2, 3, 4, 5, 7]])
+    with pytest.raises(P.PcaError, match="row strip"):  # windows would span ranks
+        strips[0].pca_ssim_windowed(truth[bounds[0]:bounds[1]][None], P.EST_LAST)
 
 
 def test_checkpoint_resume_is_bit_exact(cuda_device):
