@@ -93,7 +93,11 @@ def lib():
                                        ctypes.c_uint32, ctypes.c_uint32]),
             "orc_gibbs_run": (None, [mp, u8p, u8p, u32p, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_int,
-                                     ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int]),
+                                     ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
+                                     ctypes.c_int]),
+            "orc_gibbs_sweep_coloured": (None, [mp, u8p, u8p, ctypes.c_double, ctypes.c_uint64,
+                                                ctypes.c_uint32, ctypes.c_uint32]),
+            "orc_gibbs_colour": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
             "orc_mpm": (None, [u32p, ctypes.c_int, ctypes.c_size_t, u8p]),
             "orc_metrics": (ctypes.c_int, [u8p, u8p, ctypes.c_size_t, ctypes.c_int, f64p, f64p,
                                            f64p]),
@@ -208,13 +212,29 @@ def gibbs_sweep(m: Model, x, g, beta, seed, chain, t):
     return x
 
 
-def gibbs_run(m: Model, x0, g, n, beta0, beta_step, period, seed, chain=0, t0=0, burn_in=-1):
+def gibbs_sweep_coloured(m: Model, x, g, beta, seed, chain, t):
+    """One Gibbs sweep in checkerboard colour order (see orc_gibbs_colour)."""
+    x = _u8(x).copy()
+    g = _u8(g)
+    lib().orc_gibbs_sweep_coloured(ctypes.byref(m), _p(x, ctypes.c_uint8), _p(g, ctypes.c_uint8),
+                                   beta, seed, chain, t)
+    return x
+
+
+def gibbs_colour(nbhd, r, c) -> int:
+    return int(lib().orc_gibbs_colour(nbhd, r, c))
+
+
+def gibbs_run(m: Model, x0, g, n, beta0, beta_step, period, seed, chain=0, t0=0, burn_in=-1,
+              order="column"):
+    """order: "column" = the paper's column-major scan, "colour" = the
+    checkerboard colour order of the GPU Gibbs sampler."""
     x = _u8(x0).copy()
     g = _u8(g)
     counts = np.zeros((m.levels,) + x.shape, np.uint32)
     lib().orc_gibbs_run(ctypes.byref(m), _p(x, ctypes.c_uint8), _p(g, ctypes.c_uint8),
                         _p(counts, ctypes.c_uint32), t0, n, beta0, beta_step, period, seed, chain,
-                        burn_in)
+                        burn_in, {"column": 0, "colour": 1}[order])
     return x, counts
 
 

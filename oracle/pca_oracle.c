@@ -250,13 +250,46 @@ void orc_gibbs_sweep(const orc_model* m, uint8_t* x, const uint8_t* g, double be
     }
 }
 
+/* Colour of site (r, c) in the checkerboard partition of the lattice graph: von Neumann-4
+ * (r + c) mod 2 (2 colours), Moore-8 2(r mod 2) + (c mod 2) (4 colours).  No two sites of
+ * one colour are neighbours (on a torus: when H and W are even), so the systematic scan
+ * "colour 0, colour 1, ..." is a scan order whose colour classes can be updated at once.  */
+int orc_gibbs_colour(int nbhd, int r, int c) {
+    return nbhd == 4 ? ((r + c) & 1) : (((r & 1) << 1) | (c & 1));
+}
+
+/* One systematic Gibbs sweep in colour order: for colour
+ * k = 0, 1, ... every site of colour k in row-major order, in place, each from its Gibbs
+ * conditional given the CURRENT configuration.  Random word: tag GIBBS, counter t.       */
+void orc_gibbs_sweep_coloured(const orc_model* m, uint8_t* x, const uint8_t* g, double beta,
+                              uint64_t seed, uint32_t chain, uint32_t t) {
+    double p[256];
+    const int ncol = m->nbhd == 4 ? 2 : 4;
+    for (int k = 0; k < ncol; k++) {
+        for (int r = 0; r < m->H; r++) {
+            for (int c = 0; c < m->W; c++) {
+                if (orc_gibbs_colour(m->nbhd, r, c) != k) continue;
+                site_probs(m, x, g, r, c, beta, 0, p);
+                uint32_t rnd = orc_draw(seed, ORC_TAG_GIBBS, chain, t, (uint32_t)r, (uint32_t)c);
+                double u = (double)rnd * (1.0 / 4294967296.0);
+                x[r * m->W + c] = (uint8_t)orc_decide(p, m->levels, u, NULL);
+            }
+        }
+    }
+}
+
+/* n Gibbs sweeps t = t0 .. t0+n-1; order 0 = the paper's column-major scan, 1 = colour
+ * order.  Counts as orc_pca_run (x after sweep t for t >= burn_in).                    */
 void orc_gibbs_run(const orc_model* m, uint8_t* x, const uint8_t* g, uint32_t* counts, int t0,
                    int n, double beta0, double beta_step, int period, uint64_t seed,
-                   uint32_t chain, int burn_in) {
+                   uint32_t chain, int burn_in, int order) {
     size_t N = (size_t)m->H * (size_t)m->W;
     for (int t = t0; t < t0 + n; t++) {
         double beta = orc_beta_at(beta0, beta_step, period, t);
-        orc_gibbs_sweep(m, x, g, beta, seed, chain, (uint32_t)t);
+        if (order == 1)
+            orc_gibbs_sweep_coloured(m, x, g, beta, seed, chain, (uint32_t)t);
+        else
+            orc_gibbs_sweep(m, x, g, beta, seed, chain, (uint32_t)t);
         if (counts && burn_in >= 0 && t >= burn_in) {
             for (size_t i = 0; i < N; i++) counts[(size_t)x[i] * N + i] += 1;
         }

@@ -332,3 +332,88 @@ def test_generate_mrf():
         agree = np.concatenate([(y[1:, :] == y[:-1, :]).ravel(), (y[:, 1:] == y[:, :-1]).ravel(),
                                 (y[1:, 1:] == y[:-1, :-1]).ravel(), (y[1:, :-1] == y[:-1, 1:]).ravel()])
         assert agree.mean() > 0.9
+
+
+# --- checkerboard-colour Gibbs scan (the GPU Gibbs sampler's order) ---
+
+@pytest.mark.parametrize("lat", [en.Lattice(4, 6, 2, nbhd=4, periodic=True),
+                                 en.Lattice(4, 6, 2, nbhd=8, periodic=True),
+                                 en.Lattice(3, 5, 2, nbhd=8, periodic=False),
+                                 en.Lattice(5, 3, 2, nbhd=4, periodic=False)])
+def test_gibbs_colours_are_independent_sets(lat):
+    """No two sites of one colour are neighbours (even torus sides; any free lattice), so a
+    colour class may be updated at once (checked on the enumeration's own neighbour lists)."""
+    nbrs = lat.neighbours()
+    col = [orc.gibbs_colour(lat.nbhd, i // lat.W, i % lat.W) for i in range(lat.n)]
+    assert len(set(col)) == (2 if lat.nbhd == 4 else 4)
+    for i in range(lat.n):
+        for j in nbrs[i]:
+            assert col[i] != col[j]
+
+
+def test_coloured_sweep_is_any_order_within_a_colour():
+    """Updating the sites of one colour in a random order, one at a time from the current
+    state (site conditional of PAPER.md:417-429, tag GIBBS uniform), gives exactly the
+    coloured sweep: the sites of a colour do not see each other."""
+    H, W, L = 6, 8, 5
+    m = orc.model(H, W, L, nbhd=8, periodic=True, J=1 / 3, q=0.0, sigma=0.3)
+    rng = np.random.default_rng(3)
+    g = rng.integers(0, L, (H, W)).astype(np.uint8)
+    x = rng.integers(0, L, (H, W)).astype(np.uint8)
+    beta, seed, chain, t = 1.4, 17, 2, 9
+    ref = orc.gibbs_sweep_coloured(m, x, g, beta, seed, chain, t)
+    y = x.copy()
+    for k in range(4):
+        sites = [(r, c) for r in range(H) for c in range(W) if orc.gibbs_colour(8, r, c) == k]
+        for idx in rng.permutation(len(sites)):
+            r, c = sites[idx]
+            p = orc.gibbs_site_probs(m, y, g, r, c, beta)
+            u = orc.draw(seed, 2, chain, t, r, c) / 2.0 ** 32
+            y[r, c] = orc.decide(p, u)[0]
+    assert np.array_equal(y, ref)
+    assert not np.array_equal(ref, orc.gibbs_sweep(m, x, g, beta, seed, chain, t))  # != column scan
+
+
+@pytest.mark.parametrize("lat,g", [(en.Lattice(2, 3, 2, nbhd=4), np.array([[0, 1, 1], [1, 0, 1]])),
+                                   (en.Lattice(2, 3, 3, nbhd=8), np.array([[0, 2, 1], [2, 2, 0]]))])
+def test_coloured_sweep_law_is_the_product_of_site_kernels(lat, g):
+    """The C coloured sweep's one-step law from a fixed x equals the row of
+    K_{i1} K_{i2} ... K_{in} (sites in colour order), the single-site Gibbs kernels of the
+    enumeration (independent code), over independent streams (chain ids)."""
+    m = orc.model(lat.H, lat.W, lat.levels, nbhd=lat.nbhd, periodic=False, J=1 / 3, q=0.0,
+                  sigma=0.5)
+    g = g.astype(np.uint8)
+    beta = 1.25
+    a, b, _ = en.coefficients(beta, 1 / 3, 0.0, 0.5)
+    order = sorted(range(lat.n), key=lambda i: (orc.gibbs_colour(lat.nbhd, i // lat.W, i % lat.W), i))
+    K = np.eye(lat.levels ** lat.n)
+    for i in order:
+        K = K @ en.gibbs_site_kernel(lat, g.reshape(-1), a, b, i)
+    x = np.array([[1, 0, 1], [0, 1, 1]], np.uint8) % lat.levels
+    row = K[en.state_index(lat, x.reshape(-1))]
+    n = 30000
+    counts = np.zeros(len(row))
+    for k in range(n):
+        w = orc.gibbs_sweep_coloured(m, x, g, beta, seed=5, chain=k, t=3)
+        counts[en.state_index(lat, w.reshape(-1))] += 1
+    ok, stat, crit = _chi2_ok(counts, row, n)
+    assert ok, (stat, crit)
+    gs = en.gibbs_posterior(lat, g.reshape(-1), a, b)
+    assert np.abs(gs @ K - gs).max() < 1e-15  # the coloured sweep leaves pi_GS invariant
+
+
+def test_coloured_gibbs_run_counts():
+    """orc_gibbs_run(order = colour) == repeated coloured sweeps, with counts of x after
+    every sweep t >= burn_in."""
+    m = orc.model(6, 8, 3, nbhd=4, periodic=True, J=1 / 3, q=0.0, sigma=0.4)
+    rng = np.random.default_rng(8)
+    g = rng.integers(0, 3, (6, 8)).astype(np.uint8)
+    x, cnt = orc.gibbs_run(m, g, g, 12, 1.0, 0.5, 4, 21, chain=1, burn_in=5, order="colour")
+    y = g.copy()
+    ref = np.zeros_like(cnt)
+    for t in range(12):
+        y = orc.gibbs_sweep_coloured(m, y, g, orc.beta_at(1.0, 0.5, 4, t), 21, 1, t)
+        if t >= 5:
+            for k in range(3):
+                ref[k] += (y == k)
+    assert np.array_equal(x, y) and np.array_equal(cnt, ref)
