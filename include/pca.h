@@ -193,6 +193,17 @@ pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, doubl
  * PCA_EUNSUPPORTED for a row-strip context (windows would span ranks).  Synchronises. */
 pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* ssim);
 
+/* Enqueue n sweeps of the Gibbs sampler (conditional PAPER.md:417-429,
+ * no inertia term) on the same state, schedule, sweep counter t and MPM counts: a
+ * systematic scan in checkerboard colour order (4-neighbour: colours (r + c) mod 2;
+ * Moore-8: 2 (r mod 2) + (c mod 2); global r), one launch per colour, in place, with the
+ * Philox words of tag GIBBS.  The paper's own scan is column-major; the
+ * colour order gives another chain with the same stationary law (R21).
+ * PCA_EUNSUPPORTED on a torus with odd height or width (the colouring would not be
+ * proper); a row strip needs NCCL attached (halos are exchanged after every colour).
+ * Asynchronous like pca_sweep. */
+pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n);
+
 /* Copy the current state [batch][rows][width] to out / from x (host or device). */
 pca_status pca_read_state(pca_ctx* ctx, uint8_t* out);
 pca_status pca_write_state(pca_ctx* ctx, const uint8_t* x);

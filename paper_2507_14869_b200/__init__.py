@@ -29,7 +29,8 @@ STATUS_NAMES = {0: "PCA_OK", -1: "PCA_EINVAL", -2: "PCA_ESTATE", -3: "PCA_ECUDA"
 
 # every symbol include/pca.h declares
 EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "pca_sweep",
-           "pca_estimate", "pca_metric_sums", "pca_psnr_ssim", "pca_ssim_windowed", "pca_read_state",
+           "pca_gibbs_sweep", "pca_estimate", "pca_metric_sums", "pca_psnr_ssim",
+           "pca_ssim_windowed", "pca_read_state",
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
            "pca_destroy", "pca_last_error"]
@@ -89,6 +90,7 @@ def lib():
             "pca_init": (i32, [ctypes.POINTER(vp), cfgp, vp, sz, vp, vp, vp]),
             "pca_reset": (i32, [vp, vp, vp]),
             "pca_sweep": (i32, [vp, i32]),
+            "pca_gibbs_sweep": (i32, [vp, i32]),
             "pca_estimate": (i32, [vp, i32, vp]),
             "pca_metric_sums": (i32, [vp, vp, i32, vp]),
             "pca_psnr_ssim": (i32, [vp, vp, i32, vp, vp]),
@@ -196,6 +198,9 @@ class PcaContext:
 
     def pca_sweep(self, n: int):
         _check(lib().pca_sweep(self.handle, int(n)), "pca_sweep")
+
+    def pca_gibbs_sweep(self, n: int):
+        _check(lib().pca_gibbs_sweep(self.handle, int(n)), "pca_gibbs_sweep")
 
     def pca_estimate(self, kind: int, out):
         _check(lib().pca_estimate(self.handle, int(kind), _ptr(out)), "pca_estimate")

@@ -28,6 +28,8 @@ constexpr int HALO = 2;            // x halo rows above / below the owned rows
 constexpr int GHALO = 1;           // g halo rows above / below the owned rows
 constexpr int THR_ENTRIES = 324;   // binary thresholds [np 0..8][n1 0..8][g 0..1][x 0..1]
 constexpr uint32_t TAG_PCA = 1u;
+constexpr uint32_t TAG_GIBBS = 2u;
+constexpr int GIBBS_THR2 = 162;   // levels == 2 Gibbs thresholds [np 0..8][n1 0..8][g 0..1]
 
 struct Geometry {
     int W;             // columns
@@ -50,7 +52,7 @@ struct Geometry {
 
 struct SweepCommon {
     Geometry geo;
-    const uint8_t* x_in;   // padded buffer of chain 0, pointing at row -1, byte 0
+    const uint8_t* x_in;   // padded buffer of chain 0, pointing at padded row -HALO, byte 0
     uint8_t* x_out;
     const uint8_t* g;
     uint16_t* counts;
@@ -92,6 +94,22 @@ struct GeneralSweepParams {
     const uint32_t* uthr;
 };
 
+// Gibbs sampler, one colour class per launch, in place (x_in == x_out): sites of colour k
+// (4-neighbour: (r + c) mod 2; Moore-8: 2 (r mod 2) + (c mod 2), global r) draw from the
+// Gibbs conditional exp(a n_i(s) - b (lum g_i - lum s)^2) given the current state.
+// levels == 2: thr2[(np*9 + n1)*2 + g] = ceil(p0 2^32) - 1 (integer-exact);
+// levels > 2: uthr[(s*L + g)*(L-1) + k] for uniform neighbourhoods (L <= 16), else fp64
+// A[n] D[g][s] weights (log-domain when they under/overflow).
+struct GibbsSweepParams {
+    SweepCommon c;
+    int colour;
+    double A[9];
+    double coef_a, coef_b;
+    const double* dtab;
+    const uint32_t* uthr;
+    uint32_t thr2[GIBBS_THR2];
+};
+
 struct MetricParams {
     Geometry geo;
     const uint8_t* x;      // padded current state, chain 0 row -1
@@ -106,6 +124,7 @@ struct MetricParams {
 int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread,
                         void* stream);
 int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream);
+int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream);
 int launch_sweep_binary2(const Binary2SweepParams& p, int batch, int rows_per_thread, void* stream);
 int launch_pack_state(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad_flag, void* stream);

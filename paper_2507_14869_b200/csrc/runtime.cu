@@ -100,6 +100,7 @@ struct Layout {
     size_t xbuf = 0;      // bytes of one x buffer
     size_t gbuf = 0;      // bytes of the g buffer
     size_t off_uthr = 0, uthr_entries = 0;
+    size_t off_gthr = 0, gthr_entries = 0;  // Gibbs uniform-neighbourhood thresholds
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
            off_sums_max = 0, off_flag = 0, off_stage = 0;
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
@@ -178,6 +179,9 @@ Layout make_layout(const pca_config* c) {
     L.uthr_entries = c->levels <= UTHR_MAX_LEVELS
                          ? (size_t)c->levels * c->levels * c->levels * (c->levels - 1) : 0;
     L.off_uthr = o; o = align256(o + L.uthr_entries * sizeof(uint32_t));
+    L.gthr_entries = (c->levels > 2 && c->levels <= UTHR_MAX_LEVELS)
+                         ? (size_t)c->levels * c->levels * (c->levels - 1) : 0;
+    L.off_gthr = o; o = align256(o + L.gthr_entries * sizeof(uint32_t));
     L.off_sums = o; o = align256(o + B * 8 * sizeof(unsigned long long));
     L.off_sums_max = o; o = align256(o + B * 8 * sizeof(unsigned long long));
     L.off_flag = o; o = align256(o + 256);
@@ -213,6 +217,10 @@ struct pca_ctx {
     int poisoned = 0;
     int x_initialized = 0;
     int64_t tab_stage = -1;
+    int64_t gtab_stage = -1;
+    GibbsSweepParams gib;
+    std::vector<uint32_t> gthr_host;
+    uint32_t* gthr = nullptr;
     BinarySweepParams bin;
     Binary2SweepParams bin2;
     GeneralSweepParams gen;
@@ -417,6 +425,70 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
     return PCA_OK;
 }
 
+// Gibbs tables for the stage of sweep t: the conditional of PAPER.md:417-429 (no inertia),
+// E_s = a n_s - b d_s^2, softmax and cumulative sum in the oracle's fp64 order.
+pca_status build_gibbs_tables(pca_ctx* ctx, int64_t t) {
+    const pca_config& c = ctx->cfg;
+    const int64_t stage = t / c.beta_period;
+    if (stage == ctx->gtab_stage) return PCA_OK;
+    const double beta = beta_at(c, t);
+    const double a = c.coef_scale * 2.0 * beta * c.J;
+    const double b = c.coef_scale / (2.0 * c.sigma * c.sigma);
+    GibbsSweepParams& m = ctx->gib;
+    for (int n = 0; n <= 8; ++n) m.A[n] = exp(a * (double)n);
+    m.coef_a = a;
+    m.coef_b = b;
+    const int L = c.levels;
+    // cumulative thresholds T_k = ceil(F_k 2^32) - 1 of the law with label counts n[]
+    auto thresholds = [&](const int* n, int gl, uint32_t* out) {
+        double E[UTHR_MAX_LEVELS], pr[UTHR_MAX_LEVELS];
+        double Emax = -INFINITY;
+        for (int s = 0; s < L; ++s) {
+            const double d = lum(gl, L) - lum(s, L);
+            E[s] = a * (double)n[s] - b * d * d;
+            if (E[s] > Emax) Emax = E[s];
+        }
+        double Z = 0.0;
+        for (int s = 0; s < L; ++s) {
+            pr[s] = exp(E[s] - Emax);
+            Z += pr[s];
+        }
+        for (int s = 0; s < L; ++s) pr[s] = pr[s] / Z;
+        double F = 0.0;
+        for (int k = 0; k < L - 1; ++k) {
+            F += pr[k];
+            const double T = ceil(F * 4294967296.0);
+            out[k] = T < 1.0 ? 0u : (T > 4294967296.0 ? 0xFFFFFFFFu : (uint32_t)(T - 1.0));
+        }
+    };
+    if (L == 2) {
+        for (int np = 0; np <= 8; ++np)
+            for (int n1 = 0; n1 <= 8; ++n1)
+                for (int gl = 0; gl < 2; ++gl) {
+                    uint32_t* out = &m.thr2[(np * 9 + n1) * 2 + gl];
+                    if (n1 > np) {
+                        *out = 0u;
+                        continue;
+                    }
+                    const int n[2] = {np - n1, n1};
+                    thresholds(n, gl, out);
+                }
+    } else if (ctx->lay.gthr_entries) {
+        const int NB = c.neighborhood;
+        int n[UTHR_MAX_LEVELS];
+        uint32_t* out = ctx->gthr_host.data();
+        for (int s0 = 0; s0 < L; ++s0) {
+            for (int s = 0; s < L; ++s) n[s] = (s == s0) ? NB : 0;
+            for (int gl = 0; gl < L; ++gl, out += L - 1) thresholds(n, gl, out);
+        }
+        CK(ctx, cudaMemcpyAsync(ctx->gthr, ctx->gthr_host.data(),
+                                ctx->gthr_host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                ctx->stream));
+    }
+    ctx->gtab_stage = stage;
+    return PCA_OK;
+}
+
 void fill_common(pca_ctx* ctx, SweepCommon& sc, int64_t t, int count) {
     sc.geo = ctx->geo;
     sc.x_in = ctx->x[ctx->cur];
@@ -572,6 +644,8 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->stage = ctx->ws + L.off_stage;
     ctx->uthr = L.uthr_entries ? (uint32_t*)(ctx->ws + L.off_uthr) : nullptr;
     ctx->uthr_host.resize(L.uthr_entries);
+    ctx->gthr = L.gthr_entries ? (uint32_t*)(ctx->ws + L.off_gthr) : nullptr;
+    ctx->gthr_host.resize(L.gthr_entries);
     ctx->kernel = (cfg->kernel == PCA_KERNEL_AUTO) ? (cfg->levels == 2 ? PCA_KERNEL_BINARY
                                                                        : PCA_KERNEL_GENERAL)
                                                    : cfg->kernel;
@@ -607,6 +681,8 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->gen.itab = ctx->itab;
     ctx->gen.inertia_p = cfg->inertia_p;
     ctx->gen.uthr = ctx->uthr;
+    ctx->gib.dtab = ctx->dtab;
+    ctx->gib.uthr = ctx->gthr;
 
     auto bail = [&](pca_status s) {
         delete ctx;
@@ -719,6 +795,47 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             if (st != PCA_OK) return st;
         }
         ctx->cur ^= 1;
+        ctx->t = t + 1;
+        ctx->counted += count;
+    }
+    return PCA_OK;
+}
+
+pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
+    const pca_config& c = ctx->cfg;
+    if (c.periodic && ((c.height & 1) || (c.width & 1)))
+        return fail(PCA_EUNSUPPORTED, "the Gibbs colouring needs even height and width on a torus");
+    const bool strip = ctx->lay.rows < c.height;
+    if (strip && !(ctx->comm && ctx->nranks > 1))
+        return fail(PCA_EINVAL, "a row-strip Gibbs sweep exchanges halos between colours: attach NCCL");
+    const int ncol = c.neighborhood == 4 ? 2 : 4;
+    for (int32_t i = 0; i < n; ++i) {
+        const int64_t t = ctx->t;
+        if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
+        st = build_gibbs_tables(ctx, t);
+        if (st != PCA_OK) return st;
+        const int count = (c.mpm_burn_in >= 0 && t >= c.mpm_burn_in) ? 1 : 0;
+        if (count && ctx->counted + 1 > 65535)
+            return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+        fill_common(ctx, ctx->gib.c, t, 0);
+        ctx->gib.c.x_out = ctx->x[ctx->cur];  // in place
+        ctx->gib.c.rlo = 0;
+        ctx->gib.c.rhi = ctx->lay.rows;
+        for (int k = 0; k < ncol; ++k) {
+            ctx->gib.colour = k;
+            ctx->gib.c.count_enable = count && (k & 1);  // rows are final after colour 1 / 3
+            ctx->launches++;
+            ctx->sweep_launches++;
+            const int e = launch_sweep_gibbs(ctx->gib, c.batch, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep");
+            if (strip) {
+                st = exchange(ctx, ctx->x[ctx->cur], 1);
+                if (st != PCA_OK) return st;
+            }
+        }
         ctx->t = t + 1;
         ctx->counted += count;
     }
