@@ -98,6 +98,9 @@ def lib():
             "orc_gibbs_sweep_coloured": (None, [mp, u8p, u8p, ctypes.c_double, ctypes.c_uint64,
                                                 ctypes.c_uint32, ctypes.c_uint32]),
             "orc_gibbs_colour": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+            "orc_gibbs_colour_phase": (None, [mp, u8p, u8p, ctypes.c_double, ctypes.c_uint64,
+                                              ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
+                                              ctypes.c_int, ctypes.c_int]),
             "orc_mpm": (None, [u32p, ctypes.c_int, ctypes.c_size_t, u8p]),
             "orc_metrics": (ctypes.c_int, [u8p, u8p, ctypes.c_size_t, ctypes.c_int, f64p, f64p,
                                            f64p]),
@@ -218,6 +221,16 @@ def gibbs_sweep_coloured(m: Model, x, g, beta, seed, chain, t):
     g = _u8(g)
     lib().orc_gibbs_sweep_coloured(ctypes.byref(m), _p(x, ctypes.c_uint8), _p(g, ctypes.c_uint8),
                                    beta, seed, chain, t)
+    return x
+
+
+def gibbs_colour_phase(m: Model, x, g, beta, seed, chain, t, k, rows=None):
+    """Colour k of the colour-order scan over rows [r0, r1) (default all), in place on a copy."""
+    x = _u8(x).copy()
+    g = _u8(g)
+    r0, r1 = rows if rows is not None else (0, m.H)
+    lib().orc_gibbs_colour_phase(ctypes.byref(m), _p(x, ctypes.c_uint8), _p(g, ctypes.c_uint8),
+                                 beta, seed, chain, t, k, r0, r1)
     return x
 
 

@@ -258,24 +258,30 @@ int orc_gibbs_colour(int nbhd, int r, int c) {
     return nbhd == 4 ? ((r + c) & 1) : (((r & 1) << 1) | (c & 1));
 }
 
-/* One systematic Gibbs sweep in colour order: for colour
- * k = 0, 1, ... every site of colour k in row-major order, in place, each from its Gibbs
- * conditional given the CURRENT configuration.  Random word: tag GIBBS, counter t.       */
-void orc_gibbs_sweep_coloured(const orc_model* m, uint8_t* x, const uint8_t* g, double beta,
-                              uint64_t seed, uint32_t chain, uint32_t t) {
+/* One colour phase of the colour-order scan: every site of colour k in rows [r_begin, r_end),
+ * row-major, in place, from its Gibbs conditional given the CURRENT
+ * configuration.  Random word: tag GIBBS, counter t.                                      */
+void orc_gibbs_colour_phase(const orc_model* m, uint8_t* x, const uint8_t* g, double beta,
+                            uint64_t seed, uint32_t chain, uint32_t t, int k, int r_begin,
+                            int r_end) {
     double p[256];
-    const int ncol = m->nbhd == 4 ? 2 : 4;
-    for (int k = 0; k < ncol; k++) {
-        for (int r = 0; r < m->H; r++) {
-            for (int c = 0; c < m->W; c++) {
-                if (orc_gibbs_colour(m->nbhd, r, c) != k) continue;
-                site_probs(m, x, g, r, c, beta, 0, p);
-                uint32_t rnd = orc_draw(seed, ORC_TAG_GIBBS, chain, t, (uint32_t)r, (uint32_t)c);
-                double u = (double)rnd * (1.0 / 4294967296.0);
-                x[r * m->W + c] = (uint8_t)orc_decide(p, m->levels, u, NULL);
-            }
+    for (int r = r_begin; r < r_end; r++) {
+        for (int c = 0; c < m->W; c++) {
+            if (orc_gibbs_colour(m->nbhd, r, c) != k) continue;
+            site_probs(m, x, g, r, c, beta, 0, p);
+            uint32_t rnd = orc_draw(seed, ORC_TAG_GIBBS, chain, t, (uint32_t)r, (uint32_t)c);
+            double u = (double)rnd * (1.0 / 4294967296.0);
+            x[r * m->W + c] = (uint8_t)orc_decide(p, m->levels, u, NULL);
         }
     }
+}
+
+/* One systematic Gibbs sweep in colour order: colour 0, 1, ...,
+ * each phase over the whole lattice.                                                      */
+void orc_gibbs_sweep_coloured(const orc_model* m, uint8_t* x, const uint8_t* g, double beta,
+                              uint64_t seed, uint32_t chain, uint32_t t) {
+    const int ncol = m->nbhd == 4 ? 2 : 4;
+    for (int k = 0; k < ncol; k++) orc_gibbs_colour_phase(m, x, g, beta, seed, chain, t, k, 0, m->H);
 }
 
 /* n Gibbs sweeps t = t0 .. t0+n-1; order 0 = the paper's column-major scan, 1 = colour

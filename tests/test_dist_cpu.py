@@ -28,7 +28,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q):
+def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q, method="pca"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -70,10 +70,17 @@ def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q):
 
         exchange(x)
         for t in range(nsweeps):
-            new, _ = orc.pca_sweep(m, x, g, 1.25, 99, 0, t, rows=(row0, row0 + rows))
-            x = rng.integers(0, levels, (H, W), dtype=np.uint8)  # fresh poison every sweep
-            x[row0:row0 + rows] = new
-            exchange(x)
+            if method == "pca":
+                new, _ = orc.pca_sweep(m, x, g, 1.25, 99, 0, t, rows=(row0, row0 + rows))
+                x = rng.integers(0, levels, (H, W), dtype=np.uint8)  # fresh poison every sweep
+                x[row0:row0 + rows] = new
+                exchange(x)
+            else:  # Gibbs: one colour phase on the strip, then a halo exchange (runtime order)
+                for k in range(4):
+                    new = orc.gibbs_colour_phase(m, x, g, 1.25, 99, 0, t, k, rows=(row0, row0 + rows))
+                    x = rng.integers(0, levels, (H, W), dtype=np.uint8)
+                    x[row0:row0 + rows] = new[row0:row0 + rows]
+                    exchange(x)
         strips = [None] * world
         dist.all_gather_object(strips, (row0, x[row0:row0 + rows].copy()))
         if rank == 0:
@@ -82,7 +89,10 @@ def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q):
                 full[r0:r0 + len(s)] = s
             ref = g.copy()
             for t in range(nsweeps):
-                ref, _ = orc.pca_sweep(m, ref, g, 1.25, 99, 0, t)
+                if method == "pca":
+                    ref, _ = orc.pca_sweep(m, ref, g, 1.25, 99, 0, t)
+                else:
+                    ref = orc.gibbs_sweep_coloured(m, ref, g, 1.25, 99, 0, t)
             out_q.put(bool(np.array_equal(full, ref)))
     finally:
         dist.destroy_process_group()
@@ -94,6 +104,25 @@ def test_two_rank_strip_exchange_reproduces_unsharded_chain(periodic):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, 13, 11, 3, periodic, 6, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_two_rank_strip_gibbs_reproduces_unsharded_chain(periodic):
+    """pca_gibbs_sweep's strip protocol: every colour phase on the owned rows followed by a
+    halo exchange reproduces the unsharded colour-order scan (even torus sides)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    H, W = (14, 12) if periodic else (13, 11)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, H, W, 3, periodic, 5, q, "gibbs"))
              for r in range(2)]
     for p in procs:
         p.start()
