@@ -1,0 +1,98 @@
+"""PCA vs Gibbs on the GPU (the run-time comparison PAPER.md:723 calls for) -- developer tool.
+
+    python tools/pca_vs_gibbs.py
+
+For each config: device time per sweep of the synchronous PCA (pca_sweep, one launch per
+sweep) and of the checkerboard Gibbs sampler (pca_gibbs_sweep, one launch per colour), and,
+for the config-2 images (256x256, Moore-8, free, paper protocol: 1000 sweeps, beta 1.25 +
+0.25 every 250, MPM over the last 250), the restoration quality of both: PSNR, global SSIM
+and 7x7 windowed SSIM of the last sample and of the MPM estimate.  Writes
+gpurun_out/pca_vs_gibbs.json.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2507_14869_b200 as P  # noqa: E402
+import synth  # noqa: E402
+
+
+def timed(ctx, method, sweeps):
+    run = ctx.pca_sweep if method == "pca" else ctx.pca_gibbs_sweep
+    run(min(sweeps, 10))
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(3):
+        ctx.pca_reset(None, None)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(ctx.stream)
+        run(sweeps)
+        b.record(ctx.stream)
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best
+
+
+def main():
+    out = []
+    cases = [
+        ("c1 64x64 l2 vn4 torus", P.make_config(64, 64, 2, neighborhood=4, periodic=True, sigma=0.5,
+                                                 beta_period=50, mpm_burn_in=100),
+         synth.degrade(synth.smooth_labels(64, 64, 2, 1), 2, 0.5, 2)[None], 200),
+        ("c2 256x256 l5 moore free", P.make_config(256, 256, 5, sigma=0.25, mpm_burn_in=750),
+         synth.degrade(synth.smooth_labels(256, 256, 5, 3), 5, 0.25, 4)[None], 1000),
+        ("c3 8192x8192 l2 moore torus mpm", P.make_config(8192, 8192, 2, periodic=True, sigma=0.5,
+                                                           beta0=1.5, beta_step=0, mpm_burn_in=0),
+         synth.degrade(synth.tiled_labels(8192, 8192, 2, 1), 2, 0.5, 2)[None], 50),
+        ("c3 8192x8192 l5 moore torus mpm", P.make_config(8192, 8192, 5, periodic=True, sigma=0.25,
+                                                           beta0=1.5, beta_step=0, mpm_burn_in=0),
+         synth.degrade(synth.tiled_labels(8192, 8192, 5, 1), 5, 0.25, 2)[None], 10),
+    ]
+    for name, cfg, g, sweeps in cases:
+        ctx = P.PcaContext(cfg, torch.from_numpy(np.ascontiguousarray(g)).cuda())
+        row = {"config": name, "sweeps": sweeps}
+        for method in ("pca", "gibbs"):
+            ms = timed(ctx, method, sweeps)
+            sites = cfg.batch * cfg.height * cfg.width
+            row[method] = {"us_per_sweep": 1e3 * ms / sweeps, "SU_per_s": sites * sweeps / (ms * 1e-3)}
+        row["gibbs_over_pca_time"] = row["gibbs"]["us_per_sweep"] / row["pca"]["us_per_sweep"]
+        print(json.dumps(row), flush=True)
+        out.append(row)
+        ctx.pca_destroy()
+
+    # restoration quality on config-2-sized images (synthetic smooth label fields)
+    for L, sg in [(5, 0.25), (9, 0.2), (33, 0.1)]:
+        truth = synth.smooth_labels(256, 256, L, seed=L)
+        g = synth.degrade(truth, L, sg, seed=L + 50)
+        row = {"config": f"c2 quality l{L} sigma {sg}", "noisy_psnr": None}
+        for method in ("pca", "gibbs"):
+            cfg = P.make_config(256, 256, L, sigma=sg, seed=2025 + L, mpm_burn_in=750)
+            ctx = P.PcaContext(cfg, torch.from_numpy(g[None].copy()).cuda())
+            if row["noisy_psnr"] is None:
+                p0, s0 = ctx.pca_psnr_ssim(truth[None], P.EST_LAST)
+                row["noisy_psnr"], row["noisy_ssim"] = float(p0[0]), float(s0[0])
+                row["noisy_ssim_windowed"] = float(ctx.pca_ssim_windowed(truth[None], P.EST_LAST)[0])
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(ctx.stream)
+            (ctx.pca_sweep if method == "pca" else ctx.pca_gibbs_sweep)(1000)
+            b.record(ctx.stream)
+            torch.cuda.synchronize()
+            res = {"ms_1000_sweeps": a.elapsed_time(b)}
+            for kind, kn in [(P.EST_LAST, "last"), (P.EST_MPM, "mpm")]:
+                p, s = ctx.pca_psnr_ssim(truth[None], kind)
+                res[f"{kn}_psnr"], res[f"{kn}_ssim"] = float(p[0]), float(s[0])
+                res[f"{kn}_ssim_windowed"] = float(ctx.pca_ssim_windowed(truth[None], kind)[0])
+            row[method] = res
+            ctx.pca_destroy()
+        print(json.dumps(row), flush=True)
+        out.append(row)
+    os.makedirs("gpurun_out", exist_ok=True)
+    json.dump(out, open(os.path.join("gpurun_out", "pca_vs_gibbs.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
