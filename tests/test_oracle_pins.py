@@ -282,6 +282,18 @@ def test_windowed_ssim_properties():
     ref = ((2 * la.mean() * lb.mean() + 1e-4) * (2 * cov + 9e-4)) / (
         (la.mean() ** 2 + lb.mean() ** 2 + 1e-4) * (la.var(ddof=1) + lb.var(ddof=1) + 9e-4))
     assert orc.ssim_windowed(a, b, 5) == pytest.approx(ref, abs=1e-13)
+    # a change at the corner pixel touches only the window at (0, 0): the mean over the
+    # (H-6)(W-6) stride-1 windows is (count - 1 + SSIM_window(0,0)) / count
+    def one(wa, wb):
+        la, lb = wa / 4.0, wb / 4.0
+        cv = ((la - la.mean()) * (lb - lb.mean())).sum() / 48
+        return ((2 * la.mean() * lb.mean() + 1e-4) * (2 * cv + 9e-4)) / (
+            (la.mean() ** 2 + lb.mean() ** 2 + 1e-4) * (la.var(ddof=1) + lb.var(ddof=1) + 9e-4))
+    c = z.copy()
+    c[0, 0] = (c[0, 0] + 3) % 5
+    count = (20 - 6) * (23 - 6)
+    assert orc.ssim_windowed(z, c, 5) == pytest.approx((count - 1 + one(z[:7, :7], c[:7, :7])) / count,
+                                                        abs=1e-13)
 
 
 def test_quantizer():
