@@ -319,7 +319,17 @@ __global__ void __launch_bounds__(SSIM_TPB) ssim_windowed_kernel(const WinSsimPa
     }
 }
 
+__global__ void param_table_kernel(const __grid_constant__ ParamTable t, int n, uint32_t* dst) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = t.v[i];
+}
+
 }  // namespace
+
+int launch_param_table(const ParamTable& t, int n, uint32_t* dst, void* stream) {
+    if (n < 0 || n > PARAM_TABLE_MAX) return (int)cudaErrorInvalidValue;
+    param_table_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(t, n, dst);
+    return (int)cudaGetLastError();
+}
 
 int launch_pack_state(const Geometry& G, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad, void* stream) {

@@ -65,9 +65,11 @@ struct SweepCommon {
 
 // levels == 2 fast path: thr[((np*9 + n1)*2 + g)*2 + x] = ceil(p0 * 2^32) - 1, the
 // largest Philox word r for which the new label is 0 (u = r 2^-32 < F_0 = p0).
+// The table lives in the workspace (uploaded once per beta stage) and reaches shared memory
+// with one TMA bulk copy per CTA.
 struct BinarySweepParams {
     SweepCommon c;
-    uint32_t thr[THR_ENTRIES];
+    const uint32_t* thr;  // device [THR_ENTRIES]
 };
 
 // two sweeps (t, t+1) per pass: thr[0] for sweep t, thr[1] for sweep t+1; c.count_enable
@@ -125,6 +127,13 @@ int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thre
                         void* stream);
 int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream);
 int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream);
+// copy a small host table into device memory through the kernel parameter block (stream
+// ordered, no host synchronisation, no pinned staging buffer to protect)
+constexpr int PARAM_TABLE_MAX = 1024;
+struct ParamTable {
+    uint32_t v[PARAM_TABLE_MAX];
+};
+int launch_param_table(const ParamTable& t, int n, uint32_t* dst, void* stream);
 int launch_sweep_binary2(const Binary2SweepParams& p, int batch, int rows_per_thread, void* stream);
 int launch_pack_state(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad_flag, void* stream);

@@ -101,6 +101,7 @@ struct Layout {
     size_t gbuf = 0;      // bytes of the g buffer
     size_t off_uthr = 0, uthr_entries = 0;
     size_t off_gthr = 0, gthr_entries = 0;  // Gibbs uniform-neighbourhood thresholds
+    size_t off_bthr = 0;                    // binary PCA thresholds [THR_ENTRIES]
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
            off_sums_max = 0, off_flag = 0, off_stage = 0;
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
@@ -182,6 +183,7 @@ Layout make_layout(const pca_config* c) {
     L.gthr_entries = (c->levels > 2 && c->levels <= UTHR_MAX_LEVELS)
                          ? (size_t)c->levels * c->levels * (c->levels - 1) : 0;
     L.off_gthr = o; o = align256(o + L.gthr_entries * sizeof(uint32_t));
+    L.off_bthr = o; o = align256(o + THR_ENTRIES * sizeof(uint32_t));
     L.off_sums = o; o = align256(o + B * 8 * sizeof(unsigned long long));
     L.off_sums_max = o; o = align256(o + B * 8 * sizeof(unsigned long long));
     L.off_flag = o; o = align256(o + 256);
@@ -219,6 +221,7 @@ struct pca_ctx {
     int64_t tab_stage = -1;
     int64_t gtab_stage = -1;
     GibbsSweepParams gib;
+    uint32_t bthr_host[THR_ENTRIES];  // binary thresholds of the current stage (host copy)
     std::vector<uint32_t> gthr_host;
     uint32_t* gthr = nullptr;
     BinarySweepParams bin;
@@ -343,7 +346,7 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
                     for (int xl = 0; xl < 2; ++xl) {
                         const int idx = ((np * 9 + n1) * 2 + gl) * 2 + xl;
                         if (n1 > np) {
-                            ctx->bin.thr[idx] = 0u;
+                            ctx->bthr_host[idx] = 0u;
                             continue;
                         }
                         const int n[2] = {np - n1, n1};
@@ -364,8 +367,11 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
                         // differs from the exact rule only for r = 0, where u = 0 = F_0 is an
                         // exact tie (an allowed near-tie, R19).
                         const double T = ceil(p0 * 4294967296.0);
-                        ctx->bin.thr[idx] = T >= 1.0 ? (uint32_t)(T - 1.0) : 0u;
+                        ctx->bthr_host[idx] = T >= 1.0 ? (uint32_t)(T - 1.0) : 0u;
                     }
+        ParamTable pt;
+        memcpy(pt.v, ctx->bthr_host, sizeof(ctx->bthr_host));
+        LAUNCH(ctx, launch_param_table(pt, THR_ENTRIES, const_cast<uint32_t*>(ctx->bin.thr), ctx->stream));
     } else {
         GeneralSweepParams& m = ctx->gen;
         for (int n = 0; n <= 8; ++n) m.A[n] = exp(a * (double)n);
@@ -681,6 +687,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->gen.itab = ctx->itab;
     ctx->gen.inertia_p = cfg->inertia_p;
     ctx->gen.uthr = ctx->uthr;
+    ctx->bin.thr = (const uint32_t*)(ctx->ws + L.off_bthr);
     ctx->gib.dtab = ctx->dtab;
     ctx->gib.uthr = ctx->gthr;
 
@@ -728,10 +735,10 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
                 return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
             st = build_tables(ctx, t);
             if (st != PCA_OK) return st;
-            memcpy(ctx->bin2.thr[0], ctx->bin.thr, sizeof(ctx->bin.thr));
+            memcpy(ctx->bin2.thr[0], ctx->bthr_host, sizeof(ctx->bthr_host));
             st = build_tables(ctx, t + 1);
             if (st != PCA_OK) return st;
-            memcpy(ctx->bin2.thr[1], ctx->bin.thr, sizeof(ctx->bin.thr));
+            memcpy(ctx->bin2.thr[1], ctx->bthr_host, sizeof(ctx->bthr_host));
             fill_common(ctx, ctx->bin2.c, t, c0);
             ctx->bin2.count2 = c1;
             ctx->bin2.c.rlo = 0;

@@ -44,6 +44,8 @@ constexpr int XOFS = 0, GOFS = 2 * XROW_BYTES, COFS = GOFS + 2 * GROW_BYTES;
 constexpr int STAGE_BYTES = COFS + 2 * CROW_BYTES;     // 4160
 
 constexpr int RING_OFFSET = 64;                        // mbarriers first, then the ring
+static_assert(KSTAGES + 1 <= RING_OFFSET / 8, "mbarrier slots");
+static_assert(THR_ENTRIES * 4 % 16 == 0, "bulk copy size");
 constexpr int SMEM_BYTES = RING_OFFSET + KSTAGES * STAGE_BYTES;  // dynamic smem per CTA
 
 // Map label bytes to {0,1}: 0 -> 0, 1 -> 1, free-boundary sentinel 0xFF -> 0.
@@ -72,9 +74,8 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     uint8_t* ring = smem + RING_OFFSET;
     const int lane = threadIdx.x;
-    for (int i = lane; i < THR_ENTRIES; i += 32) s_thr[i] = p.thr[i];
     if (lane == 0) {
-        for (int s = 0; s < KSTAGES; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s <= KSTAGES; ++s) mbar_init(&bars[s], 1);  // bars[KSTAGES]: the table
         fence_mbar_init();
     }
     __syncwarp();
@@ -121,8 +122,12 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
                          &bars[s]);
         }
     };
-    if (elect_one())
+    if (elect_one()) {
+        mbar_expect_tx(&bars[KSTAGES], THR_ENTRIES * 4);
+        bulk_g2s(s_thr, p.thr, THR_ENTRIES * 4, &bars[KSTAGES]);
         for (int it = 0; it < min(KSTAGES, nitems); ++it) issue(it, it);
+    }
+    mbar_wait(&bars[KSTAGES], 0);
 
     auto read_x = [&](const uint8_t* st, int q, XRow& x) {
         const uint8_t* xr = st + XOFS + q * XROW_BYTES;
