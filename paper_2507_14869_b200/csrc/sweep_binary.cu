@@ -13,9 +13,11 @@
 // per lane) of a run of R rows and streams it through a private KSTAGES-deep shared-memory
 // ring filled by 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) that complete on
 // per-stage mbarriers.  A stage carries TWO rows: two padded x rows (544 B each, incl. the
-// words left/right of the segment), two g rows (512 B) and two rows of uint16 MPM counts
-// (1 KiB), so the per-stage bookkeeping (wait, refill, fence, address arithmetic) is paid
-// once per two rows.  The 4-row neighbourhood window lives in registers; neighbour counts
+// words left/right of the segment) and two g rows (512 B); the two rows of uint16 MPM
+// counts (1 KiB each) ride in the stage too on a free boundary, while on a torus each lane
+// prefetches its counts into registers one item ahead, which halves the stage and lets 16
+// instead of 12 warps share an SM (RingCfg).  The per-stage bookkeeping (wait, refill,
+// fence, address arithmetic) is paid once per two rows.  The 4-row neighbourhood window lives in registers; neighbour counts
 // are SWAR byte sums (vertical sum of 3 rows, then funnel-shifted left/right sums); the table
 // index of each site is one byte of a pre-scaled SWAR word, extracted with one PRMT.  One
 // Philox4x32-10 call serves 4 sites.  The MPM count of label 1 (uint16) is updated in the
@@ -28,25 +30,47 @@
 namespace pcab200 {
 namespace {
 
-#ifndef PCA_KSTAGES
-#define PCA_KSTAGES 4  // measured on B200 (tools/tune_variants.py): 4 stages x 12 CTAs/SM
-#endif                 // beat 2x20, 3x16, 5x10, 6x8 and 8x6 at 8192^2
-#ifndef PCA_MIN_CTAS
-#define PCA_MIN_CTAS 12
+// Ring depth x resident CTAs x where the MPM counts travel, per boundary kind, measured on
+// B200 with tools/tune_variants.py at 8192^2 (us per sweep, MPM on):
+//   torus: counts prefetched into registers one item ahead (stage = x + g rows only),
+//          4 stages x 16 CTAs/SM: 84.8 (counts in the ring, 4 x 12: 86.2; 3 x 20: 94.4;
+//          5 x 16: 94.1; 6 x 14: 97.1; 8 x 12: 93.8)
+//   free:  counts in the ring, 4 x 12: 90.8 (registers, 4 x 16: 98.7)
+#ifndef PCA_T_K
+#define PCA_T_K 4
 #endif
-constexpr int KSTAGES = PCA_KSTAGES;                   // ring depth per warp (2 rows each)
-constexpr int MIN_CTAS = PCA_MIN_CTAS;                 // resident one-warp CTAs per SM
+#ifndef PCA_T_CTAS
+#define PCA_T_CTAS 16
+#endif
+#ifndef PCA_T_CREG
+#define PCA_T_CREG 1
+#endif
+#ifndef PCA_F_K
+#define PCA_F_K 4
+#endif
+#ifndef PCA_F_CTAS
+#define PCA_F_CTAS 12
+#endif
+#ifndef PCA_F_CREG
+#define PCA_F_CREG 0
+#endif
 constexpr int SEG_CHUNKS = 32;                         // 16-site chunks per warp segment
 constexpr int XROW_BYTES = 16 * SEG_CHUNKS + 32;       // 544: [col0-16, col0+528)
 constexpr int GROW_BYTES = 16 * SEG_CHUNKS;            // 512
 constexpr int CROW_BYTES = 32 * SEG_CHUNKS;            // 1024
 constexpr int XOFS = 0, GOFS = 2 * XROW_BYTES, COFS = GOFS + 2 * GROW_BYTES;
-constexpr int STAGE_BYTES = COFS + 2 * CROW_BYTES;     // 4160
 
-constexpr int RING_OFFSET = 64;                        // mbarriers first, then the ring
-static_assert(KSTAGES + 1 <= RING_OFFSET / 8, "mbarrier slots");
+template <bool PER>
+struct RingCfg {
+    static constexpr int K = PER ? PCA_T_K : PCA_F_K;           // ring depth (2 rows per stage)
+    static constexpr int CTAS = PER ? PCA_T_CTAS : PCA_F_CTAS;  // resident one-warp CTAs per SM
+    static constexpr bool CREG = PER ? PCA_T_CREG : PCA_F_CREG; // counts via registers
+    static constexpr int STAGE = COFS + (CREG ? 0 : 2 * CROW_BYTES);  // 2112 or 4160 bytes
+    static constexpr int RING_OFF = ((K + 1) * 8 + 63) / 64 * 64;    // mbarriers, then the ring
+    static constexpr int SMEM = RING_OFF + K * STAGE;                // dynamic smem per CTA
+    static_assert(K + 1 <= RING_OFF / 8, "mbarrier slots");
+};
 static_assert(THR_ENTRIES * 4 % 16 == 0, "bulk copy size");
-constexpr int SMEM_BYTES = RING_OFFSET + KSTAGES * STAGE_BYTES;  // dynamic smem per CTA
 
 // Map label bytes to {0,1}: 0 -> 0, 1 -> 1, free-boundary sentinel 0xFF -> 0.
 __device__ __forceinline__ uint32_t to01(uint32_t w) { return w & ~(w >> 1) & 0x01010101u; }
@@ -67,12 +91,16 @@ struct XRow {
 // from blockIdx and kernel parameters only, so the compiler keeps it in uniform registers and
 // the bulk-copy issue needs no per-lane address handling.
 template <int NB, bool PER>
-__global__ void __launch_bounds__(32, MIN_CTAS)
+__global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     sweep_binary_kernel(const __grid_constant__ BinarySweepParams p, int R) {
+    using C = RingCfg<PER>;
+    constexpr int KSTAGES = C::K;
+    constexpr int STAGE_BYTES = C::STAGE;
+    constexpr bool CREG = C::CREG;  // counts prefetched into registers (no ring slot)
     __shared__ __align__(16) uint32_t s_thr[THR_ENTRIES];  // static: LDS [reg + imm]
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    uint8_t* ring = smem + RING_OFFSET;
+    uint8_t* ring = smem + C::RING_OFF;
     const int lane = threadIdx.x;
     if (lane == 0) {
         for (int s = 0; s <= KSTAGES; ++s) mbar_init(&bars[s], 1);  // bars[KSTAGES]: the table
@@ -104,6 +132,19 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
     uint16_t* co = p.c.counts + chain * G.cchain + ccol + (long long)rbeg * G.cpitch;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const uint8_t* thr_b = reinterpret_cast<const uint8_t*>(s_thr);
+    // CREG: the count rows of the next two updated rows, loaded one item ahead
+    uint4 CR[2][2];
+    auto load_counts = [&](int rfirst) {
+        if (!CREG || !cbytes || !active) return;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (rfirst + q < rend) {
+                const uint4* src = reinterpret_cast<const uint4*>(co + (long long)(rfirst + q - rbeg) * G.cpitch);
+                CR[q][0] = __ldcs(src);
+                CR[q][1] = __ldcs(src + 1);
+            }
+        }
+    };
 
     // elected lane: load item `it` into stage s (rows past the run are skipped)
     auto issue = [&](int it, int s) {
@@ -112,12 +153,12 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
         const int nx = (rbeg - 1 + jx + 1 <= rend) ? 2 : 1;
         const int jr = 2 * it - 2;         // g / count row rbeg+jr
         const int nr = it == 0 ? 0 : min(2, rend - rbeg - jr);
-        mbar_expect_tx(&bars[s], nx * xbytes + nr * (gbytes + cbytes));
+        mbar_expect_tx(&bars[s], nx * xbytes + nr * (gbytes + (CREG ? 0u : cbytes)));
         for (int q = 0; q < nx; ++q)
             bulk_g2s(st + XOFS + q * XROW_BYTES, xin + (long long)(jx + q) * G.xpitch, xbytes, &bars[s]);
         for (int q = 0; q < nr; ++q) {
             bulk_g2s(st + GOFS + q * GROW_BYTES, gin + (long long)(jr + q) * G.gpitch, gbytes, &bars[s]);
-            if (cbytes)
+            if (!CREG && cbytes)
                 bulk_g2s(st + COFS + q * CROW_BYTES, cin + (long long)(jr + q) * G.cpitch, cbytes,
                          &bars[s]);
         }
@@ -196,8 +237,15 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
         }
         // ---- fused MPM counts of label 1 (uint16 per site) ----
         if (cbytes) {
-            const uint4* cs = reinterpret_cast<const uint4*>(st + COFS + q * CROW_BYTES + 32 * lane);
-            uint4 c0 = cs[0], c1 = cs[1];
+            uint4 c0, c1;
+            if (CREG) {
+                c0 = CR[q][0];
+                c1 = CR[q][1];
+            } else {
+                const uint4* cs = reinterpret_cast<const uint4*>(st + COFS + q * CROW_BYTES + 32 * lane);
+                c0 = cs[0];
+                c1 = cs[1];
+            }
             c0.x += __byte_perm(O[0], 0u, 0x4140); c0.y += __byte_perm(O[0], 0u, 0x4342);
             c0.z += __byte_perm(O[1], 0u, 0x4140); c0.w += __byte_perm(O[1], 0u, 0x4342);
             c1.x += __byte_perm(O[2], 0u, 0x4140); c1.y += __byte_perm(O[2], 0u, 0x4342);
@@ -290,8 +338,15 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
             const int r = r0 + q;
             // ---- fused MPM counts of label 1 (uint16 per site) ----
             if (cbytes) {
-                const uint4* cs = reinterpret_cast<const uint4*>(st + COFS + q * CROW_BYTES + 32 * lane);
-                uint4 c0 = cs[0], c1 = cs[1];
+                uint4 c0, c1;
+                if (CREG) {
+                    c0 = CR[q][0];
+                    c1 = CR[q][1];
+                } else {
+                    const uint4* cs = reinterpret_cast<const uint4*>(st + COFS + q * CROW_BYTES + 32 * lane);
+                    c0 = cs[0];
+                    c1 = cs[1];
+                }
                 c0.x += __byte_perm(O[q][0], 0u, 0x4140); c0.y += __byte_perm(O[q][0], 0u, 0x4342);
                 c0.z += __byte_perm(O[q][1], 0u, 0x4140); c0.w += __byte_perm(O[q][1], 0u, 0x4342);
                 c1.x += __byte_perm(O[q][2], 0u, 0x4140); c1.y += __byte_perm(O[q][2], 0u, 0x4342);
@@ -308,6 +363,7 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
 
     // window: A0 = x row r0-1, A1 = x row r0 (previous item), B0 = r0+1, B1 = r0+2 (current)
     XRow A0, A1, B0, B1;
+    load_counts(rbeg);
     int s = 0;
     uint32_t phase = 0;
     for (int it = 0; it < nitems; ++it) {
@@ -324,6 +380,7 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
                     update(r0, st, 0, A0, A1, B0);
                     if (r0 + 1 < rend) update(r0 + 1, st, 1, A1, B0, B1);
                 }
+                load_counts(r0 + 2);
             }
         }
         // every lane is done with this stage: refill it with item it + KSTAGES
@@ -348,13 +405,13 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     static int occ = 0, sms = 0;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, RingCfg<PER>::SMEM);
         if (e != cudaSuccess) return (int)e;
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_binary_kernel<NB, PER>, 32,
-                                                      SMEM_BYTES);
+                                                      RingCfg<PER>::SMEM);
         if (occ < 1) occ = 1;
         configured = true;
     }
@@ -371,7 +428,7 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     if (nrb <= 0) return 0;
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS, nrb, batch);
-    sweep_binary_kernel<NB, PER><<<grid, 32, SMEM_BYTES, s>>>(p, R);
+    sweep_binary_kernel<NB, PER><<<grid, 32, RingCfg<PER>::SMEM, s>>>(p, R);
     return (int)cudaGetLastError();
 }
 
