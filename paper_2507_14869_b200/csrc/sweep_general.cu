@@ -26,11 +26,12 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#include "tma_ring.cuh"  // from_left / from_right byte funnels
 
 namespace pcab200 {
 namespace {
 
-constexpr int GEN_THREADS = 256;
+constexpr int GEN_THREADS = 128;
 constexpr int GEN_WARPS = GEN_THREADS / 32;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
@@ -157,92 +158,121 @@ __device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const 
     return L - 1;
 }
 
+// Uniform-neighbourhood thresholds staged in shared memory when the table is small.
+__host__ __device__ constexpr int uthr_smem_entries(int LT) { return (LT > 0 && LT <= 9) ? LT * LT * LT * (LT - 1) : 1; }
+
 template <int NB, int LT>  // LT: levels known at compile time, 0 = any
-__global__ void __launch_bounds__(GEN_THREADS, 2)
-    sweep_general_kernel(const __grid_constant__ GeneralSweepParams p) {
+__global__ void __launch_bounds__(GEN_THREADS, 4)
+    sweep_general_kernel(const __grid_constant__ GeneralSweepParams p, int R) {
     __shared__ double sA[9];
     __shared__ double sD[LT > 0 ? LT * LT : 1];
     __shared__ double sI[LT > 0 ? LT * LT : 1];
+    __shared__ uint32_t sU[uthr_smem_entries(LT)];
     __shared__ SiteJob s_jobs[GEN_WARPS][128];
     __shared__ uint8_t s_res[GEN_WARPS][128];
+    constexpr bool SMEM_U = LT > 0 && LT <= 9;
     if (threadIdx.x < 9) sA[threadIdx.x] = p.A[threadIdx.x];
     if (LT > 0)
         for (int i = threadIdx.x; i < LT * LT; i += GEN_THREADS) {
             sD[i] = p.dtab[i];
             sI[i] = p.inertia_p != 0 ? p.itab[i] : 0.0;
         }
+    if (SMEM_U && p.uthr != nullptr)
+        for (int i = threadIdx.x; i < uthr_smem_entries(LT); i += GEN_THREADS) sU[i] = p.uthr[i];
     __syncthreads();
 
     const Geometry& G = p.c.geo;
     const int L = G.levels;
     const int nquads = (G.W + 3) >> 2;
-    const int qd = blockIdx.x * blockDim.x + threadIdx.x;
+    const int qd = blockIdx.x * GEN_THREADS + threadIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int chain = blockIdx.z;
     const bool active = qd < nquads;
     if (__ballot_sync(FULL, active) == 0) return;  // warp-uniform exit
+    const int rbeg = p.c.rlo + blockIdx.y * R;
+    const int rend = min(rbeg + R, p.c.rhi);
+    if (rbeg >= rend) return;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const unsigned lt = (1u << lane) - 1u;
     SiteJob* jobs = s_jobs[warp];
     uint8_t* res = s_res[warp];
+    const bool use_u = p.uthr != nullptr;
+    const uint32_t* U = SMEM_U ? sU : p.uthr;
+    const int c0 = 4 * qd;
+    const int nvalid = active ? min(4, G.W - c0) : 0;
+    const uint8_t* xcol = p.c.x_in + chain * G.xchain + XOFF + c0;
+    const uint8_t* gcol = p.c.g + chain * G.gchain + XOFF + c0;
 
-    for (int r = p.c.rlo + blockIdx.y; r < p.c.rhi; r += gridDim.y) {
+    // rolling 3-row window of the words left of / at / right of the quad
+    uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0};
+    auto load_row = [&](int r, uint32_t (&w)[3]) {
+        if (!active) return;
+        const uint8_t* xr = xcol + (long long)(r + HALO) * G.xpitch;
+        w[0] = ldg4(xr - 4);
+        w[1] = ldg4(xr);
+        w[2] = ldg4(xr + 4);
+    };
+    load_row(rbeg - 1, up);
+    load_row(rbeg, mid);
+
+    for (int r = rbeg; r < rend; ++r) {
+        load_row(r + 1, dn);
         const int grow = G.row0 + r;
-        const int c0 = 4 * qd;
-        const int nvalid = active ? min(4, G.W - c0) : 0;
-        uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0}, gword = 0;
+        uint32_t gword = 0;
         uint4 rnd = make_uint4(0, 0, 0, 0);
         if (active) {
-            const uint8_t* xr = p.c.x_in + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                up[j] = ldg4(xr - G.xpitch + 4 * (j - 1));
-                mid[j] = ldg4(xr + 4 * (j - 1));
-                dn[j] = ldg4(xr + G.xpitch + 4 * (j - 1));
-            }
-            gword = ldg4(p.c.g + chain * G.gchain + (long long)(r + GHALO) * G.gpitch + XOFF + c0);
+            gword = ldg4(gcol + (long long)(r + GHALO) * G.gpitch);
             rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
         }
+        // the neighbours of the 4 sites, one byte per site (byte b = neighbour of site b)
+        const uint32_t UL = from_left(up[0], up[1]), UC = up[1], UR = from_right(up[1], up[2]);
+        const uint32_t ML = from_left(mid[0], mid[1]), MR = from_right(mid[1], mid[2]);
+        const uint32_t DL = from_left(dn[0], dn[1]), DC = dn[1], DR = from_right(dn[1], dn[2]);
+        // uniform neighbourhood: all NB neighbour bytes equal (chain of XORs), SWAR zero test
+        uint32_t D;
+        if (NB == 8)
+            D = (UL ^ UC) | (UC ^ UR) | (UR ^ ML) | (ML ^ MR) | (MR ^ DL) | (DL ^ DC) | (DC ^ DR);
+        else
+            D = (UC ^ ML) | (ML ^ MR) | (MR ^ DC);
+        const uint32_t differ = (((D & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | D) & 0x80808080u;
+        const uint32_t S0 = NB == 8 ? UL : UC;  // s* when uniform
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+        const uint32_t xw = mid[1];
         uint32_t outw = 0u;
         int qpos[4];
         int qbase = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int pos = 4 + b;  // window position of this site
-            int nb[NB];
-            if (NB == 8) {
-                nb[0] = win_byte(up, pos - 1); nb[1] = win_byte(up, pos); nb[2] = win_byte(up, pos + 1);
-                nb[3] = win_byte(mid, pos - 1); nb[4] = win_byte(mid, pos + 1);
-                nb[5] = win_byte(dn, pos - 1); nb[6] = win_byte(dn, pos); nb[7] = win_byte(dn, pos + 1);
-            } else {
-                nb[0] = win_byte(up, pos); nb[1] = win_byte(mid, pos - 1);
-                nb[2] = win_byte(mid, pos + 1); nb[3] = win_byte(dn, pos);
-            }
-            const int xi = win_byte(mid, pos);
+            const int xi = (int)((xw >> (8 * b)) & 0xFFu);
             const int gi = (int)((gword >> (8 * b)) & 0xFFu);
+            const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
             const bool valid = b < nvalid;
-            bool uniform = p.uthr != nullptr && xi < L && nb[0] < L;
-#pragma unroll
-            for (int j = 1; j < NB; ++j) uniform = uniform && nb[j] == nb[0];
-            const bool need = valid && !uniform;
+            const bool uniform = use_u && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
             if (valid && uniform) {
-                // every neighbour carries s* = nb[0] (so all NB exist): integer thresholds
-                const uint32_t* T = p.uthr + (size_t)((nb[0] * L + gi) * L + xi) * (L - 1);
+                // every neighbour carries s* = s0 (so all NB exist): integer thresholds
+                const uint32_t* T = U + (size_t)((s0 * L + gi) * L + xi) * (L - 1);
                 int w = 0;
-                for (int k = 0; k < L - 1; ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
+                if (LT > 0) {
+#pragma unroll
+                    for (int k = 0; k < (LT > 0 ? LT - 1 : 1); ++k) w += (rr[b] > (SMEM_U ? T[k] : __ldg(T + k))) ? 1 : 0;
+                } else {
+                    for (int k = 0; k < L - 1; ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
+                }
                 outw |= (uint32_t)w << (8 * b);
             }
             // compact the fp64 sites of the warp into its queue
+            const bool need = valid && !uniform;
             const unsigned m = __ballot_sync(FULL, need);
             qpos[b] = qbase + __popc(m & lt);
             if (need) {
+                const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);  // byte b of a, of b
                 SiteJob jb;
-                jb.nb_lo = jb.nb_hi = 0u;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) {
-                    if (q < 4) jb.nb_lo |= (uint32_t)nb[q] << (8 * q);
-                    else jb.nb_hi |= (uint32_t)nb[q] << (8 * (q - 4));
+                if (NB == 8) {
+                    jb.nb_lo = __byte_perm(__byte_perm(UL, UC, sel), __byte_perm(UR, ML, sel), 0x5410);
+                    jb.nb_hi = __byte_perm(__byte_perm(MR, DL, sel), __byte_perm(DC, DR, sel), 0x5410);
+                } else {
+                    jb.nb_lo = __byte_perm(__byte_perm(UC, ML, sel), __byte_perm(MR, DC, sel), 0x5410);
+                    jb.nb_hi = 0u;
                 }
                 jb.xg = (uint32_t)xi | ((uint32_t)gi << 8);
                 jb.r = rr[b];
@@ -252,73 +282,131 @@ __global__ void __launch_bounds__(GEN_THREADS, 2)
             }
             qbase += __popc(m);
         }
-        __syncwarp();
-        for (int i = lane; i < qbase; i += 32) {
-            int w = -1;
-            if (LT > 0) w = decide_fp64_fixed<NB, (LT > 0 ? LT : 2)>(p, sA, sD, sI, jobs[i]);
-            if (w < 0) w = decide_fp64<NB>(p, sA, jobs[i]);
-            res[i] = (uint8_t)w;
-        }
-        __syncwarp();
+        if (qbase > 0) {  // warp-uniform
+            __syncwarp();
+            for (int i = lane; i < qbase; i += 32) {
+                int w = -1;
+                if (LT > 0) w = decide_fp64_fixed<NB, (LT > 0 ? LT : 2)>(p, sA, sD, sI, jobs[i]);
+                if (w < 0) w = decide_fp64<NB>(p, sA, jobs[i]);
+                res[i] = (uint8_t)w;
+            }
+            __syncwarp();
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if (qpos[b] >= 0) outw |= (uint32_t)res[qpos[b]] << (8 * b);
-        __syncwarp();
-        if (!active) continue;
-
-        uint8_t* op = p.c.x_out + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
-        auto store = [&](uint8_t* dst) {
-            if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
-            else for (int b = 0; b < nvalid; ++b) dst[b] = (uint8_t)(outw >> (8 * b));
-            if (G.periodic) {  // column pads (see kernels.cuh)
-                if ((G.W & 15) == 0) {
-                    if (c0 < 16) *reinterpret_cast<uint32_t*>(dst + G.W) = outw;
-                    if (c0 >= G.W - 16) *reinterpret_cast<uint32_t*>(dst - G.W) = outw;
+            for (int b = 0; b < 4; ++b)
+                if (qpos[b] >= 0) outw |= (uint32_t)res[qpos[b]] << (8 * b);
+            __syncwarp();
+        }
+        if (active) {
+            uint8_t* op = p.c.x_out + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
+            auto store = [&](uint8_t* dst) {
+                if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
+                else for (int b = 0; b < nvalid; ++b) dst[b] = (uint8_t)(outw >> (8 * b));
+                if (G.periodic) {  // column pads (see kernels.cuh)
+                    if ((G.W & 15) == 0) {
+                        if (c0 < 16) *reinterpret_cast<uint32_t*>(dst + G.W) = outw;
+                        if (c0 >= G.W - 16) *reinterpret_cast<uint32_t*>(dst - G.W) = outw;
+                    } else {
+                        if (c0 == 0) dst[G.W] = (uint8_t)outw;
+                        if (c0 + nvalid == G.W) dst[-c0 - 1] = (uint8_t)(outw >> (8 * (nvalid - 1)));
+                    }
+                }
+            };
+            store(op);
+            if (G.periodic && G.self_halo_rows) {
+                if (r < HALO) store(op + (long long)G.rows * G.xpitch);
+                if (r >= G.rows - HALO) store(op - (long long)G.rows * G.xpitch);
+            }
+            if (p.c.count_enable) {
+                uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
+                if (nvalid == 4) {
+                    // the quad's 4 counters of a plane form one 8-byte word; each distinct label
+                    // of the quad adds its per-site increments with one fire-and-forget 64-bit
+                    // reduction (no lane carries: counts stay <= 65535), so the count update
+                    // costs no load latency
+                    if (L == 2) {
+                        const unsigned long long inc =
+                            (unsigned long long)__byte_perm(outw, 0u, 0x4140) |
+                            ((unsigned long long)__byte_perm(outw, 0u, 0x4342) << 32);
+                        if (inc) atomicAdd(reinterpret_cast<unsigned long long*>(cp), inc);
+                    } else {
+                        unsigned todo = 0xFu;
+                        while (todo) {
+                            const int b0 = __ffs(todo) - 1;
+                            const uint32_t k = (outw >> (8 * b0)) & 0xFFu;
+                            // bytes equal to k -> 0x01 per byte
+                            const uint32_t e = outw ^ (k * 0x01010101u);
+                            const uint32_t nz = (((e & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | e) & 0x80808080u;
+                            const uint32_t eq = (~nz >> 7) & 0x01010101u;
+                            const unsigned long long inc =
+                                (unsigned long long)__byte_perm(eq, 0u, 0x4140) |
+                                ((unsigned long long)__byte_perm(eq, 0u, 0x4342) << 32);
+                            atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)k * G.cplane), inc);
+                            todo &= ~(unsigned)(((eq & 1u) ? 1u : 0u) | ((eq & 0x100u) ? 2u : 0u) |
+                                                ((eq & 0x10000u) ? 4u : 0u) | ((eq & 0x1000000u) ? 8u : 0u));
+                        }
+                    }
                 } else {
-                    if (c0 == 0) dst[G.W] = (uint8_t)outw;
-                    if (c0 + nvalid == G.W) dst[-c0 - 1] = (uint8_t)(outw >> (8 * (nvalid - 1)));
+                    for (int b = 0; b < nvalid; ++b) {
+                        const int w = (int)((outw >> (8 * b)) & 0xFFu);
+                        if (L == 2) cp[b] += (uint16_t)w;
+                        else cp[(long long)w * G.cplane + b] += 1;
+                    }
                 }
             }
-        };
-        store(op);
-        if (G.periodic && G.self_halo_rows) {
-            if (r < HALO) store(op + (long long)G.rows * G.xpitch);
-            if (r >= G.rows - HALO) store(op - (long long)G.rows * G.xpitch);
         }
-        if (p.c.count_enable) {
-            uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
-            for (int b = 0; b < nvalid; ++b) {
-                const int w = (int)((outw >> (8 * b)) & 0xFFu);
-                if (L == 2) cp[b] += (uint16_t)w;
-                else cp[(long long)w * G.cplane + b] += 1;
-            }
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            up[j] = mid[j];
+            mid[j] = dn[j];
         }
     }
+}
+
+template <int NB, int LT>
+int launch_g(const GeneralSweepParams& p, int batch, cudaStream_t s) {
+    static int occ = 0, sms = 0;
+    if (occ == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_general_kernel<NB, LT>, GEN_THREADS, 0);
+        if (occ < 1) occ = 1;
+    }
+    const Geometry& G = p.c.geo;
+    const int nquads = (G.W + 3) / 4;
+    const int nr = p.c.rhi - p.c.rlo;
+    if (nr <= 0) return 0;
+    const long long xblocks = (nquads + GEN_THREADS - 1) / GEN_THREADS;
+    // rows per block: about four waves of blocks (the fp64 share of a row varies, so several
+    // waves balance the tail), each block walking a run of rows with a rolling window
+    const long long target = 4LL * sms * occ;
+    long long R = ((long long)nr * xblocks * batch + target - 1) / target;
+    if (R < 1) R = 1;
+    long long nrb = (nr + R - 1) / R;
+    if (nrb > 65535) {
+        nrb = 65535;
+        R = (nr + nrb - 1) / nrb;
+    }
+    dim3 grid((unsigned)xblocks, (unsigned)nrb, batch);
+    sweep_general_kernel<NB, LT><<<grid, GEN_THREADS, 0, s>>>(p, (int)R);
+    return (int)cudaGetLastError();
 }
 
 }  // namespace
 
 int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream) {
     const Geometry& G = p.c.geo;
-    const int nquads = (G.W + 3) / 4;
-    const int nr = p.c.rhi - p.c.rlo;
-    if (nr <= 0) return 0;
-    dim3 grid((nquads + GEN_THREADS - 1) / GEN_THREADS, nr < 65535 ? nr : 65535, batch);
     cudaStream_t s = (cudaStream_t)stream;
-#define PCA_GEN_LAUNCH(LTV)                                                              \
-    do {                                                                                 \
-        if (G.nbhd == 8) sweep_general_kernel<8, LTV><<<grid, GEN_THREADS, 0, s>>>(p);   \
-        else sweep_general_kernel<4, LTV><<<grid, GEN_THREADS, 0, s>>>(p);               \
-    } while (0)
+#define PCA_GEN_LAUNCH(LTV) \
+    return G.nbhd == 8 ? launch_g<8, LTV>(p, batch, s) : launch_g<4, LTV>(p, batch, s)
     switch (G.levels) {  // the paper's level counts (and 3) get fully unrolled fp64 paths
-        case 3: PCA_GEN_LAUNCH(3); break;
-        case 5: PCA_GEN_LAUNCH(5); break;
-        case 9: PCA_GEN_LAUNCH(9); break;
-        case 16: PCA_GEN_LAUNCH(16); break;
-        default: PCA_GEN_LAUNCH(0); break;
+        case 3: PCA_GEN_LAUNCH(3);
+        case 5: PCA_GEN_LAUNCH(5);
+        case 9: PCA_GEN_LAUNCH(9);
+        case 16: PCA_GEN_LAUNCH(16);
+        default: PCA_GEN_LAUNCH(0);
     }
 #undef PCA_GEN_LAUNCH
-    return (int)cudaGetLastError();
 }
 
 }  // namespace pcab200
