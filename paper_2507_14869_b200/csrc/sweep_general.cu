@@ -212,18 +212,26 @@ __global__ void __launch_bounds__(GEN_THREADS, 4)
         w[1] = ldg4(xr);
         w[2] = ldg4(xr + 4);
     };
+    // software pipeline: the x row r+2 and the g row r+1 are loaded one iteration ahead, so
+    // the load latency overlaps a row of work (rows rbeg-1 .. rend+1 exist: HALO = 2)
+    uint32_t nxt[3] = {0, 0, 0}, gnext = 0;
     load_row(rbeg - 1, up);
     load_row(rbeg, mid);
+    load_row(rbeg + 1, nxt);
+    if (active) gnext = ldg4(gcol + (long long)(rbeg + GHALO) * G.gpitch);
 
     for (int r = rbeg; r < rend; ++r) {
-        load_row(r + 1, dn);
-        const int grow = G.row0 + r;
-        uint32_t gword = 0;
-        uint4 rnd = make_uint4(0, 0, 0, 0);
-        if (active) {
-            gword = ldg4(gcol + (long long)(r + GHALO) * G.gpitch);
-            rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) dn[j] = nxt[j];
+        const uint32_t gword = gnext;
+        if (r + 1 < rend) {
+            load_row(r + 2, nxt);
+            if (active) gnext = ldg4(gcol + (long long)(r + 1 + GHALO) * G.gpitch);
         }
+        const int grow = G.row0 + r;
+        uint4 rnd = make_uint4(0, 0, 0, 0);
+        if (active)
+            rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
         // the neighbours of the 4 sites, one byte per site (byte b = neighbour of site b)
         const uint32_t UL = from_left(up[0], up[1]), UC = up[1], UR = from_right(up[1], up[2]);
         const uint32_t ML = from_left(mid[0], mid[1]), MR = from_right(mid[1], mid[2]);
