@@ -12,28 +12,29 @@
 // g_i) -- exact; levels > 2: the uniform-neighbourhood threshold table (levels <= 16) or
 // fp64 weights, as in sweep_general.cu.
 //
-// Thread = 4 consecutive sites of a row (one Philox call).  Moore-8 launches cover only the
-// rows of the colour's parity.  A thread rewrites its whole 4-byte word: the bytes of other
-// colours are rewritten with the values it read, which no thread of this launch changes, so
-// concurrent readers see the same neighbour labels either way.  MPM counts are taken in the
-// launch after which a row is final (colours 1 and 3).
+// Thread = 4 consecutive sites of a row (one Philox call), walking a run of rows with a
+// rolling window (as sweep_general.cu).  Moore-8 launches cover only the rows of the
+// colour's parity.  levels == 2 uses SWAR byte sums for the label-1 and present neighbours
+// of the 4 sites and one table lookup per site.  A thread rewrites its whole 4-byte word:
+// the bytes of other colours are rewritten with the values it read, which no thread of this
+// launch changes, so concurrent readers see the same neighbour labels either way.  MPM counts
+// are taken in the launch after which a row is final (colours 1 and 3), with fire-and-forget
+// 64-bit reductions.
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#include "tma_ring.cuh"  // from_left / from_right byte funnels
 
 namespace pcab200 {
 namespace {
 
-constexpr int GB_THREADS = 256;
+constexpr int GB_THREADS = 128;
 constexpr int GB_WARPS = GB_THREADS / 32;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
 // plain (coherent) loads: the buffer is written by this same launch, so not the read-only path
 __device__ __forceinline__ uint32_t ld4(const uint8_t* p) {
     return *reinterpret_cast<const uint32_t*>(p);
-}
-__device__ __forceinline__ int win_byte(const uint32_t (&w)[3], int pos) {
-    return (int)((w[pos >> 2] >> (8 * (pos & 3))) & 0xFFu);
 }
 
 struct GibbsJob {
@@ -102,7 +103,7 @@ __device__ int gibbs_fp64(const GibbsSweepParams& p, const double* sA, const Gib
 }
 
 template <int NB, bool BIN>
-__global__ void __launch_bounds__(GB_THREADS, 2) sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p) {
+__global__ void __launch_bounds__(GB_THREADS, 4) sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
     __shared__ double sA[9];
     __shared__ uint32_t sT[BIN ? GIBBS_THR2 : 1];
     __shared__ GibbsJob s_jobs[GB_WARPS][64];
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(GB_THREADS, 2) sweep_gibbs_kernel(const __grid
     const int L = G.levels;
     const int k = p.colour;
     const int nquads = (G.W + 3) >> 2;
-    const int qd = blockIdx.x * blockDim.x + threadIdx.x;
+    const int qd = blockIdx.x * GB_THREADS + threadIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int chain = blockIdx.z;
     const bool active = qd < nquads;
@@ -125,148 +126,228 @@ __global__ void __launch_bounds__(GB_THREADS, 2) sweep_gibbs_kernel(const __grid
     const unsigned lt = (1u << lane) - 1u;
     GibbsJob* jobs = s_jobs[warp];
     uint8_t* res = s_res[warp];
-    // Moore-8: only rows whose global parity is k >> 1 hold colour k
+    // rows of this block: Moore-8 visits only rows whose global parity is k >> 1
     const int rstep = NB == 8 ? 2 : 1;
     int rfirst = p.c.rlo;
     if (NB == 8 && ((G.row0 + rfirst) & 1) != (k >> 1)) ++rfirst;
+    const int rbeg = rfirst + rstep * R * (int)blockIdx.y;
+    const int rend = min(rbeg + rstep * R, p.c.rhi);
+    if (rbeg >= rend) return;
+    const int c0 = 4 * qd;
+    const int nvalid = active ? min(4, G.W - c0) : 0;
+    uint8_t* xcol = p.c.x_out + chain * G.xchain + XOFF + c0;
+    const uint8_t* gcol = p.c.g + chain * G.gchain + XOFF + c0;
+    auto load_row = [&](int r, uint32_t (&w)[3]) {
+        if (!active) return;
+        const uint8_t* xr = xcol + (long long)(r + HALO) * G.xpitch;
+        w[0] = ld4(xr - 4);
+        w[1] = ld4(xr);
+        w[2] = ld4(xr + 4);
+    };
+    // rolling window; the rows a launch reads around its rows never change in the launch
+    // (4-neighbour: only the other colour's bytes are used; Moore-8: the other row parity)
+    uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0};
+    load_row(rbeg - 1, up);
+    load_row(rbeg, mid);
+    load_row(rbeg + 1, dn);
 
-    for (int r = rfirst + rstep * (int)blockIdx.y; r < p.c.rhi; r += rstep * (int)gridDim.y) {
+    for (int r = rbeg; r < rend; r += rstep) {
         const int grow = G.row0 + r;
-        const int c0 = 4 * qd;
-        const int nvalid = active ? min(4, G.W - c0) : 0;
-        uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0}, gword = 0;
+        uint32_t gword = 0;
         uint4 rnd = make_uint4(0, 0, 0, 0);
-        uint8_t* xr = p.c.x_out + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
         if (active) {
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                up[j] = ld4(xr - G.xpitch + 4 * (j - 1));
-                mid[j] = ld4(xr + 4 * (j - 1));
-                dn[j] = ld4(xr + G.xpitch + 4 * (j - 1));
-            }
-            gword = __ldg(reinterpret_cast<const uint32_t*>(
-                p.c.g + chain * G.gchain + (long long)(r + GHALO) * G.gpitch + XOFF + c0));
+            gword = __ldg(reinterpret_cast<const uint32_t*>(gcol + (long long)(r + GHALO) * G.gpitch));
             rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
         }
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+        const uint32_t UL = from_left(up[0], up[1]), UC = up[1], UR = from_right(up[1], up[2]);
+        const uint32_t ML = from_left(mid[0], mid[1]), MR = from_right(mid[1], mid[2]);
+        const uint32_t DL = from_left(dn[0], dn[1]), DC = dn[1], DR = from_right(dn[1], dn[2]);
+        // sites of colour k in this quad (c0 is a multiple of 4)
+        unsigned mine = NB == 4 ? (((grow + k) & 1) ? 0xAu : 0x5u) : ((k & 1) ? 0xAu : 0x5u);
+        if (nvalid < 4) mine &= (1u << nvalid) - 1u;
         uint32_t outw = mid[1];  // start from the current labels of the 4 sites
-        int qpos[4];
+        int qpos[4] = {-1, -1, -1, -1};
         int qbase = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int pos = 4 + b;
-            const int col = c0 + b;
-            const int colour = NB == 4 ? ((grow + col) & 1) : (((grow & 1) << 1) | (col & 1));
-            const bool mine = b < nvalid && colour == k;
-            int nb[NB];
+        if (BIN) {
+            // SWAR over the 4 sites: label-1 neighbours and present neighbours per byte
+            auto one = [](uint32_t w) { return w & ~(w >> 1) & 0x01010101u; };  // 0xFF -> 0
+            auto pres = [](uint32_t w) { return (~w >> 7) & 0x01010101u; };     // 0xFF -> 0
+            uint32_t n1, np;
             if (NB == 8) {
-                nb[0] = win_byte(up, pos - 1); nb[1] = win_byte(up, pos); nb[2] = win_byte(up, pos + 1);
-                nb[3] = win_byte(mid, pos - 1); nb[4] = win_byte(mid, pos + 1);
-                nb[5] = win_byte(dn, pos - 1); nb[6] = win_byte(dn, pos); nb[7] = win_byte(dn, pos + 1);
+                n1 = one(UL) + one(UC) + one(UR) + one(ML) + one(MR) + one(DL) + one(DC) + one(DR);
+                np = G.periodic ? 0x08080808u
+                                : pres(UL) + pres(UC) + pres(UR) + pres(ML) + pres(MR) + pres(DL) + pres(DC) + pres(DR);
             } else {
-                nb[0] = win_byte(up, pos); nb[1] = win_byte(mid, pos - 1);
-                nb[2] = win_byte(mid, pos + 1); nb[3] = win_byte(dn, pos);
+                n1 = one(UC) + one(ML) + one(MR) + one(DC);
+                np = G.periodic ? 0x04040404u : pres(UC) + pres(ML) + pres(MR) + pres(DC);
             }
-            const int gi = (int)((gword >> (8 * b)) & 0xFFu);
-            bool need = false;
-            if (BIN) {
-                if (mine) {
-                    int np = 0, n1 = 0;
+            const uint32_t idx4 = ((np * 9u + n1) << 1) | gword;  // (np*9 + n1)*2 + g per byte
 #pragma unroll
-                    for (int q = 0; q < NB; ++q) {
-                        np += nb[q] != 0xFF;
-                        n1 += nb[q] == 1;
-                    }
-                    const int w = rr[b] > sT[(np * 9 + n1) * 2 + gi] ? 1 : 0;
-                    outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)w << (8 * b));
+            for (int b = 0; b < 4; ++b) {
+                if ((mine >> b) & 1u) {
+                    const uint32_t w = rr[b] > sT[(idx4 >> (8 * b)) & 0xFFu] ? 1u : 0u;
+                    outw = (outw & ~(0xFFu << (8 * b))) | (w << (8 * b));
                 }
-            } else {
-                bool uniform = p.uthr != nullptr && nb[0] < L;
+            }
+        } else {
+            uint32_t D;
+            if (NB == 8)
+                D = (UL ^ UC) | (UC ^ UR) | (UR ^ ML) | (ML ^ MR) | (MR ^ DL) | (DL ^ DC) | (DC ^ DR);
+            else
+                D = (UC ^ ML) | (ML ^ MR) | (MR ^ DC);
+            const uint32_t differ = (((D & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | D) & 0x80808080u;
+            const uint32_t S0 = NB == 8 ? UL : UC;
 #pragma unroll
-                for (int j = 1; j < NB; ++j) uniform = uniform && nb[j] == nb[0];
-                if (mine && uniform) {
-                    const uint32_t* T = p.uthr + (size_t)(nb[0] * L + gi) * (L - 1);
+            for (int b = 0; b < 4; ++b) {
+                const bool my = (mine >> b) & 1u;
+                const int gi = (int)((gword >> (8 * b)) & 0xFFu);
+                const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
+                const bool uniform = p.uthr != nullptr && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
+                if (my && uniform) {
+                    const uint32_t* T = p.uthr + (size_t)(s0 * L + gi) * (L - 1);
                     int w = 0;
                     for (int kk = 0; kk < L - 1; ++kk) w += (rr[b] > __ldg(T + kk)) ? 1 : 0;
                     outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)w << (8 * b));
                 }
-                need = mine && !uniform;
-            }
-            const unsigned m = __ballot_sync(FULL, need);
-            qpos[b] = need ? qbase + __popc(m & lt) : -1;
-            if (need) {
-                GibbsJob jb;
-                jb.nb_lo = jb.nb_hi = 0u;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) {
-                    if (q < 4) jb.nb_lo |= (uint32_t)nb[q] << (8 * q);
-                    else jb.nb_hi |= (uint32_t)nb[q] << (8 * (q - 4));
+                const bool need = my && !uniform;
+                const unsigned m = __ballot_sync(FULL, need);
+                if (need) {
+                    qpos[b] = qbase + __popc(m & lt);
+                    const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);
+                    GibbsJob jb;
+                    if (NB == 8) {
+                        jb.nb_lo = __byte_perm(__byte_perm(UL, UC, sel), __byte_perm(UR, ML, sel), 0x5410);
+                        jb.nb_hi = __byte_perm(__byte_perm(MR, DL, sel), __byte_perm(DC, DR, sel), 0x5410);
+                    } else {
+                        jb.nb_lo = __byte_perm(__byte_perm(UC, ML, sel), __byte_perm(MR, DC, sel), 0x5410);
+                        jb.nb_hi = 0u;
+                    }
+                    jb.g = (uint32_t)gi;
+                    jb.r = rr[b];
+                    jobs[qpos[b]] = jb;
                 }
-                jb.g = (uint32_t)gi;
-                jb.r = rr[b];
-                jobs[qpos[b]] = jb;
+                qbase += __popc(m);
             }
-            qbase += __popc(m);
-        }
-        if (!BIN) {
-            __syncwarp();
-            for (int i = lane; i < qbase; i += 32) res[i] = (uint8_t)gibbs_fp64<NB>(p, sA, jobs[i]);
-            __syncwarp();
+            if (qbase > 0) {
+                __syncwarp();
+                for (int i = lane; i < qbase; i += 32) res[i] = (uint8_t)gibbs_fp64<NB>(p, sA, jobs[i]);
+                __syncwarp();
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (qpos[b] >= 0) outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)res[qpos[b]] << (8 * b));
-            __syncwarp();
+                for (int b = 0; b < 4; ++b)
+                    if (qpos[b] >= 0) outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)res[qpos[b]] << (8 * b));
+                __syncwarp();
+            }
         }
-        if (!active) continue;
-
-        auto store = [&](uint8_t* dst) {
-            if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
-            else for (int b = 0; b < nvalid; ++b) dst[b] = (uint8_t)(outw >> (8 * b));
-            if (G.periodic) {  // column pads (W even on a torus)
-                if ((G.W & 15) == 0) {
-                    if (c0 < 16) *reinterpret_cast<uint32_t*>(dst + G.W) = outw;
-                    if (c0 >= G.W - 16) *reinterpret_cast<uint32_t*>(dst - G.W) = outw;
+        if (active) {
+            uint8_t* xr = xcol + (long long)(r + HALO) * G.xpitch;
+            auto store = [&](uint8_t* dst) {
+                if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
+                else for (int b = 0; b < nvalid; ++b) dst[b] = (uint8_t)(outw >> (8 * b));
+                if (G.periodic) {  // column pads (W even on a torus)
+                    if ((G.W & 15) == 0) {
+                        if (c0 < 16) *reinterpret_cast<uint32_t*>(dst + G.W) = outw;
+                        if (c0 >= G.W - 16) *reinterpret_cast<uint32_t*>(dst - G.W) = outw;
+                    } else {
+                        if (c0 == 0) dst[G.W] = (uint8_t)outw;
+                        if (c0 + nvalid == G.W) dst[-c0 - 1] = (uint8_t)(outw >> (8 * (nvalid - 1)));
+                    }
+                }
+            };
+            store(xr);
+            if (G.periodic && G.self_halo_rows) {
+                if (r < HALO) store(xr + (long long)G.rows * G.xpitch);
+                if (r >= G.rows - HALO) store(xr - (long long)G.rows * G.xpitch);
+            }
+            if (p.c.count_enable) {  // the row is final after this colour (1 or 3)
+                uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
+                if (nvalid == 4) {
+                    if (L == 2) {
+                        const unsigned long long inc =
+                            (unsigned long long)__byte_perm(outw, 0u, 0x4140) |
+                            ((unsigned long long)__byte_perm(outw, 0u, 0x4342) << 32);
+                        if (inc) atomicAdd(reinterpret_cast<unsigned long long*>(cp), inc);
+                    } else {
+                        unsigned todo = 0xFu;
+                        while (todo) {
+                            const int b0 = __ffs(todo) - 1;
+                            const uint32_t kk = (outw >> (8 * b0)) & 0xFFu;
+                            const uint32_t e = outw ^ (kk * 0x01010101u);
+                            const uint32_t nz = (((e & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | e) & 0x80808080u;
+                            const uint32_t eq = (~nz >> 7) & 0x01010101u;
+                            const unsigned long long inc =
+                                (unsigned long long)__byte_perm(eq, 0u, 0x4140) |
+                                ((unsigned long long)__byte_perm(eq, 0u, 0x4342) << 32);
+                            atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)kk * G.cplane), inc);
+                            todo &= ~(unsigned)(((eq & 1u) ? 1u : 0u) | ((eq & 0x100u) ? 2u : 0u) |
+                                                ((eq & 0x10000u) ? 4u : 0u) | ((eq & 0x1000000u) ? 8u : 0u));
+                        }
+                    }
                 } else {
-                    if (c0 == 0) dst[G.W] = (uint8_t)outw;
-                    if (c0 + nvalid == G.W) dst[-c0 - 1] = (uint8_t)(outw >> (8 * (nvalid - 1)));
+                    for (int b = 0; b < nvalid; ++b) {
+                        const int w = (int)((outw >> (8 * b)) & 0xFFu);
+                        if (L == 2) cp[b] += (uint16_t)w;
+                        else cp[(long long)w * G.cplane + b] += 1;
+                    }
                 }
             }
-        };
-        store(xr);
-        if (G.periodic && G.self_halo_rows) {
-            if (r < HALO) store(xr + (long long)G.rows * G.xpitch);
-            if (r >= G.rows - HALO) store(xr - (long long)G.rows * G.xpitch);
         }
-        if (p.c.count_enable) {
-            uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
-            for (int b = 0; b < nvalid; ++b) {
-                const int w = (int)((outw >> (8 * b)) & 0xFFu);
-                if (L == 2) cp[b] += (uint16_t)w;
-                else cp[(long long)w * G.cplane + b] += 1;
+        // slide the window by rstep rows
+        if (r + rstep < rend) {
+            if (NB == 8) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) up[j] = dn[j];
+                load_row(r + 2, mid);
+                load_row(r + 3, dn);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    up[j] = mid[j];
+                    mid[j] = dn[j];
+                }
+                load_row(r + 2, dn);
             }
         }
     }
+}
+
+template <int NB, bool BIN>
+int launch_gb(const GibbsSweepParams& p, int batch, cudaStream_t s) {
+    static int occ = 0, sms = 0;
+    if (occ == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_gibbs_kernel<NB, BIN>, GB_THREADS, 0);
+        if (occ < 1) occ = 1;
+    }
+    const Geometry& G = p.c.geo;
+    const int nquads = (G.W + 3) / 4;
+    int nr = p.c.rhi - p.c.rlo;
+    if (G.nbhd == 8) nr = (nr + 1) / 2;  // rows of one parity
+    if (nr <= 0) return 0;
+    const long long xblocks = (nquads + GB_THREADS - 1) / GB_THREADS;
+    const long long target = 4LL * sms * occ;
+    long long R = ((long long)nr * xblocks * batch + target - 1) / target;
+    if (R < 1) R = 1;
+    long long nrb = (nr + R - 1) / R;
+    if (nrb > 65535) {
+        nrb = 65535;
+        R = (nr + nrb - 1) / nrb;
+    }
+    dim3 grid((unsigned)xblocks, (unsigned)nrb, batch);
+    sweep_gibbs_kernel<NB, BIN><<<grid, GB_THREADS, 0, s>>>(p, (int)R);
+    return (int)cudaGetLastError();
 }
 
 }  // namespace
 
 int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream) {
     const Geometry& G = p.c.geo;
-    const int nquads = (G.W + 3) / 4;
-    int nr = p.c.rhi - p.c.rlo;
-    if (G.nbhd == 8) nr = (nr + 1) / 2;
-    if (nr <= 0) return 0;
-    dim3 grid((nquads + GB_THREADS - 1) / GB_THREADS, nr < 65535 ? nr : 65535, batch);
     cudaStream_t s = (cudaStream_t)stream;
     const bool bin = G.levels == 2;
-    if (G.nbhd == 8) {
-        if (bin) sweep_gibbs_kernel<8, true><<<grid, GB_THREADS, 0, s>>>(p);
-        else sweep_gibbs_kernel<8, false><<<grid, GB_THREADS, 0, s>>>(p);
-    } else {
-        if (bin) sweep_gibbs_kernel<4, true><<<grid, GB_THREADS, 0, s>>>(p);
-        else sweep_gibbs_kernel<4, false><<<grid, GB_THREADS, 0, s>>>(p);
-    }
-    return (int)cudaGetLastError();
+    if (G.nbhd == 8) return bin ? launch_gb<8, true>(p, batch, s) : launch_gb<8, false>(p, batch, s);
+    return bin ? launch_gb<4, true>(p, batch, s) : launch_gb<4, false>(p, batch, s);
 }
 
 }  // namespace pcab200
