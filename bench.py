@@ -321,6 +321,29 @@ def run_ours(args):
                "ms_per_step": ems / args.steps}
 
     clk = clocks.stop()
+
+    # ---- exposed halo exchange (N > 1): the same strip swept as an isolated torus of
+    # rows x W (identical kernels, no NCCL) vs the sharded sweeps timed above ----
+    halo = None
+    if world > 1:
+        local = P.PcaContext(P.make_config(rows, W, wl["levels"], **kw), g_dev, stream=stream)
+        local.pca_sweep(S)
+        barrier()
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        for _ in range(args.steps):
+            local.pca_sweep(S)
+        l1.record(stream)
+        barrier()
+        local_us = max_over_ranks(l0.elapsed_time(l1)) * 1e3 / (S * args.steps)
+        local.pca_destroy()
+        halo = {"sweep_us_sharded": sweep_s * 1e6, "sweep_us_local_only": local_us,
+                "exposed_us_per_sweep": sweep_s * 1e6 - local_us,
+                "messages_per_sweep_per_rank": 4, "bytes_per_message": 16 * ((W + 15) // 16) + 32,  # one padded row (depth 1)
+                "method": "max over ranks of S sharded sweeps (edge rows + NCCL send/recv "
+                          "overlapping the interior) minus S sweeps of the same strip as an "
+                          "isolated torus (no exchange)"}
+
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_oracle(wl, truth, g, rows=wl["rows"], sweeps=2)
@@ -345,6 +368,7 @@ def run_ours(args):
                          "traffic_source": traffic_src},
             "gpu_launches": launches,
             "e2e": e2e,
+            "halo": halo,
             "clocks": clk,
             "cpu_baseline": cpu,
         }
