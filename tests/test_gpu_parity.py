@@ -362,25 +362,62 @@ def test_distribution_matches_exact_transition_powers(cuda_device):
     assert ok, (stat, crit)
 
 
-def test_full_size_sampled_rows(cuda_device):
-    """Bench configuration (config 3, 8192^2, l = 2, Moore-8 torus, MPM on): a few GPU sweeps,
-    then rows sampled across the lattice are recomputed by the oracle from the GPU's x_t."""
-    H = W = 8192
+@pytest.mark.parametrize("H,W,nb,per", [(8192, 8192, 8, True), (4096, 32768, 8, True),
+                                        (8192, 8192, 8, False), (8192, 8192, 4, True)],
+                         ids=["c3", "c4-strip-shape", "c3-free", "c3-vn4"])
+def test_full_size_sampled_rows(cuda_device, H, W, nb, per):
+    """Bench-size lattices (config 3, 8192^2, and config 4's per-GPU 4096 x 32768 shape, l = 2,
+    MPM on): rows sampled across the lattice (edges, middle, random) are recomputed by the
+    oracle from the GPU's x_t for the last sweep; the MPM counts must equal the sum of the
+    four states exactly at every site."""
     truth = synth.tiled_labels(H, W, 2, seed=1)
     g = synth.degrade(truth, 2, 0.5, seed=2)
-    cfg = P.make_config(H, W, 2, neighborhood=8, periodic=True, sigma=0.5, beta0=1.5,
+    cfg = P.make_config(H, W, 2, neighborhood=nb, periodic=per, sigma=0.5, beta0=1.5,
                         beta_step=0.0, seed=11, mpm_burn_in=0)
     ctx = make_ctx(cfg, g)
-    ctx.pca_sweep(3)
+    acc = np.zeros((H, W), np.uint16)
+    for _ in range(3):
+        ctx.pca_sweep(1)
+        acc += ctx.state()[0]
     x3 = ctx.state()[0]
     ctx.pca_sweep(1)
     x4 = ctx.state()[0]
+    acc += x4
     m = oracle_model(cfg)
-    rows = sorted({0, 1, H - 1, H // 2} | set(np.random.default_rng(0).integers(0, H, 24).tolist()))
+    rows = sorted({0, 1, H - 1, H // 2} | set(np.random.default_rng(0).integers(0, H, 16).tolist()))
     tally = Tally()
     for r in rows:
         ref, mg = orc.pca_sweep(m, x3, g, 1.5, cfg.seed, 0, 3, rows=(r, r + 1))
         tally.add(x4[r], ref[0], mg[0])
     tally.check()
-    c = ctx.counts()[0]
-    assert c.max() <= 4 and np.array_equal(c[rows[0]] >= 0, np.ones(W, bool))
+    assert np.array_equal(ctx.counts()[0], acc)
+
+
+def test_config5_batch_full_size_sampled_chains(cuda_device):
+    """Config 5 per GPU (128 chains of 512^2, l = 5, Moore-8, free, MPM on): whole chains
+    sampled across the batch are recomputed by the oracle for the last sweep, and their
+    planar counts equal the one-hot sums of the states."""
+    B, H, W, L = 128, 512, 512, 5
+    g = np.stack([synth.degrade(synth.smooth_labels(H, W, L, 7 + (b % 8)), L, 0.25, b) for b in range(B)])
+    cfg = P.make_config(H, W, L, batch=B, sigma=0.25, seed=2025, mpm_burn_in=0)
+    ctx = make_ctx(cfg, g)
+    picks = [0, 1, 63, 100, 127]
+    acc = np.zeros((len(picks), L, H, W), np.uint16)
+    for _ in range(3):
+        ctx.pca_sweep(1)
+        xs = ctx.state()
+        for i, b in enumerate(picks):
+            acc[i] += (np.arange(L)[:, None, None] == xs[b][None]).astype(np.uint16)
+    x3 = ctx.state()
+    ctx.pca_sweep(1)
+    x4 = ctx.state()
+    m = oracle_model(cfg)
+    tally = Tally()
+    for i, b in enumerate(picks):
+        ref, mg = orc.pca_sweep(m, x3[b], g[b], beta_of(cfg, 3), cfg.seed, b, 3)
+        tally.add(x4[b], ref, mg)
+        acc[i] += (np.arange(L)[:, None, None] == x4[b][None]).astype(np.uint16)
+    tally.check()
+    cnt = ctx.counts()
+    for i, b in enumerate(picks):
+        assert np.array_equal(cnt[b], acc[i])
