@@ -94,6 +94,7 @@ struct GeneralSweepParams {
     const double* itab;
     int inertia_p;
     const uint32_t* uthr;
+    const uint32_t* bthr;  // levels == 2: the binary thresholds [THR_ENTRIES] (exact path)
 };
 
 // Gibbs sampler, one colour class per launch, in place (x_in == x_out): sites of colour k
@@ -125,7 +126,9 @@ struct MetricParams {
 // ---- launchers (return cudaError_t as int) ----
 int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread,
                         void* stream);
-int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream);
+// nsweeps > 1: consecutive sweeps t .. t+nsweeps-1 (same tables and counting) in one
+// cooperative launch, x_in / x_out alternating; the result is in x_in when nsweeps is even.
+int launch_sweep_general(const GeneralSweepParams& p, int batch, int nsweeps, void* stream);
 int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream);
 // copy a small host table into device memory through the kernel parameter block (stream
 // ordered, no host synchronisation, no pinned staging buffer to protect)

@@ -10,9 +10,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -93,6 +95,16 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // uniform-neighbourhood integer threshold tables (multilevel kernel) up to 16 levels:
 // 16^3 * 15 entries = 240 KiB
 constexpr int UTHR_MAX_LEVELS = 16;
+// lattices up to this many sites (x batch) sweep in runs of one cooperative launch; the
+// environment variable PCA_B200_MULTI_MAX_SITES overrides it (a tuning knob: the chain is the
+// same either way)
+size_t multi_max_sites() {
+    static size_t v = [] {
+        const char* e = getenv("PCA_B200_MULTI_MAX_SITES");
+        return e ? (size_t)strtoull(e, nullptr, 10) : (size_t(1) << 18);
+    }();
+    return v;
+}
 
 // Workspace layout: byte offsets of every region.
 struct Layout {
@@ -339,7 +351,7 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
     const double a = c.coef_scale * 2.0 * beta * c.J;
     const double b = c.coef_scale / (2.0 * c.sigma * c.sigma);
     const double cq = beta * c.q;
-    if (ctx->kernel == PCA_KERNEL_BINARY) {
+    if (c.levels == 2) {  // binary thresholds: the binary kernel and the exact l = 2 general path
         for (int np = 0; np <= 8; ++np)
             for (int n1 = 0; n1 <= 8; ++n1)
                 for (int gl = 0; gl < 2; ++gl)
@@ -372,7 +384,8 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
         ParamTable pt;
         memcpy(pt.v, ctx->bthr_host, sizeof(ctx->bthr_host));
         LAUNCH(ctx, launch_param_table(pt, THR_ENTRIES, const_cast<uint32_t*>(ctx->bin.thr), ctx->stream));
-    } else {
+    }
+    {
         GeneralSweepParams& m = ctx->gen;
         for (int n = 0; n <= 8; ++n) m.A[n] = exp(a * (double)n);
         m.Cw = exp(-cq);
@@ -688,6 +701,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->gen.inertia_p = cfg->inertia_p;
     ctx->gen.uthr = ctx->uthr;
     ctx->bin.thr = (const uint32_t*)(ctx->ws + L.off_bthr);
+    ctx->gen.bthr = ctx->bin.thr;
     ctx->gib.dtab = ctx->dtab;
     ctx->gib.uthr = ctx->gthr;
 
@@ -726,9 +740,39 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     auto counts_at = [&](int64_t t) {
         return (ctx->cfg.mpm_burn_in >= 0 && t >= ctx->cfg.mpm_burn_in) ? 1 : 0;
     };
+    // small lattices: runs of sweeps in one cooperative launch (sweep_multi_kernel)
+    const bool small = !strip && !pairs &&
+                       (size_t)ctx->lay.rows * ctx->cfg.width * ctx->cfg.batch <= multi_max_sites();
     for (int32_t i = 0; i < n; ++i) {
         const int64_t t = ctx->t;
         if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
+        if (small && n - i >= 2) {
+            // the run stays inside one beta stage and one counting mode
+            int64_t run = n - i;
+            const int64_t period = ctx->cfg.beta_period;
+            run = std::min<int64_t>(run, period - t % period);
+            if (ctx->cfg.mpm_burn_in >= 0 && t < ctx->cfg.mpm_burn_in)
+                run = std::min<int64_t>(run, ctx->cfg.mpm_burn_in - t);
+            run = std::min<int64_t>(run, (int64_t)0xFFFFFFFFLL - t);
+            const int count = counts_at(t);
+            if (count) run = std::min<int64_t>(run, 65535 - ctx->counted);
+            if (run >= 2) {
+                st = build_tables(ctx, t);
+                if (st != PCA_OK) return st;
+                fill_common(ctx, ctx->gen.c, t, count);
+                ctx->gen.c.rlo = 0;
+                ctx->gen.c.rhi = ctx->lay.rows;
+                ctx->launches++;
+                ctx->sweep_launches++;
+                const int e = launch_sweep_general(ctx->gen, ctx->cfg.batch, (int)run, ctx->stream);
+                if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (multi-sweep launch)");
+                ctx->cur ^= (int)(run & 1);
+                ctx->t = t + run;
+                ctx->counted += count * run;
+                i += (int32_t)run - 1;
+                continue;
+            }
+        }
         if (pairs && i + 1 < n && t + 1 < (int64_t)0xFFFFFFFFLL) {
             const int c0 = counts_at(t), c1 = counts_at(t + 1);
             if (ctx->counted + c0 + c1 > 65535)
@@ -771,7 +815,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             }
             ctx->gen.c.rlo = rlo;
             ctx->gen.c.rhi = rhi;
-            return launch_sweep_general(ctx->gen, ctx->cfg.batch, s);
+            return launch_sweep_general(ctx->gen, ctx->cfg.batch, 1, s);
         };
         const int R = ctx->lay.rows;
         int e = 0;

@@ -23,6 +23,7 @@
 // (ballot + popc) and processed round-robin by all 32 lanes, so a warp pays
 // ceil(#fp64 sites / 32) fp64 evaluations instead of one per site slot that any lane needs.
 // The free-boundary sentinel 0xFF never equals a label, so n_i(s) needs no position test.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -31,17 +32,14 @@
 namespace pcab200 {
 namespace {
 
+namespace cg = cooperative_groups;
+
 constexpr int GEN_THREADS = 128;
 constexpr int GEN_WARPS = GEN_THREADS / 32;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t ldg4(const uint8_t* p) {
     return __ldg(reinterpret_cast<const uint32_t*>(p));
-}
-
-// byte at window position pos (0..11) of a 3-word row window
-__device__ __forceinline__ int win_byte(const uint32_t (&w)[3], int pos) {
-    return (int)((w[pos >> 2] >> (8 * (pos & 3))) & 0xFFu);
 }
 
 // a queued fp64 site: neighbour labels (NB <= 8 bytes), x_i, g_i, the Philox word
@@ -161,151 +159,211 @@ __device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const 
 // Uniform-neighbourhood thresholds staged in shared memory when the table is small.
 __host__ __device__ constexpr int uthr_smem_entries(int LT) { return (LT > 0 && LT <= 9) ? LT * LT * LT * (LT - 1) : 1; }
 
-template <int NB, int LT>  // LT: levels known at compile time, 0 = any
-__global__ void __launch_bounds__(GEN_THREADS, 4)
-    sweep_general_kernel(const __grid_constant__ GeneralSweepParams p, int R) {
-    __shared__ double sA[9];
-    __shared__ double sD[LT > 0 ? LT * LT : 1];
-    __shared__ double sI[LT > 0 ? LT * LT : 1];
-    __shared__ uint32_t sU[uthr_smem_entries(LT)];
-    __shared__ SiteJob s_jobs[GEN_WARPS][128];
-    __shared__ uint8_t s_res[GEN_WARPS][128];
-    constexpr bool SMEM_U = LT > 0 && LT <= 9;
-    if (threadIdx.x < 9) sA[threadIdx.x] = p.A[threadIdx.x];
-    if (LT > 0)
-        for (int i = threadIdx.x; i < LT * LT; i += GEN_THREADS) {
-            sD[i] = p.dtab[i];
-            sI[i] = p.inertia_p != 0 ? p.itab[i] : 0.0;
-        }
-    if (SMEM_U && p.uthr != nullptr)
-        for (int i = threadIdx.x; i < uthr_smem_entries(LT); i += GEN_THREADS) sU[i] = p.uthr[i];
-    __syncthreads();
+template <int LT>
+struct GenSmem {
+    double A[9];
+    double D[LT > 2 ? LT * LT : 1];
+    double I[LT > 2 ? LT * LT : 1];
+    uint32_t U[LT == 2 ? THR_ENTRIES : uthr_smem_entries(LT)];  // levels == 2: binary table
+    SiteJob jobs[GEN_WARPS][128];
+    uint8_t res[GEN_WARPS][128];
+};
 
+template <int LT>
+__device__ __forceinline__ void gen_load_tables(const GeneralSweepParams& p, GenSmem<LT>& sm) {
+    if (threadIdx.x < 9) sm.A[threadIdx.x] = p.A[threadIdx.x];
+    if (LT > 2)
+        for (int i = threadIdx.x; i < LT * LT; i += blockDim.x) {
+            sm.D[i] = p.dtab[i];
+            sm.I[i] = p.inertia_p != 0 ? p.itab[i] : 0.0;
+        }
+    if (LT == 2)
+        for (int i = threadIdx.x; i < THR_ENTRIES; i += blockDim.x) sm.U[i] = p.bthr[i];
+    else if (LT > 0 && LT <= 9 && p.uthr != nullptr)
+        for (int i = threadIdx.x; i < uthr_smem_entries(LT); i += blockDim.x) sm.U[i] = p.uthr[i];
+}
+
+// Work decomposition shared by both kernels: a block of GEN_THREADS threads covers QW
+// consecutive quads (QW = the quad count rounded up to a power of two, at most GEN_THREADS)
+// times RS = GEN_THREADS / QW row runs of R rows, so narrow lattices keep every lane busy.
+struct Decomp {
+    int QW, RS, R;  // quads per block row, row runs per block, rows per run
+    int nxb, nrb;   // x-blocks, run-blocks (each RS runs)
+};
+__host__ __device__ inline Decomp make_decomp(int nquads, int nrows, int R) {
+    Decomp d;
+    d.QW = 1;
+    while (d.QW < nquads && d.QW < GEN_THREADS) d.QW <<= 1;
+    d.RS = GEN_THREADS / d.QW;
+    d.R = R < 1 ? 1 : R;
+    d.nxb = (nquads + d.QW - 1) / d.QW;
+    const int runs = (nrows + d.R - 1) / d.R;
+    d.nrb = (runs + d.RS - 1) / d.RS;
+    return d;
+}
+
+// One quad column (4 sites, quad qd) of chain `chain` over local rows [rbeg, rend), sweep t:
+// x_in -> x_out.  Every thread of the block calls it with the same `iters` (the warp-level
+// queue needs uniform trip counts); lanes past their rows idle.  COH: x is read through L2
+// (ld.global.cg) because an earlier sweep of the same launch wrote it; otherwise through the
+// read-only path.
+template <int NB, int LT, bool COH>
+__device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT>& sm,
+                                         const uint8_t* __restrict__ x_in, uint8_t* __restrict__ x_out,
+                                         uint32_t t, int count_enable, int qd, int chain, int rbeg,
+                                         int rend, int iters) {
+    constexpr bool SMEM_U = LT > 0 && LT <= 9;
     const Geometry& G = p.c.geo;
     const int L = G.levels;
     const int nquads = (G.W + 3) >> 2;
-    const int qd = blockIdx.x * GEN_THREADS + threadIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int chain = blockIdx.z;
-    const bool active = qd < nquads;
+    const bool active = qd < nquads && rbeg < rend;
     if (__ballot_sync(FULL, active) == 0) return;  // warp-uniform exit
-    const int rbeg = p.c.rlo + blockIdx.y * R;
-    const int rend = min(rbeg + R, p.c.rhi);
-    if (rbeg >= rend) return;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const unsigned lt = (1u << lane) - 1u;
-    SiteJob* jobs = s_jobs[warp];
-    uint8_t* res = s_res[warp];
-    const bool use_u = p.uthr != nullptr;
-    const uint32_t* U = SMEM_U ? sU : p.uthr;
+    SiteJob* jobs = sm.jobs[warp];
+    uint8_t* res = sm.res[warp];
+    const bool use_u = LT == 2 || p.uthr != nullptr;
+    const uint32_t* U = (SMEM_U || LT == 2) ? sm.U : p.uthr;
     const int c0 = 4 * qd;
     const int nvalid = active ? min(4, G.W - c0) : 0;
-    const uint8_t* xcol = p.c.x_in + chain * G.xchain + XOFF + c0;
+    const uint8_t* xcol = x_in + chain * G.xchain + XOFF + c0;
     const uint8_t* gcol = p.c.g + chain * G.gchain + XOFF + c0;
 
     // rolling 3-row window of the words left of / at / right of the quad
     uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0};
     auto load_row = [&](int r, uint32_t (&w)[3]) {
-        if (!active) return;
         const uint8_t* xr = xcol + (long long)(r + HALO) * G.xpitch;
-        w[0] = ldg4(xr - 4);
-        w[1] = ldg4(xr);
-        w[2] = ldg4(xr + 4);
+        if (COH) {
+            w[0] = __ldcg(reinterpret_cast<const uint32_t*>(xr - 4));
+            w[1] = __ldcg(reinterpret_cast<const uint32_t*>(xr));
+            w[2] = __ldcg(reinterpret_cast<const uint32_t*>(xr + 4));
+        } else {
+            w[0] = ldg4(xr - 4);
+            w[1] = ldg4(xr);
+            w[2] = ldg4(xr + 4);
+        }
     };
     // software pipeline: the x row r+2 and the g row r+1 are loaded one iteration ahead, so
     // the load latency overlaps a row of work (rows rbeg-1 .. rend+1 exist: HALO = 2)
     uint32_t nxt[3] = {0, 0, 0}, gnext = 0;
-    load_row(rbeg - 1, up);
-    load_row(rbeg, mid);
-    load_row(rbeg + 1, nxt);
-    if (active) gnext = ldg4(gcol + (long long)(rbeg + GHALO) * G.gpitch);
+    if (active) {
+        load_row(rbeg - 1, up);
+        load_row(rbeg, mid);
+        load_row(rbeg + 1, nxt);
+        gnext = ldg4(gcol + (long long)(rbeg + GHALO) * G.gpitch);
+    }
 
-    for (int r = rbeg; r < rend; ++r) {
+    for (int it = 0; it < iters; ++it) {
+        const int r = rbeg + it;
+        const bool act = active && r < rend;
 #pragma unroll
         for (int j = 0; j < 3; ++j) dn[j] = nxt[j];
         const uint32_t gword = gnext;
-        if (r + 1 < rend) {
+        if (act && r + 1 < rend) {
             load_row(r + 2, nxt);
-            if (active) gnext = ldg4(gcol + (long long)(r + 1 + GHALO) * G.gpitch);
+            gnext = ldg4(gcol + (long long)(r + 1 + GHALO) * G.gpitch);
         }
         const int grow = G.row0 + r;
         uint4 rnd = make_uint4(0, 0, 0, 0);
-        if (active)
-            rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+        if (act)
+            rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, t, tagchain), p.c.keys);
         // the neighbours of the 4 sites, one byte per site (byte b = neighbour of site b)
         const uint32_t UL = from_left(up[0], up[1]), UC = up[1], UR = from_right(up[1], up[2]);
         const uint32_t ML = from_left(mid[0], mid[1]), MR = from_right(mid[1], mid[2]);
         const uint32_t DL = from_left(dn[0], dn[1]), DC = dn[1], DR = from_right(dn[1], dn[2]);
-        // uniform neighbourhood: all NB neighbour bytes equal (chain of XORs), SWAR zero test
-        uint32_t D;
-        if (NB == 8)
-            D = (UL ^ UC) | (UC ^ UR) | (UR ^ ML) | (ML ^ MR) | (MR ^ DL) | (DL ^ DC) | (DC ^ DR);
-        else
-            D = (UC ^ ML) | (ML ^ MR) | (MR ^ DC);
-        const uint32_t differ = (((D & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | D) & 0x80808080u;
-        const uint32_t S0 = NB == 8 ? UL : UC;  // s* when uniform
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
         const uint32_t xw = mid[1];
         uint32_t outw = 0u;
-        int qpos[4];
-        int qbase = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int xi = (int)((xw >> (8 * b)) & 0xFFu);
-            const int gi = (int)((gword >> (8 * b)) & 0xFFu);
-            const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
-            const bool valid = b < nvalid;
-            const bool uniform = use_u && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
-            if (valid && uniform) {
-                // every neighbour carries s* = s0 (so all NB exist): integer thresholds
-                const uint32_t* T = U + (size_t)((s0 * L + gi) * L + xi) * (L - 1);
-                int w = 0;
-                if (LT > 0) {
-#pragma unroll
-                    for (int k = 0; k < (LT > 0 ? LT - 1 : 1); ++k) w += (rr[b] > (SMEM_U ? T[k] : __ldg(T + k))) ? 1 : 0;
-                } else {
-                    for (int k = 0; k < L - 1; ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
-                }
-                outw |= (uint32_t)w << (8 * b);
-            }
-            // compact the fp64 sites of the warp into its queue
-            const bool need = valid && !uniform;
-            const unsigned m = __ballot_sync(FULL, need);
-            qpos[b] = qbase + __popc(m & lt);
-            if (need) {
-                const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);  // byte b of a, of b
-                SiteJob jb;
-                if (NB == 8) {
-                    jb.nb_lo = __byte_perm(__byte_perm(UL, UC, sel), __byte_perm(UR, ML, sel), 0x5410);
-                    jb.nb_hi = __byte_perm(__byte_perm(MR, DL, sel), __byte_perm(DC, DR, sel), 0x5410);
-                } else {
-                    jb.nb_lo = __byte_perm(__byte_perm(UC, ML, sel), __byte_perm(MR, DC, sel), 0x5410);
-                    jb.nb_hi = 0u;
-                }
-                jb.xg = (uint32_t)xi | ((uint32_t)gi << 8);
-                jb.r = rr[b];
-                jobs[qpos[b]] = jb;
+        if (LT == 2) {
+            // two levels: every site is an integer-threshold decision (as sweep_binary.cu):
+            // T[((np*9 + n1)*2 + g)*2 + x], n1 / np = label-1 / present neighbours (SWAR)
+            auto one = [](uint32_t w) { return w & ~(w >> 1) & 0x01010101u; };  // 0xFF -> 0
+            auto pres = [](uint32_t w) { return (~w >> 7) & 0x01010101u; };     // 0xFF -> 0
+            uint32_t n1, np;
+            if (NB == 8) {
+                n1 = one(UL) + one(UC) + one(UR) + one(ML) + one(MR) + one(DL) + one(DC) + one(DR);
+                np = pres(UL) + pres(UC) + pres(UR) + pres(ML) + pres(MR) + pres(DL) + pres(DC) + pres(DR);
             } else {
-                qpos[b] = -1;
+                n1 = one(UC) + one(ML) + one(MR) + one(DC);
+                np = pres(UC) + pres(ML) + pres(MR) + pres(DC);
             }
-            qbase += __popc(m);
-        }
-        if (qbase > 0) {  // warp-uniform
-            __syncwarp();
-            for (int i = lane; i < qbase; i += 32) {
-                int w = -1;
-                if (LT > 0) w = decide_fp64_fixed<NB, (LT > 0 ? LT : 2)>(p, sA, sD, sI, jobs[i]);
-                if (w < 0) w = decide_fp64<NB>(p, sA, jobs[i]);
-                res[i] = (uint8_t)w;
-            }
-            __syncwarp();
+            const uint32_t lo4 = (((n1 << 1) | gword) << 1) | xw;  // (n1*2 + g)*2 + x <= 35
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (qpos[b] >= 0) outw |= (uint32_t)res[qpos[b]] << (8 * b);
-            __syncwarp();
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t idx = ((np >> (8 * b)) & 0xFFu) * 36u + ((lo4 >> (8 * b)) & 0xFFu);
+                outw |= (rr[b] > U[idx] ? 1u : 0u) << (8 * b);
+            }
+        } else {
+            // uniform neighbourhood: all NB neighbour bytes equal (chain of XORs), SWAR zero test
+            uint32_t D;
+            if (NB == 8)
+                D = (UL ^ UC) | (UC ^ UR) | (UR ^ ML) | (ML ^ MR) | (MR ^ DL) | (DL ^ DC) | (DC ^ DR);
+            else
+                D = (UC ^ ML) | (ML ^ MR) | (MR ^ DC);
+            const uint32_t differ = (((D & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | D) & 0x80808080u;
+            const uint32_t S0 = NB == 8 ? UL : UC;  // s* when uniform
+            int qpos[4];
+            int qbase = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int xi = (int)((xw >> (8 * b)) & 0xFFu);
+                const int gi = (int)((gword >> (8 * b)) & 0xFFu);
+                const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
+                const bool valid = act && b < nvalid;
+                const bool uniform = use_u && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
+                if (valid && uniform) {
+                    // every neighbour carries s* = s0 (so all NB exist): integer thresholds
+                    const uint32_t* T = U + (size_t)((s0 * L + gi) * L + xi) * (L - 1);
+                    int w = 0;
+                    if (LT > 0) {
+#pragma unroll
+                        for (int k = 0; k < (LT > 0 ? LT - 1 : 1); ++k)
+                            w += (rr[b] > (SMEM_U ? T[k] : __ldg(T + k))) ? 1 : 0;
+                    } else {
+                        for (int k = 0; k < L - 1; ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
+                    }
+                    outw |= (uint32_t)w << (8 * b);
+                }
+                // compact the fp64 sites of the warp into its queue
+                const bool need = valid && !uniform;
+                const unsigned m = __ballot_sync(FULL, need);
+                qpos[b] = qbase + __popc(m & lt);
+                if (need) {
+                    const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);  // byte b of a, of b
+                    SiteJob jb;
+                    if (NB == 8) {
+                        jb.nb_lo = __byte_perm(__byte_perm(UL, UC, sel), __byte_perm(UR, ML, sel), 0x5410);
+                        jb.nb_hi = __byte_perm(__byte_perm(MR, DL, sel), __byte_perm(DC, DR, sel), 0x5410);
+                    } else {
+                        jb.nb_lo = __byte_perm(__byte_perm(UC, ML, sel), __byte_perm(MR, DC, sel), 0x5410);
+                        jb.nb_hi = 0u;
+                    }
+                    jb.xg = (uint32_t)xi | ((uint32_t)gi << 8);
+                    jb.r = rr[b];
+                    jobs[qpos[b]] = jb;
+                } else {
+                    qpos[b] = -1;
+                }
+                qbase += __popc(m);
+            }
+            if (qbase > 0) {  // warp-uniform
+                __syncwarp();
+                for (int i = lane; i < qbase; i += 32) {
+                    int w = -1;
+                    if (LT > 2) w = decide_fp64_fixed<NB, (LT > 2 ? LT : 3)>(p, sm.A, sm.D, sm.I, jobs[i]);
+                    if (w < 0) w = decide_fp64<NB>(p, sm.A, jobs[i]);
+                    res[i] = (uint8_t)w;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (qpos[b] >= 0) outw |= (uint32_t)res[qpos[b]] << (8 * b);
+                __syncwarp();
+            }
         }
-        if (active) {
-            uint8_t* op = p.c.x_out + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
+        if (act) {
+            uint8_t* op = x_out + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
             auto store = [&](uint8_t* dst) {
                 if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
                 else for (int b = 0; b < nvalid; ++b) dst[b] = (uint8_t)(outw >> (8 * b));
@@ -324,7 +382,7 @@ __global__ void __launch_bounds__(GEN_THREADS, 4)
                 if (r < HALO) store(op + (long long)G.rows * G.xpitch);
                 if (r >= G.rows - HALO) store(op - (long long)G.rows * G.xpitch);
             }
-            if (p.c.count_enable) {
+            if (count_enable) {
                 uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
                 if (nvalid == 4) {
                     // the quad's 4 counters of a plane form one 8-byte word; each distinct label
@@ -370,44 +428,120 @@ __global__ void __launch_bounds__(GEN_THREADS, 4)
     }
 }
 
+template <int NB, int LT>  // LT: levels known at compile time, 0 = any
+__global__ void __launch_bounds__(GEN_THREADS, 4)
+    sweep_general_kernel(const __grid_constant__ GeneralSweepParams p, int R) {
+    __shared__ GenSmem<LT> sm;
+    gen_load_tables<LT>(p, sm);
+    __syncthreads();
+    const Decomp d = make_decomp(((p.c.geo.W + 3) >> 2), p.c.rhi - p.c.rlo, R);
+    const int qd = blockIdx.x * d.QW + (threadIdx.x & (d.QW - 1));
+    const int rbeg = p.c.rlo + (blockIdx.y * d.RS + threadIdx.x / d.QW) * d.R;
+    const int rend = min(rbeg + d.R, p.c.rhi);
+    gen_rows<NB, LT, false>(p, sm, p.c.x_in, p.c.x_out, p.c.t, p.c.count_enable, qd, blockIdx.z,
+                            rbeg, rend, d.R);
+}
+
+// Small lattices: `nsweeps` consecutive sweeps (one beta stage, one counting mode) in ONE
+// cooperative launch, the grid synchronising between sweeps, instead of one launch per sweep
+// (a 64^2 or 256^2 sweep is a few microseconds of launch latency and under a microsecond of
+// work).  Work items (x-block, row block, chain) are distributed grid-stride; the double
+// buffer alternates in the kernel.  Same per-site code, same chain.
 template <int NB, int LT>
-int launch_g(const GeneralSweepParams& p, int batch, cudaStream_t s) {
-    static int occ = 0, sms = 0;
-    if (occ == 0) {
+__global__ void __launch_bounds__(GEN_THREADS, 4)
+    sweep_multi_kernel(const __grid_constant__ GeneralSweepParams p, int R, int nsweeps, int batch) {
+    __shared__ GenSmem<LT> sm;
+    gen_load_tables<LT>(p, sm);
+    __syncthreads();
+    const Decomp d = make_decomp(((p.c.geo.W + 3) >> 2), p.c.rhi - p.c.rlo, R);
+    const int items = d.nxb * d.nrb * batch;
+    for (int sw = 0; sw < nsweeps; ++sw) {
+        const uint8_t* xi = (sw & 1) ? p.c.x_out : p.c.x_in;
+        uint8_t* xo = (sw & 1) ? const_cast<uint8_t*>(p.c.x_in) : p.c.x_out;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            const int xb = it % d.nxb;
+            const int rb = (it / d.nxb) % d.nrb;
+            const int chain = it / (d.nxb * d.nrb);
+            const int qd = xb * d.QW + (threadIdx.x & (d.QW - 1));
+            const int rbeg = p.c.rlo + (rb * d.RS + threadIdx.x / d.QW) * d.R;
+            const int rend = min(rbeg + d.R, p.c.rhi);
+            gen_rows<NB, LT, true>(p, sm, xi, xo, p.c.t + (uint32_t)sw, p.c.count_enable, qd, chain,
+                                   rbeg, rend, d.R);
+        }
+        // every store of this sweep (x, halos, count reductions) before any read of the next;
+        // a one-block grid needs only the block barrier
+        if (gridDim.x == 1) {
+            __syncthreads();
+        } else {
+            __threadfence();
+            cg::this_grid().sync();
+        }
+    }
+}
+
+template <int NB, int LT>
+struct GenLaunch {
+    static int occ, sms, mocc;
+    static void init() {
+        if (occ) return;
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_general_kernel<NB, LT>, GEN_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, sweep_multi_kernel<NB, LT>, GEN_THREADS, 0);
         if (occ < 1) occ = 1;
+        if (mocc < 1) mocc = 1;
     }
+};
+template <int NB, int LT> int GenLaunch<NB, LT>::occ = 0;
+template <int NB, int LT> int GenLaunch<NB, LT>::sms = 0;
+template <int NB, int LT> int GenLaunch<NB, LT>::mocc = 0;
+
+template <int NB, int LT>
+int launch_g(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t s) {
+    using GL = GenLaunch<NB, LT>;
+    GL::init();
     const Geometry& G = p.c.geo;
     const int nquads = (G.W + 3) / 4;
     const int nr = p.c.rhi - p.c.rlo;
     if (nr <= 0) return 0;
-    const long long xblocks = (nquads + GEN_THREADS - 1) / GEN_THREADS;
-    // rows per block: about four waves of blocks (the fp64 share of a row varies, so several
-    // waves balance the tail), each block walking a run of rows with a rolling window
-    const long long target = 4LL * sms * occ;
-    long long R = ((long long)nr * xblocks * batch + target - 1) / target;
-    if (R < 1) R = 1;
-    long long nrb = (nr + R - 1) / R;
-    if (nrb > 65535) {
-        nrb = 65535;
-        R = (nr + nrb - 1) / nrb;
+    const Decomp d1 = make_decomp(nquads, nr, 1);
+    const long long quadrows = (long long)d1.nxb * d1.QW * nr * batch;  // thread-rows of work
+    if (nsweeps > 1) {
+        // spread the thread-rows over the co-resident blocks, one row per thread when they fit
+        const long long slots = (long long)GL::sms * GL::mocc;
+        long long R = (quadrows + slots * GEN_THREADS - 1) / (slots * GEN_THREADS);
+        if (R < 1) R = 1;
+        const Decomp d = make_decomp(nquads, nr, (int)R);
+        const long long items = (long long)d.nxb * d.nrb * batch;
+        const int grid = (int)(items < slots ? items : slots);
+        GeneralSweepParams pp = p;
+        int Ri = (int)R, ns = nsweeps, b = batch;
+        void* args[] = {&pp, &Ri, &ns, &b};
+        return (int)cudaLaunchCooperativeKernel((const void*)sweep_multi_kernel<NB, LT>, dim3(grid),
+                                                dim3(GEN_THREADS), args, 0, s);
     }
-    dim3 grid((unsigned)xblocks, (unsigned)nrb, batch);
-    sweep_general_kernel<NB, LT><<<grid, GEN_THREADS, 0, s>>>(p, (int)R);
+    // rows per run: about four waves of blocks (the fp64 share of a row varies, so several
+    // waves balance the tail), each thread walking a run of rows with a rolling window
+    const long long target = 4LL * GL::sms * GL::occ * GEN_THREADS;
+    long long R = (quadrows + target - 1) / target;
+    if (R < 1) R = 1;
+    Decomp d = make_decomp(nquads, nr, (int)R);
+    while (d.nrb > 65535) d = make_decomp(nquads, nr, d.R * 2);
+    dim3 grid((unsigned)d.nxb, (unsigned)d.nrb, batch);
+    sweep_general_kernel<NB, LT><<<grid, GEN_THREADS, 0, s>>>(p, d.R);
     return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-int launch_sweep_general(const GeneralSweepParams& p, int batch, void* stream) {
+int launch_sweep_general(const GeneralSweepParams& p, int batch, int nsweeps, void* stream) {
     const Geometry& G = p.c.geo;
     cudaStream_t s = (cudaStream_t)stream;
 #define PCA_GEN_LAUNCH(LTV) \
-    return G.nbhd == 8 ? launch_g<8, LTV>(p, batch, s) : launch_g<4, LTV>(p, batch, s)
-    switch (G.levels) {  // the paper's level counts (and 3) get fully unrolled fp64 paths
+    return G.nbhd == 8 ? launch_g<8, LTV>(p, batch, nsweeps, s) : launch_g<4, LTV>(p, batch, nsweeps, s)
+    switch (G.levels) {  // two levels: exact integer path; the paper's level counts (and 3)
+        case 2: PCA_GEN_LAUNCH(2);  // get fully unrolled fp64 paths
         case 3: PCA_GEN_LAUNCH(3);
         case 5: PCA_GEN_LAUNCH(5);
         case 9: PCA_GEN_LAUNCH(9);
