@@ -45,6 +45,11 @@ namespace {
 #ifndef PCA_T_CREG
 #define PCA_T_CREG 1
 #endif
+// PCA_T_RED = 1: torus counts by fire-and-forget 64-bit reductions (no load): measured
+// 138 us per sweep (16.8 M RED.64 per sweep saturate the L2 atomic units), so it stays off.
+#ifndef PCA_T_RED
+#define PCA_T_RED 0
+#endif
 #ifndef PCA_F_K
 #define PCA_F_K 4
 #endif
@@ -64,8 +69,9 @@ template <bool PER>
 struct RingCfg {
     static constexpr int K = PER ? PCA_T_K : PCA_F_K;           // ring depth (2 rows per stage)
     static constexpr int CTAS = PER ? PCA_T_CTAS : PCA_F_CTAS;  // resident one-warp CTAs per SM
-    static constexpr bool CREG = PER ? PCA_T_CREG : PCA_F_CREG; // counts via registers
-    static constexpr int STAGE = COFS + (CREG ? 0 : 2 * CROW_BYTES);  // 2112 or 4160 bytes
+    static constexpr bool RED = PER ? PCA_T_RED : 0;              // counts via reductions
+    static constexpr bool CREG = !RED && (PER ? PCA_T_CREG : PCA_F_CREG); // counts via registers
+    static constexpr int STAGE = COFS + ((CREG || RED) ? 0 : 2 * CROW_BYTES);  // 2112 or 4160
     static constexpr int RING_OFF = ((K + 1) * 8 + 63) / 64 * 64;    // mbarriers, then the ring
     static constexpr int SMEM = RING_OFF + K * STAGE;                // dynamic smem per CTA
     static_assert(K + 1 <= RING_OFF / 8, "mbarrier slots");
@@ -97,6 +103,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     constexpr int KSTAGES = C::K;
     constexpr int STAGE_BYTES = C::STAGE;
     constexpr bool CREG = C::CREG;  // counts prefetched into registers (no ring slot)
+    constexpr bool RED = C::RED;    // counts added by reductions (no ring slot, no load)
     __shared__ __align__(16) uint32_t s_thr[THR_ENTRIES];  // static: LDS [reg + imm]
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -153,12 +160,12 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
         const int nx = (rbeg - 1 + jx + 1 <= rend) ? 2 : 1;
         const int jr = 2 * it - 2;         // g / count row rbeg+jr
         const int nr = it == 0 ? 0 : min(2, rend - rbeg - jr);
-        mbar_expect_tx(&bars[s], nx * xbytes + nr * (gbytes + (CREG ? 0u : cbytes)));
+        mbar_expect_tx(&bars[s], nx * xbytes + nr * (gbytes + ((CREG || RED) ? 0u : cbytes)));
         for (int q = 0; q < nx; ++q)
             bulk_g2s(st + XOFS + q * XROW_BYTES, xin + (long long)(jx + q) * G.xpitch, xbytes, &bars[s]);
         for (int q = 0; q < nr; ++q) {
             bulk_g2s(st + GOFS + q * GROW_BYTES, gin + (long long)(jr + q) * G.gpitch, gbytes, &bars[s]);
-            if (!CREG && cbytes)
+            if (!CREG && !RED && cbytes)
                 bulk_g2s(st + COFS + q * CROW_BYTES, cin + (long long)(jr + q) * G.cpitch, cbytes,
                          &bars[s]);
         }
@@ -337,7 +344,17 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
             if (q == 1 && nrow < 2) break;
             const int r = r0 + q;
             // ---- fused MPM counts of label 1 (uint16 per site) ----
-            if (cbytes) {
+            if (cbytes && RED) {
+                unsigned long long* cp =
+                    reinterpret_cast<unsigned long long*>(co + (long long)(r - rbeg) * G.cpitch);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const unsigned long long inc =
+                        (unsigned long long)__byte_perm(O[q][i], 0u, 0x4140) |
+                        ((unsigned long long)__byte_perm(O[q][i], 0u, 0x4342) << 32);
+                    atomicAdd(cp + i, inc);
+                }
+            } else if (cbytes) {
                 uint4 c0, c1;
                 if (CREG) {
                     c0 = CR[q][0];
