@@ -184,6 +184,15 @@ pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int
 pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* psnr,
                          double* ssim);
 
+/* The end of a run in ONE fused pass over truth, the current state and the counts
+ * (SURVEY 8(a) a8 + a9): the MPM image (written to mpm_out, host or device
+ * [batch][rows][width], when non-NULL) and PSNR / global SSIM of both the last sample and
+ * the MPM estimate, psnr[2*b + 0] / ssim[2*b + 0] for LAST and [2*b + 1] for MPM (each
+ * array [batch][2]).  Same definitions and exactness as pca_psnr_ssim; needs counted sweeps;
+ * sums are all-reduced over NCCL for row strips.  Synchronises. */
+pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
+                        double* ssim);
+
 /* Windowed SSIM (R16's secondary metric, the form Table 1 of PAPER.md:703 appears to use):
  * the mean over every 7x7 window position inside the image (stride 1, no padding) of
  *   SSIM_w = (2 mx my + c1)(2 sxy + c2) / ((mx^2 + my^2 + c1)(sx^2 + sy^2 + c2)),

@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "PCA_OK", -1: "PCA_EINVAL", -2: "PCA_ESTATE", -3: "PCA_ECUDA"
 
 # every symbol include/pca.h declares
 EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "pca_sweep",
-           "pca_gibbs_sweep", "pca_estimate", "pca_metric_sums", "pca_psnr_ssim",
+           "pca_gibbs_sweep", "pca_estimate", "pca_metric_sums", "pca_psnr_ssim", "pca_finalize",
            "pca_ssim_windowed", "pca_read_state",
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
@@ -95,6 +95,7 @@ def lib():
             "pca_metric_sums": (i32, [vp, vp, i32, vp]),
             "pca_psnr_ssim": (i32, [vp, vp, i32, vp, vp]),
             "pca_ssim_windowed": (i32, [vp, vp, i32, vp]),
+            "pca_finalize": (i32, [vp, vp, vp, vp, vp]),
             "pca_read_state": (i32, [vp, vp]),
             "pca_write_state": (i32, [vp, vp]),
             "pca_read_counts": (i32, [vp, vp]),
@@ -217,6 +218,15 @@ class PcaContext:
         s = np.zeros(self.cfg.batch, np.float64)
         _check(lib().pca_psnr_ssim(self.handle, _ptr(truth), int(kind), p.ctypes.data,
                                    s.ctypes.data), "pca_psnr_ssim")
+        return p, s
+
+    def pca_finalize(self, truth, mpm_out=None):
+        """MPM image (into mpm_out when given) and PSNR / SSIM of LAST and MPM in one pass:
+        returns (psnr, ssim), each [batch][2] (column 0 LAST, column 1 MPM)."""
+        p = np.zeros((self.cfg.batch, 2), np.float64)
+        s = np.zeros((self.cfg.batch, 2), np.float64)
+        _check(lib().pca_finalize(self.handle, _ptr(truth), _ptr(mpm_out), p.ctypes.data,
+                                  s.ctypes.data), "pca_finalize")
         return p, s
 
     def pca_ssim_windowed(self, truth, kind: int):

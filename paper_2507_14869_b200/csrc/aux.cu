@@ -7,6 +7,7 @@
 //  * metric_sums: one pass over truth and the LAST or MPM estimate, accumulating the exact
 //    integer sums of PAPER.md:516-534's statistics (sum (x-y)^2, sum x, sum y, sum x^2,
 //    sum y^2, sum xy, max x) per chain; block reduction, then one atomic per block per sum.
+//    The finalisation variant does LAST and MPM (and stores the MPM image) in one pass.
 //  * ssim_windowed: mean SSIM over every 7x7 window (R16's secondary metric): exact integer
 //    window sums, fp64 per window, deterministic fixed-order per-block partial sums.
 //
@@ -194,61 +195,89 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
     return v;
 }
 
+// BOTH: the finalisation pass (SURVEY 8(a) a8 + a9 fused): one read of truth, x and the
+// counts gives the MPM image (optional store) and the sums of LAST and of MPM.
+template <bool BOTH>
 __global__ void __launch_bounds__(TPB) metric_sums_kernel(const MetricParams p) {
+    constexpr int NS = BOTH ? 12 : 6;
     const Geometry& G = p.geo;
     const int chain = blockIdx.z;
     const int c0 = 16 * (blockIdx.x * TPB + threadIdx.x);
     const int n = c0 < G.W ? min(16, G.W - c0) : 0;
     const bool vec = (G.W & 15) == 0 && ((uintptr_t)p.truth & 15) == 0;
+    const bool ovec = (G.W & 15) == 0 && ((uintptr_t)p.mpm_out & 15) == 0;
     const uint8_t* truth = p.truth + (long long)chain * G.rows * G.W;
     const uint8_t* xb = p.x + chain * G.xchain;
     const uint16_t* cc = p.counts + chain * G.cchain;
-    unsigned long long s[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long s[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = 0;
     uint32_t mx = 0;
     if (n > 0) {
         for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
             const uint4 tv = load16(truth + (long long)r * G.W, c0, n, vec);
-            const uint4 yv = p.kind == 0 ? load16(xb + (long long)(r + HALO) * G.xpitch + XOFF, c0, n, true)
-                                         : mpm16(G, cc, r, c0, p.nsamp);
-            uint32_t t[6] = {0, 0, 0, 0, 0, 0};  // 16 sites: every partial sum < 2^21
+            uint4 yv[2];
+            if (BOTH) {
+                yv[0] = load16(xb + (long long)(r + HALO) * G.xpitch + XOFF, c0, n, true);
+                yv[1] = mpm16(G, cc, r, c0, p.nsamp);
+                if (p.mpm_out) store16(p.mpm_out + ((long long)chain * G.rows + r) * G.W, c0, n, ovec, yv[1]);
+            } else {
+                yv[0] = p.kind == 0 ? load16(xb + (long long)(r + HALO) * G.xpitch + XOFF, c0, n, true)
+                                    : mpm16(G, cc, r, c0, p.nsamp);
+            }
+            uint32_t t[NS];  // 16 sites: every partial sum < 2^21
+#pragma unroll
+            for (int k = 0; k < NS; ++k) t[k] = 0;
             for (int j = 0; j < n; ++j) {
-                const uint32_t x = byte_of(tv, j), y = byte_of(yv, j);
-                const int d = (int)x - (int)y;
-                t[0] += (uint32_t)(d * d);
-                t[1] += x;
-                t[2] += y;
-                t[3] += x * x;
-                t[4] += y * y;
-                t[5] += x * y;
+                const uint32_t x = byte_of(tv, j);
                 mx = x > mx ? x : mx;
+#pragma unroll
+                for (int e = 0; e < (BOTH ? 2 : 1); ++e) {
+                    const uint32_t y = byte_of(yv[e], j);
+                    const int d = (int)x - (int)y;
+                    t[6 * e + 0] += (uint32_t)(d * d);
+                    t[6 * e + 1] += x;
+                    t[6 * e + 2] += y;
+                    t[6 * e + 3] += x * x;
+                    t[6 * e + 4] += y * y;
+                    t[6 * e + 5] += x * y;
+                }
             }
 #pragma unroll
-            for (int k = 0; k < 6; ++k) s[k] += t[k];
+            for (int k = 0; k < NS; ++k) s[k] += t[k];
         }
     }
-    __shared__ unsigned long long red[TPB / 32][7];
+    __shared__ unsigned long long red[TPB / 32][NS + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) s[k] = warp_sum(s[k]);
+    for (int k = 0; k < NS; ++k) s[k] = warp_sum(s[k]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
     if (lane == 0) {
-        for (int k = 0; k < 6; ++k) red[warp][k] = s[k];
-        red[warp][6] = mx;
+        for (int k = 0; k < NS; ++k) red[warp][k] = s[k];
+        red[warp][NS] = mx;
     }
     __syncthreads();
-    if (threadIdx.x < 7) {
+    // slot layout per estimate: 0..5 sums, 6 max truth, 7 site count
+    if (threadIdx.x <= NS) {
         unsigned long long acc = 0;
         for (int w = 0; w < TPB / 32; ++w) {
             const unsigned long long v = red[w][threadIdx.x];
-            acc = threadIdx.x == 6 ? (v > acc ? v : acc) : acc + v;
+            acc = threadIdx.x == NS ? (v > acc ? v : acc) : acc + v;
         }
-        unsigned long long* dst = p.sums + chain * 8;
-        if (threadIdx.x == 6) atomicMax(dst + 6, acc);
-        else atomicAdd(dst + threadIdx.x, acc);
+        unsigned long long* dst = p.sums + chain * (BOTH ? 16 : 8);
+        if (threadIdx.x == NS) {
+            atomicMax(dst + 6, acc);
+            if (BOTH) atomicMax(dst + 14, acc);
+        } else {
+            const int e = threadIdx.x / 6, k = threadIdx.x % 6;
+            atomicAdd(dst + 8 * e + k, acc);
+        }
     }
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-        atomicAdd(p.sums + chain * 8 + 7, (unsigned long long)G.rows * G.W);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        atomicAdd(p.sums + chain * (BOTH ? 16 : 8) + 7, (unsigned long long)G.rows * G.W);
+        if (BOTH) atomicAdd(p.sums + chain * 16 + 15, (unsigned long long)G.rows * G.W);
+    }
 }
 
 // x: 16-site chunks of a row; y: rows, grid-stride, sized for ~8 resident blocks per SM
@@ -376,7 +405,10 @@ int launch_marginals(const Geometry& G, const uint16_t* counts, int nsamp, float
 }
 
 int launch_metric_sums(const MetricParams& p, int batch, void* stream) {
-    metric_sums_kernel<<<chunk_grid(p.geo, batch, 512), TPB, 0, (cudaStream_t)stream>>>(p);
+    if (p.kind == 2)
+        metric_sums_kernel<true><<<chunk_grid(p.geo, batch, 512), TPB, 0, (cudaStream_t)stream>>>(p);
+    else
+        metric_sums_kernel<false><<<chunk_grid(p.geo, batch, 512), TPB, 0, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

@@ -115,12 +115,13 @@ struct GibbsSweepParams {
 
 struct MetricParams {
     Geometry geo;
-    const uint8_t* x;      // padded current state, chain 0 row -1
+    const uint8_t* x;      // padded current state, chain 0 at padded row -HALO
     const uint16_t* counts;
     const uint8_t* truth;  // dense [batch][rows][W]
-    unsigned long long* sums;  // [batch][8]
-    int kind;              // 0 LAST, 1 MPM
+    unsigned long long* sums;  // kind 0/1: [batch][8]; kind 2: [batch][16] (LAST, then MPM)
+    int kind;              // 0 LAST, 1 MPM, 2 both in one pass (finalize)
     int nsamp;             // counted sweeps (MPM ties for levels == 2)
+    uint8_t* mpm_out;      // kind 2: dense MPM image [batch][rows][W], or nullptr
 };
 
 // ---- launchers (return cudaError_t as int) ----
@@ -150,7 +151,7 @@ int launch_mpm(const Geometry& geo, const uint16_t* counts, int nsamp, uint8_t* 
                int batch, void* stream);
 int launch_marginals(const Geometry& geo, const uint16_t* counts, int nsamp, float* out,
                      long long out_chain_stride, int k, int batch, void* stream);
-int launch_metric_sums(const MetricParams& p, int batch, void* stream);
+int launch_metric_sums(const MetricParams& p, int batch, void* stream);  // kind 0, 1 or 2
 
 // windowed SSIM: 7x7 uniform windows at every position inside the image, sample moments
 constexpr int SSIM_WIN = 7, SSIM_TPB = 128, SSIM_ROWS_PER_BLOCK = 64;

@@ -196,8 +196,8 @@ Layout make_layout(const pca_config* c) {
                          ? (size_t)c->levels * c->levels * (c->levels - 1) : 0;
     L.off_gthr = o; o = align256(o + L.gthr_entries * sizeof(uint32_t));
     L.off_bthr = o; o = align256(o + THR_ENTRIES * sizeof(uint32_t));
-    L.off_sums = o; o = align256(o + B * 8 * sizeof(unsigned long long));
-    L.off_sums_max = o; o = align256(o + B * 8 * sizeof(unsigned long long));
+    L.off_sums = o; o = align256(o + B * 16 * sizeof(unsigned long long));
+    L.off_sums_max = o; o = align256(o + B * 16 * sizeof(unsigned long long));
     L.off_flag = o; o = align256(o + 256);
     L.off_stage = o; o = align256(o + L.stage_bytes);
     L.total = o;
@@ -952,6 +952,7 @@ pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int
     mp.sums = ctx->sums;
     mp.kind = kind;
     mp.nsamp = (int)ctx->counted;
+    mp.mpm_out = nullptr;
     LAUNCH(ctx, launch_metric_sums(mp, c.batch, ctx->stream));
     if (ctx->comm && ctx->nranks > 1) {
         NcclApi& N = nccl();
@@ -981,34 +982,98 @@ pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int
     return PCA_OK;
 }
 
+// PSNR (R17) and global SSIM (R16) from the exact sums
+// v[0..7] of one chain (sum d^2, sum x, sum y, sum x^2, sum y^2, sum xy, max x, N); false
+// when the original is all black (PSNR undefined)
+bool metrics_from_sums(const int64_t* v, int levels, double* psnr, double* ssim) {
+    const double L1 = (double)(levels - 1);
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    const __int128 N = v[7];
+    const double Nd = (double)v[7];
+    // MSE on luminances, PSNR with the original's max
+    const double mse = (double)v[0] / (Nd * L1 * L1);
+    const double xmax = (double)v[6] / L1;
+    *psnr = (mse == 0.0) ? INFINITY : 20.0 * log10(xmax / sqrt(mse));
+    // global SSIM (R16): population moments from exact numerators
+    const __int128 vx = N * (__int128)v[3] - (__int128)v[1] * v[1];
+    const __int128 vy = N * (__int128)v[4] - (__int128)v[2] * v[2];
+    const __int128 cxy = N * (__int128)v[5] - (__int128)v[1] * v[2];
+    const double den = Nd * Nd * L1 * L1;
+    const double mux = (double)v[1] / (Nd * L1), muy = (double)v[2] / (Nd * L1);
+    const double sx = (double)vx / den, sy = (double)vy / den, sxy = (double)cxy / den;
+    *ssim = ((2.0 * mux * muy + c1) * (2.0 * sxy + c2)) / ((mux * mux + muy * muy + c1) * (sx + sy + c2));
+    return v[6] != 0;
+}
+
 pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* psnr,
                          double* ssim) {
     if (!psnr || !ssim) return fail(PCA_EINVAL, "psnr and ssim must be non-NULL");
     std::vector<int64_t> s((size_t)(ctx ? ctx->cfg.batch : 1) * 8);
     pca_status st = pca_metric_sums(ctx, truth, kind, s.data());
     if (st != PCA_OK) return st;
-    const double L1 = (double)(ctx->cfg.levels - 1);
-    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
     bool black = false;
-    for (int b = 0; b < ctx->cfg.batch; ++b) {
-        const int64_t* v = &s[(size_t)b * 8];
-        const __int128 N = v[7];
-        const double Nd = (double)v[7];
-        // MSE on luminances, PSNR with the original's max
-        const double mse = (double)v[0] / (Nd * L1 * L1);
-        if (v[6] == 0) black = true;
-        const double xmax = (double)v[6] / L1;
-        psnr[b] = (mse == 0.0) ? INFINITY : 20.0 * log10(xmax / sqrt(mse));
-        // global SSIM (R16): population moments from exact numerators
-        const __int128 vx = N * (__int128)v[3] - (__int128)v[1] * v[1];
-        const __int128 vy = N * (__int128)v[4] - (__int128)v[2] * v[2];
-        const __int128 cxy = N * (__int128)v[5] - (__int128)v[1] * v[2];
-        const double den = Nd * Nd * L1 * L1;
-        const double mux = (double)v[1] / (Nd * L1), muy = (double)v[2] / (Nd * L1);
-        const double sx = (double)vx / den, sy = (double)vy / den, sxy = (double)cxy / den;
-        ssim[b] = ((2.0 * mux * muy + c1) * (2.0 * sxy + c2)) /
-                  ((mux * mux + muy * muy + c1) * (sx + sy + c2));
+    for (int b = 0; b < ctx->cfg.batch; ++b)
+        if (!metrics_from_sums(&s[(size_t)b * 8], ctx->cfg.levels, &psnr[b], &ssim[b])) black = true;
+    if (black) return fail(PCA_EINVAL, "original image is all black: PSNR undefined (R17)");
+    return PCA_OK;
+}
+
+pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
+                        double* ssim) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!truth || !psnr || !ssim) return fail(PCA_EINVAL, "truth, psnr and ssim must be non-NULL");
+    if (ctx->counted < 1) return fail(PCA_EINVAL, "finalize needs counted sweeps (mpm_burn_in)");
+    const pca_config& c = ctx->cfg;
+    const uint8_t* dt = nullptr;
+    st = device_input(ctx, truth, &dt);  // host truth -> stage[0, BRW)
+    if (st != PCA_OK) return st;
+    const bool dev_out = mpm_out && is_device_ptr(mpm_out);
+    uint8_t* mo = mpm_out ? (dev_out ? mpm_out : ctx->stage + align256(dense_bytes(ctx))) : nullptr;
+    const size_t nb = (size_t)c.batch * 16 * sizeof(unsigned long long);
+    CK(ctx, cudaMemsetAsync(ctx->sums, 0, nb, ctx->stream));
+    MetricParams mp;
+    mp.geo = ctx->geo;
+    mp.x = ctx->x[ctx->cur];
+    mp.counts = ctx->counts;
+    mp.truth = dt;
+    mp.sums = ctx->sums;
+    mp.kind = 2;
+    mp.nsamp = (int)ctx->counted;
+    mp.mpm_out = mo;
+    LAUNCH(ctx, launch_metric_sums(mp, c.batch, ctx->stream));
+    if (ctx->comm && ctx->nranks > 1) {
+        NcclApi& N = nccl();
+        CK(ctx, cudaMemcpyAsync(ctx->sums_max, ctx->sums, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+        ncclResult_t e = N.AllReduce(ctx->sums, ctx->sums, (size_t)c.batch * 16, ncclUint64, ncclSum,
+                                     ctx->comm, ctx->stream);
+        if (e == ncclSuccess)
+            e = N.AllReduce(ctx->sums_max, ctx->sums_max, (size_t)c.batch * 16, ncclUint64, ncclMax,
+                            ctx->comm, ctx->stream);
+        if (e != ncclSuccess) {
+            ctx->poisoned = 1;
+            return fail(PCA_ENCCL, "finalize all-reduce: %s", N.GetErrorString(e));
+        }
     }
+    std::vector<unsigned long long> h((size_t)c.batch * 16), hm((size_t)c.batch * 16);
+    CK(ctx, cudaMemcpyAsync(h.data(), ctx->sums, nb, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->comm && ctx->nranks > 1)
+        CK(ctx, cudaMemcpyAsync(hm.data(), ctx->sums_max, nb, cudaMemcpyDeviceToHost, ctx->stream));
+    if (mpm_out && !dev_out)
+        CK(ctx, cudaMemcpyAsync(mpm_out, mo, dense_bytes(ctx), cudaMemcpyDeviceToHost, ctx->stream));
+    st = sync(ctx);
+    if (st != PCA_OK) return st;
+    bool black = false;
+    for (int b = 0; b < c.batch; ++b)
+        for (int e = 0; e < 2; ++e) {  // e = 0: LAST, 1: MPM
+            int64_t v[8];
+            for (int k = 0; k < 8; ++k) {
+                unsigned long long x = h[(size_t)b * 16 + 8 * e + k];
+                if (k == 6 && ctx->comm && ctx->nranks > 1) x = hm[(size_t)b * 16 + 8 * e + k];
+                v[k] = (int64_t)x;
+            }
+            if (!metrics_from_sums(v, c.levels, &psnr[2 * b + e], &ssim[2 * b + e])) black = true;
+        }
     if (black) return fail(PCA_EINVAL, "original image is all black: PSNR undefined (R17)");
     return PCA_OK;
 }

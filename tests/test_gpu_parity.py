@@ -104,6 +104,14 @@ def test_config1_free_running_chain(cuda_device, seed):
         assert abs(ssim[0] - s_o) < 1e-9
         sw = ctx.pca_ssim_windowed(truth[None], kind)
         assert abs(sw[0] - orc.ssim_windowed(truth, est, 2)) < 1e-12
+    # the fused finalisation pass: MPM image + LAST and MPM metrics, host and device outputs
+    for out in (np.zeros((1, 64, 64), np.uint8), _to_device(np.zeros((1, 64, 64), np.uint8))):
+        pf, sf = ctx.pca_finalize(truth[None], out)
+        got = out if isinstance(out, np.ndarray) else out.cpu().numpy()
+        assert np.array_equal(got[0], mpm_o)
+        for e, est in enumerate((x_o, mpm_o)):
+            _, p_o, s_o, _ = orc.metrics(truth, est, 2)
+            assert abs(pf[0, e] - p_o) < 1e-9 and abs(sf[0, e] - s_o) < 1e-9
     marg = ctx.estimate(P.EST_MARGINALS)[0]
     assert np.allclose(marg[1], cnt_o[1] / 100.0, atol=1e-6)
     assert np.allclose(marg[0] + marg[1], 1.0, atol=1e-6)
@@ -421,3 +429,13 @@ def test_config5_batch_full_size_sampled_chains(cuda_device):
     cnt = ctx.counts()
     for i, b in enumerate(picks):
         assert np.array_equal(cnt[b], acc[i])
+    # fused finalisation over the whole batch vs the oracle's metrics on the picked chains
+    truth = np.stack([synth.smooth_labels(H, W, L, 7 + (b % 8)) for b in range(B)])
+    mpm = np.zeros((B, H, W), np.uint8)
+    pf, sf = ctx.pca_finalize(truth, mpm)
+    for i, b in enumerate(picks):
+        cnt_o = acc[i].astype(np.uint32)
+        assert np.array_equal(mpm[b], orc.mpm(cnt_o))
+        for e, est in enumerate((x4[b], orc.mpm(cnt_o))):
+            _, p_o, s_o, _ = orc.metrics(truth[b], est, L)
+            assert abs(pf[b, e] - p_o) < 1e-9 and abs(sf[b, e] - s_o) < 1e-9
