@@ -1,0 +1,38 @@
+"""CPU checks of bench.py's contract that need no GPU: the reference arm (the oracle, timed on
+the host) prints one JSON line with the keys the driver reads, and the workload recipe."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.timeout(300)
+def test_reference_arm_prints_one_contract_line():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], cwd=ROOT, capture_output=True, text=True, timeout=280)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert "workload" in d["config"]
+
+
+def test_workloads():
+    sys.path.insert(0, ROOT)
+    import bench
+    w1 = bench.workload(1)
+    assert (w1["H"], w1["W"], w1["rows"], w1["levels"]) == (8192, 8192, 8192, 2)
+    w8 = bench.workload(8)
+    assert (w8["H"], w8["W"], w8["rows"]) == (32768, 32768, 4096)  # config 4 at P = 8
+    assert bench.BYTES_PER_SU == 7
