@@ -184,12 +184,20 @@ pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int
 pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* psnr,
                          double* ssim);
 
+/* Copy the truth image (host or device [batch][rows][width]) into the context on an internal
+ * copy stream, so the transfer overlaps the sweeps enqueued after it; a later pca_finalize
+ * with truth == NULL uses it (and waits for the copy on the device, not the host).  Host
+ * memory must stay valid until that finalize returns (pinned memory makes the copy truly
+ * asynchronous).  Asynchronous. */
+pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth);
+
 /* The end of a run in ONE fused pass over truth, the current state and the counts
  * (SURVEY 8(a) a8 + a9): the MPM image (written to mpm_out, host or device
  * [batch][rows][width], when non-NULL) and PSNR / global SSIM of both the last sample and
  * the MPM estimate, psnr[2*b + 0] / ssim[2*b + 0] for LAST and [2*b + 1] for MPM (each
- * array [batch][2]).  Same definitions and exactness as pca_psnr_ssim; needs counted sweeps;
- * sums are all-reduced over NCCL for row strips.  Synchronises. */
+ * array [batch][2]).  truth == NULL: the image given to pca_stage_truth.  Same definitions and
+ * exactness as pca_psnr_ssim; needs counted sweeps; sums are all-reduced over NCCL for row
+ * strips.  Synchronises. */
 pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
                         double* ssim);
 

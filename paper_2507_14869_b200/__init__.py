@@ -30,6 +30,7 @@ STATUS_NAMES = {0: "PCA_OK", -1: "PCA_EINVAL", -2: "PCA_ESTATE", -3: "PCA_ECUDA"
 # every symbol include/pca.h declares
 EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "pca_sweep",
            "pca_gibbs_sweep", "pca_estimate", "pca_metric_sums", "pca_psnr_ssim", "pca_finalize",
+           "pca_stage_truth",
            "pca_ssim_windowed", "pca_read_state",
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
@@ -96,6 +97,7 @@ def lib():
             "pca_psnr_ssim": (i32, [vp, vp, i32, vp, vp]),
             "pca_ssim_windowed": (i32, [vp, vp, i32, vp]),
             "pca_finalize": (i32, [vp, vp, vp, vp, vp]),
+            "pca_stage_truth": (i32, [vp, vp]),
             "pca_read_state": (i32, [vp, vp]),
             "pca_write_state": (i32, [vp, vp]),
             "pca_read_counts": (i32, [vp, vp]),
@@ -220,9 +222,16 @@ class PcaContext:
                                    s.ctypes.data), "pca_psnr_ssim")
         return p, s
 
+    def pca_stage_truth(self, truth):
+        """Copy the truth on the context's copy stream (overlaps later sweeps); the host buffer
+        must stay alive until the next pca_finalize(None, ...) returns."""
+        self._staged_truth = truth  # keep the host buffer alive
+        _check(lib().pca_stage_truth(self.handle, _ptr(truth)), "pca_stage_truth")
+
     def pca_finalize(self, truth, mpm_out=None):
         """MPM image (into mpm_out when given) and PSNR / SSIM of LAST and MPM in one pass:
-        returns (psnr, ssim), each [batch][2] (column 0 LAST, column 1 MPM)."""
+        returns (psnr, ssim), each [batch][2] (column 0 LAST, column 1 MPM).  truth None:
+        the image staged with pca_stage_truth."""
         p = np.zeros((self.cfg.batch, 2), np.float64)
         s = np.zeros((self.cfg.batch, 2), np.float64)
         _check(lib().pca_finalize(self.handle, _ptr(truth), _ptr(mpm_out), p.ctypes.data,

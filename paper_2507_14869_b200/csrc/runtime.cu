@@ -115,7 +115,7 @@ struct Layout {
     size_t off_gthr = 0, gthr_entries = 0;  // Gibbs uniform-neighbourhood thresholds
     size_t off_bthr = 0;                    // binary PCA thresholds [THR_ENTRIES]
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
-           off_sums_max = 0, off_flag = 0, off_stage = 0;
+           off_sums_max = 0, off_flag = 0, off_stage = 0, off_truth = 0;
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
 };
 
@@ -200,6 +200,7 @@ Layout make_layout(const pca_config* c) {
     L.off_sums_max = o; o = align256(o + B * 16 * sizeof(unsigned long long));
     L.off_flag = o; o = align256(o + 256);
     L.off_stage = o; o = align256(o + L.stage_bytes);
+    L.off_truth = o; o = align256(o + B * R * W);  // staged truth (pca_stage_truth)
     L.total = o;
     return L;
 }
@@ -246,6 +247,11 @@ struct pca_ctx {
     int nranks = 1, rank = 0;
     cudaStream_t side = nullptr;  // interior rows of a strip, overlapping the halo exchange
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // pca_stage_truth: the truth copied on its own stream, overlapping the sweeps
+    uint8_t* truth = nullptr;
+    int truth_staged = 0;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_truth_ready = nullptr, ev_truth_free = nullptr;
 };
 
 namespace {
@@ -661,6 +667,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->sums_max = (unsigned long long*)(ctx->ws + L.off_sums_max);
     ctx->flag = (int*)(ctx->ws + L.off_flag);
     ctx->stage = ctx->ws + L.off_stage;
+    ctx->truth = ctx->ws + L.off_truth;
     ctx->uthr = L.uthr_entries ? (uint32_t*)(ctx->ws + L.off_uthr) : nullptr;
     ctx->uthr_host.resize(L.uthr_entries);
     ctx->gthr = L.gthr_entries ? (uint32_t*)(ctx->ws + L.off_gthr) : nullptr;
@@ -1018,16 +1025,41 @@ pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, doubl
     return PCA_OK;
 }
 
+pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!truth) return fail(PCA_EINVAL, "truth is NULL");
+    if (!ctx->copy) {
+        CK(ctx, cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+        CK(ctx, cudaEventCreateWithFlags(&ctx->ev_truth_ready, cudaEventDisableTiming));
+        CK(ctx, cudaEventCreateWithFlags(&ctx->ev_truth_free, cudaEventDisableTiming));
+        CK(ctx, cudaEventRecord(ctx->ev_truth_free, ctx->stream));
+    }
+    // the previous finalize's read of the buffer comes first
+    CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev_truth_free, 0));
+    CK(ctx, cudaMemcpyAsync(ctx->truth, truth, dense_bytes(ctx), cudaMemcpyDefault, ctx->copy));
+    CK(ctx, cudaEventRecord(ctx->ev_truth_ready, ctx->copy));
+    ctx->truth_staged = 1;
+    return PCA_OK;
+}
+
 pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
                         double* ssim) {
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
-    if (!truth || !psnr || !ssim) return fail(PCA_EINVAL, "truth, psnr and ssim must be non-NULL");
+    if (!psnr || !ssim) return fail(PCA_EINVAL, "psnr and ssim must be non-NULL");
+    if (!truth && !ctx->truth_staged)
+        return fail(PCA_EINVAL, "truth is NULL and no truth was staged (pca_stage_truth)");
     if (ctx->counted < 1) return fail(PCA_EINVAL, "finalize needs counted sweeps (mpm_burn_in)");
     const pca_config& c = ctx->cfg;
     const uint8_t* dt = nullptr;
-    st = device_input(ctx, truth, &dt);  // host truth -> stage[0, BRW)
-    if (st != PCA_OK) return st;
+    if (truth) {
+        st = device_input(ctx, truth, &dt);  // host truth -> stage[0, BRW)
+        if (st != PCA_OK) return st;
+    } else {
+        CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_truth_ready, 0));
+        dt = ctx->truth;
+    }
     const bool dev_out = mpm_out && is_device_ptr(mpm_out);
     uint8_t* mo = mpm_out ? (dev_out ? mpm_out : ctx->stage + align256(dense_bytes(ctx))) : nullptr;
     const size_t nb = (size_t)c.batch * 16 * sizeof(unsigned long long);
@@ -1042,6 +1074,7 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
     mp.nsamp = (int)ctx->counted;
     mp.mpm_out = mo;
     LAUNCH(ctx, launch_metric_sums(mp, c.batch, ctx->stream));
+    if (!truth) CK(ctx, cudaEventRecord(ctx->ev_truth_free, ctx->stream));
     if (ctx->comm && ctx->nranks > 1) {
         NcclApi& N = nccl();
         CK(ctx, cudaMemcpyAsync(ctx->sums_max, ctx->sums, nb, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1256,6 +1289,12 @@ pca_status pca_destroy(pca_ctx* ctx) {
         cudaStreamDestroy(ctx->side);
         cudaEventDestroy(ctx->ev_fork);
         cudaEventDestroy(ctx->ev_join);
+    }
+    if (ctx->copy) {
+        cudaStreamSynchronize(ctx->copy);
+        cudaStreamDestroy(ctx->copy);
+        cudaEventDestroy(ctx->ev_truth_ready);
+        cudaEventDestroy(ctx->ev_truth_free);
     }
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     delete ctx;

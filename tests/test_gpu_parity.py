@@ -112,6 +112,12 @@ def test_config1_free_running_chain(cuda_device, seed):
         for e, est in enumerate((x_o, mpm_o)):
             _, p_o, s_o, _ = orc.metrics(truth, est, 2)
             assert abs(pf[0, e] - p_o) < 1e-9 and abs(sf[0, e] - s_o) < 1e-9
+    # a staged truth (copy stream, overlapping) gives the same result
+    with pytest.raises(P.PcaError, match="staged"):
+        ctx.pca_finalize(None)
+    ctx.pca_stage_truth(truth[None].copy())
+    ps, ss = ctx.pca_finalize(None)
+    assert np.array_equal(ps, pf) and np.array_equal(ss, sf)
     marg = ctx.estimate(P.EST_MARGINALS)[0]
     assert np.allclose(marg[1], cnt_o[1] / 100.0, atol=1e-6)
     assert np.allclose(marg[0] + marg[1], 1.0, atol=1e-6)
