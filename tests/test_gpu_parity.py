@@ -445,3 +445,26 @@ def test_config5_batch_full_size_sampled_chains(cuda_device):
         for e, est in enumerate((x4[b], orc.mpm(cnt_o))):
             _, p_o, s_o, _ = orc.metrics(truth[b], est, L)
             assert abs(pf[b, e] - p_o) < 1e-9 and abs(sf[b, e] - s_o) < 1e-9
+
+
+def test_nccl_loads_and_a_one_rank_communicator_attaches(cuda_device):
+    """The NCCL plumbing of the strip path on the one GPU available: the unique id comes from
+    the dlopen'ed libnccl, a one-rank communicator attaches (ncclCommInitRank) and a context
+    with it sweeps and finalises like one without (one rank has no exchange and no
+    all-reduce partner, so the chain must be unchanged)."""
+    uid = P.pca_nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
+    H, W = 48, 80
+    truth = synth.smooth_labels(H, W, 2, 3)
+    g = synth.degrade(truth, 2, 0.5, 4)
+    cfg = P.make_config(H, W, 2, periodic=True, sigma=0.5, seed=5, mpm_burn_in=0)
+    a = make_ctx(cfg, g)
+    a.pca_attach_nccl(uid, 1, 0)
+    b = make_ctx(cfg, g)
+    for ctx in (a, b):
+        ctx.pca_sweep(7)
+    assert np.array_equal(a.state(), b.state())
+    assert np.array_equal(a.pca_finalize(truth[None])[0], b.pca_finalize(truth[None])[0])
+    with pytest.raises(P.PcaError, match="already"):
+        a.pca_attach_nccl(uid, 1, 0)
+    a.pca_destroy()
