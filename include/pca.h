@@ -76,12 +76,16 @@ enum {
     PCA_EST_CM = 3         /* float32 [batch][rows][width] = sum_k lum(k) count_k / N_samp  */
 };
 
-/* Kernel selection (all give the same chain up to fp64 near-ties). */
+/* Kernel selection (all give the same chain up to fp64 near-ties).  Runs of
+ * sweeps on small contexts (rows x width x batch <= 2^18) execute in one cooperative launch
+ * of the general code whatever the selection (exact integer thresholds for levels == 2). */
 enum {
     PCA_KERNEL_AUTO = 0,    /* BINARY when levels == 2, else GENERAL                        */
-    PCA_KERNEL_GENERAL = 1, /* any levels: integer thresholds where all neighbours agree    */
-                            /* (levels <= 16), else fp64 per-site weights                   */
-    PCA_KERNEL_BINARY = 2   /* levels == 2: SWAR neighbour counts + integer thresholds      */
+    PCA_KERNEL_GENERAL = 1, /* levels == 2: integer thresholds for every site; more levels:  */
+                            /* integer thresholds where all neighbours agree (levels <= 16), */
+                            /* else fp64 per-site weights (log-domain when they overflow)    */
+    PCA_KERNEL_BINARY = 2   /* levels == 2: TMA-staged rows, SWAR neighbour counts, integer  */
+                            /* thresholds                                                    */
 };
 
 typedef struct pca_config {
@@ -162,9 +166,8 @@ pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0);
 /* Enqueue n >= 0 synchronous PCA sweeps t, t+1, ..., t+n-1 (asynchronous).  When the
  * context owns a strip (rows < height) and NCCL is attached, each sweep is followed by
  * the halo exchange with the neighbouring ranks; without NCCL, n must be <= 1 and the
- * caller exchanges halos (pca_halo_ptrs).  Returns PCA_EUNSUPPORTED if a beta stage
- * makes the exponent range exceed 700 (fp64 weight underflow) or if the uint16 MPM
- * counters would overflow (> 65535 counted sweeps). */
+ * caller exchanges halos (pca_halo_ptrs).  Returns PCA_EUNSUPPORTED if the uint16 MPM
+ * counters would overflow (> 65535 counted sweeps) or the sweep index would pass 2^32-1. */
 pca_status pca_sweep(pca_ctx* ctx, int32_t n);
 
 /* Write an estimate of the chain (kind PCA_EST_*) to out (host or device; layout in the
