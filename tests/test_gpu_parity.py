@@ -333,6 +333,20 @@ def test_error_paths(cuda_device):
     black = np.zeros((1, H, W), np.uint8)
     with pytest.raises(P.PcaError):
         ctx.pca_psnr_ssim(black, P.EST_LAST)
+    # finalisation needs counted sweeps; a staged truth needs a non-NULL image
+    with pytest.raises(P.PcaError, match="counted"):
+        ctx.pca_finalize(g[None].copy())
+    with pytest.raises(P.PcaError, match="NULL"):
+        ctx.pca_stage_truth(None)
+    # a row strip without NCCL: one PCA sweep per call, no Gibbs, no windowed SSIM
+    strip = make_ctx(P.make_config(H, W, 2, row0=0, rows=8), g[:8])
+    with pytest.raises(P.PcaError, match="one step"):
+        strip.pca_sweep(2)
+    with pytest.raises(P.PcaError, match="NCCL"):
+        strip.pca_gibbs_sweep(1)
+    # the context stays usable after argument errors (they do not poison it)
+    ctx.pca_sweep(1)
+    assert ctx.pca_get_stats().sweeps_done == 1
 
 
 @pytest.mark.parametrize("kernel", [P.KERNEL_AUTO, P.KERNEL_GENERAL])
