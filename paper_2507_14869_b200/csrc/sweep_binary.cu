@@ -59,7 +59,10 @@ namespace {
 #ifndef PCA_F_CREG
 #define PCA_F_CREG 0
 #endif
-constexpr int SEG_CHUNKS = 32;                         // 16-site chunks per warp segment
+// 16-site chunks per warp segment (one per lane).  Two chunks per lane (1024-column segments,
+// halving the per-row bookkeeping per site) measured 114.6 us per sweep at best (4 x 12):
+// the doubled register window cut occupancy more than it saved.
+constexpr int SEG_CHUNKS = 32;
 constexpr int XROW_BYTES = 16 * SEG_CHUNKS + 32;       // 544: [col0-16, col0+528)
 constexpr int GROW_BYTES = 16 * SEG_CHUNKS;            // 512
 constexpr int CROW_BYTES = 32 * SEG_CHUNKS;            // 1024
