@@ -95,6 +95,10 @@ struct GeneralSweepParams {
     int inertia_p;
     const uint32_t* uthr;
     const uint32_t* bthr;  // levels == 2: the binary thresholds [THR_ENTRIES] (exact path)
+    // 16 < levels <= 64: W0[g][x][s] = D[g][s] I[x][s] and pfx[g][x][k] = sum_{s<=k} W0
+    // (per beta stage); nullptr otherwise
+    const double* w0;
+    const double* pfx;
 };
 
 // Gibbs sampler, one colour class per launch, in place (x_in == x_out): sites of colour k

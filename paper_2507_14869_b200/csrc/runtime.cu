@@ -95,6 +95,9 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // uniform-neighbourhood integer threshold tables (multilevel kernel) up to 16 levels:
 // 16^3 * 15 entries = 240 KiB
 constexpr int UTHR_MAX_LEVELS = 16;
+// above 16 levels (up to 64) the fp64 path uses per-stage tables W0[g][x][s] = D[g][s] I[x][s]
+// and their prefix sums over s, so a site costs O(#distinct neighbour labels), not O(levels)
+constexpr int SPARSE_MAX_LEVELS = 64;
 // lattices up to this many sites (x batch) sweep in runs of one cooperative launch; the
 // environment variable PCA_B200_MULTI_MAX_SITES overrides it (a tuning knob: the chain is the
 // same either way)
@@ -112,6 +115,7 @@ struct Layout {
     size_t xbuf = 0;      // bytes of one x buffer
     size_t gbuf = 0;      // bytes of the g buffer
     size_t off_uthr = 0, uthr_entries = 0;
+    size_t off_sparse = 0, sparse_entries = 0;  // W0 and prefix tables (16 < levels <= 64)
     size_t off_gthr = 0, gthr_entries = 0;  // Gibbs uniform-neighbourhood thresholds
     size_t off_bthr = 0;                    // binary PCA thresholds [THR_ENTRIES]
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
@@ -192,6 +196,9 @@ Layout make_layout(const pca_config* c) {
     L.uthr_entries = c->levels <= UTHR_MAX_LEVELS
                          ? (size_t)c->levels * c->levels * c->levels * (c->levels - 1) : 0;
     L.off_uthr = o; o = align256(o + L.uthr_entries * sizeof(uint32_t));
+    L.sparse_entries = (c->levels > UTHR_MAX_LEVELS && c->levels <= SPARSE_MAX_LEVELS)
+                           ? (size_t)c->levels * c->levels * c->levels : 0;
+    L.off_sparse = o; o = align256(o + 2 * L.sparse_entries * sizeof(double));
     L.gthr_entries = (c->levels > 2 && c->levels <= UTHR_MAX_LEVELS)
                          ? (size_t)c->levels * c->levels * (c->levels - 1) : 0;
     L.off_gthr = o; o = align256(o + L.gthr_entries * sizeof(uint32_t));
@@ -240,7 +247,7 @@ struct pca_ctx {
     BinarySweepParams bin;
     Binary2SweepParams bin2;
     GeneralSweepParams gen;
-    std::vector<double> dtab_host, itab_host;
+    std::vector<double> dtab_host, itab_host, sparse_host;
     std::vector<uint32_t> uthr_host;
     uint32_t* uthr = nullptr;
     ncclComm_t comm = nullptr;
@@ -406,6 +413,27 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
             CK(ctx, cudaMemcpyAsync(ctx->itab, ctx->itab_host.data(),
                                     ctx->itab_host.size() * sizeof(double), cudaMemcpyHostToDevice,
                                     ctx->stream));
+        }
+        if (ctx->lay.sparse_entries) {
+            // W0[g][x][s] = D[g][s] * I[x][s] (I = the inertia factor of this stage) and its
+            // prefix sums over s: the weights of a site with no neighbour carrying s
+            const int L = c.levels;
+            const size_t n3 = ctx->lay.sparse_entries;
+            double* w0 = ctx->sparse_host.data();
+            double* pf = w0 + n3;
+            for (int gl = 0; gl < L; ++gl)
+                for (int xl = 0; xl < L; ++xl) {
+                    double acc = 0.0;
+                    for (int s = 0; s < L; ++s) {
+                        const size_t i = ((size_t)gl * L + xl) * L + s;
+                        const double iw = exp(-cq * inertia_pen(c.inertia_p, xl, s, L));
+                        w0[i] = ctx->dtab_host[(size_t)gl * L + s] * iw;
+                        acc += w0[i];
+                        pf[i] = acc;
+                    }
+                }
+            CK(ctx, cudaMemcpyAsync(const_cast<double*>(m.w0), w0, 2 * n3 * sizeof(double),
+                                    cudaMemcpyHostToDevice, ctx->stream));
         }
         if (ctx->lay.uthr_entries) {
             // uniform neighbourhood (all NB neighbours carry s*): the oracle's per-site law
@@ -670,6 +698,9 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->truth = ctx->ws + L.off_truth;
     ctx->uthr = L.uthr_entries ? (uint32_t*)(ctx->ws + L.off_uthr) : nullptr;
     ctx->uthr_host.resize(L.uthr_entries);
+    ctx->sparse_host.resize(2 * L.sparse_entries);
+    ctx->gen.w0 = L.sparse_entries ? (const double*)(ctx->ws + L.off_sparse) : nullptr;
+    ctx->gen.pfx = L.sparse_entries ? ctx->gen.w0 + L.sparse_entries : nullptr;
     ctx->gthr = L.gthr_entries ? (uint32_t*)(ctx->ws + L.off_gthr) : nullptr;
     ctx->gthr_host.resize(L.gthr_entries);
     ctx->kernel = (cfg->kernel == PCA_KERNEL_AUTO) ? (cfg->levels == 2 ? PCA_KERNEL_BINARY

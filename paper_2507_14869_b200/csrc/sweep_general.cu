@@ -156,6 +156,70 @@ __device__ int decide_fp64(const GeneralSweepParams& p, const double* sA, const 
     return L - 1;
 }
 
+// Many levels (16 < L <= 64): the weights of the labels no neighbour carries are the stage
+// table W0[g][x][s] = D[g][s] I[x][s], with prefix sums pfx[g][x][k].  Only the (at most NB)
+// distinct neighbour labels change the weights, by (A[n_s] - 1) W0[s], so
+//   Z = pfx[L-1] + sum_j corr_j,  F_k = pfx[k] + (sum of corr_j over neighbour labels <= k);
+// the decision walks the segments between neighbour labels in ascending order and
+// binary-searches the prefix table inside the segment that holds u Z: O(NB + log L) per site
+// instead of O(L NB).  Rounding differs from the oracle's sequential sum only in the last
+// bits (the fp64 path's near-tie semantics, R19).  Returns -1 when Z under/overflows.
+template <int NB>
+__device__ int decide_sparse(const GeneralSweepParams& p, const double* sA, const SiteJob& j) {
+    const int L = p.c.geo.levels;
+    const int xi = (int)(j.xg & 0xFFu), gi = (int)((j.xg >> 8) & 0xFFu);
+    const size_t row = ((size_t)gi * L + xi) * L;
+    const double* W0 = p.w0 + row;
+    const double* PF = p.pfx + row;
+    // the smallest neighbour label above `prev` (L when none) and how many neighbours carry it
+    auto next_label = [&](int prev, int& n) {
+        int best = L;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const int v = (int)(((q < 4 ? j.nb_lo : j.nb_hi) >> (8 * (q & 3))) & 0xFFu);
+            best = (v > prev && v < best) ? v : best;  // the sentinel 0xFF >= L never wins
+        }
+        n = 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+            n += (int)((((q < 4 ? j.nb_lo : j.nb_hi) >> (8 * (q & 3))) & 0xFFu) == (uint32_t)best);
+        return best;
+    };
+    double Z = __ldg(PF + L - 1);
+    for (int prev = -1;;) {
+        int n;
+        const int lab = next_label(prev, n);
+        if (lab >= L) break;
+        Z += (sA[n] - 1.0) * __ldg(W0 + lab);
+        prev = lab;
+    }
+    if (!(Z >= 1e-290 && Z <= 1e290)) return -1;
+    const double target = (double)j.r * (1.0 / 4294967296.0) * Z;
+    double C = 0.0;
+    int a = 0;
+    for (int prev = -1;;) {
+        int n;
+        const int lab = next_label(prev, n);
+        // labels a .. min(lab, L-1)-1 carry no neighbour: F_k = PF[k] + C
+        const int b = min(lab, L - 1) - 1;
+        if (b >= a && target < __ldg(PF + b) + C) {
+            int lo = a, hi = b;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (target < __ldg(PF + mid) + C) hi = mid;
+                else lo = mid + 1;
+            }
+            return lo;
+        }
+        if (lab >= L) break;
+        C += (sA[n] - 1.0) * __ldg(W0 + lab);
+        if (lab < L - 1 && target < __ldg(PF + lab) + C) return lab;
+        a = lab + 1;
+        prev = lab;
+    }
+    return L - 1;
+}
+
 // Uniform-neighbourhood thresholds staged in shared memory when the table is small.
 __host__ __device__ constexpr int uthr_smem_entries(int LT) { return (LT > 0 && LT <= 9) ? LT * LT * LT * (LT - 1) : 1; }
 
@@ -352,6 +416,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 for (int i = lane; i < qbase; i += 32) {
                     int w = -1;
                     if (LT > 2) w = decide_fp64_fixed<NB, (LT > 2 ? LT : 3)>(p, sm.A, sm.D, sm.I, jobs[i]);
+                    else if (LT == 0 && p.pfx != nullptr) w = decide_sparse<NB>(p, sm.A, jobs[i]);
                     if (w < 0) w = decide_fp64<NB>(p, sm.A, jobs[i]);
                     res[i] = (uint8_t)w;
                 }

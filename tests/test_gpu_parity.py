@@ -350,7 +350,7 @@ def test_error_paths(cuda_device):
 
 
 @pytest.mark.parametrize("kernel", [P.KERNEL_AUTO, P.KERNEL_GENERAL])
-@pytest.mark.parametrize("levels", [2, 5])
+@pytest.mark.parametrize("levels", [2, 5, 33])
 @pytest.mark.parametrize("extreme", [dict(sigma=0.01), dict(q=1e6), dict(beta0=300.0),
                                      dict(sigma=0.02, q=500.0)])
 def test_lockstep_extreme_parameters(cuda_device, kernel, levels, extreme):
