@@ -482,3 +482,25 @@ def test_nccl_loads_and_a_one_rank_communicator_attaches(cuda_device):
     with pytest.raises(P.PcaError, match="already"):
         a.pca_attach_nccl(uid, 1, 0)
     a.pca_destroy()
+
+
+@pytest.mark.parametrize("L", [2, 5])
+def test_maximum_batch_of_tiny_lattices(cuda_device, L):
+    """batch = 65535 (the grid-z limit) of 3x4 tori: sampled chains vs the oracle."""
+    B, H, W = 65535, 3, 4
+    g = np.random.default_rng(L).integers(0, L, (B, H, W)).astype(np.uint8)
+    cfg = P.make_config(H, W, L, batch=B, neighborhood=8, periodic=True, sigma=0.4, seed=3,
+                        mpm_burn_in=0)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_sweep(2)
+    x2 = ctx.state()
+    ctx.pca_sweep(1)
+    x3 = ctx.state()
+    m = oracle_model(cfg)
+    tally = Tally()
+    for b in (0, 1, 777, 40000, B - 1):
+        ref, mg = orc.pca_sweep(m, x2[b], g[b], beta_of(cfg, 2), cfg.seed, b, 2)
+        tally.add(x3[b], ref, mg)
+    tally.check(allow_rate=False)
+    with pytest.raises(P.PcaError):
+        P.PcaContext(P.make_config(H, W, L, batch=B + 1), np.zeros((B + 1, H, W), np.uint8))
