@@ -109,7 +109,8 @@ struct GeneralSweepParams {
 // A[n] D[g][s] weights (log-domain when they under/overflow).
 struct GibbsSweepParams {
     SweepCommon c;
-    int colour;
+    int colour;   // fused: the row parity (both colours of those rows in one launch)
+    int fused;    // Moore-8 with the two colours of a row in one launch (2 launches a sweep)
     double A[9];
     double coef_a, coef_b;
     const double* dtab;

@@ -900,7 +900,10 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
     const bool strip = ctx->lay.rows < c.height;
     if (strip && !(ctx->comm && ctx->nranks > 1))
         return fail(PCA_EINVAL, "a row-strip Gibbs sweep exchanges halos between colours: attach NCCL");
-    const int ncol = c.neighborhood == 4 ? 2 : 4;
+    // Moore-8: the two colours of a row parity in one launch (2 launches per sweep) when the
+    // right-neighbour recomputation has its columns (free boundary, or 16-column torus pads)
+    const bool fused = c.neighborhood == 8 && (!c.periodic || (c.width % 16) == 0);
+    const int nlaunch = c.neighborhood == 4 ? 2 : (fused ? 2 : 4);
     for (int32_t i = 0; i < n; ++i) {
         const int64_t t = ctx->t;
         if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
@@ -913,9 +916,11 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
         ctx->gib.c.x_out = ctx->x[ctx->cur];  // in place
         ctx->gib.c.rlo = 0;
         ctx->gib.c.rhi = ctx->lay.rows;
-        for (int k = 0; k < ncol; ++k) {
+        ctx->gib.fused = fused ? 1 : 0;
+        for (int k = 0; k < nlaunch; ++k) {
             ctx->gib.colour = k;
-            ctx->gib.c.count_enable = count && (k & 1);  // rows are final after colour 1 / 3
+            // rows are final after colour 1 / 3, or after their fused launch
+            ctx->gib.c.count_enable = count && (fused || (k & 1));
             ctx->launches++;
             ctx->sweep_launches++;
             const int e = launch_sweep_gibbs(ctx->gib, c.batch, ctx->stream);

@@ -102,7 +102,7 @@ __device__ int gibbs_fp64(const GibbsSweepParams& p, const double* sA, const Gib
     return L - 1;
 }
 
-template <int NB, bool BIN>
+template <int NB, bool BIN, bool FUSED>
 __global__ void __launch_bounds__(GB_THREADS, 4) sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
     __shared__ double sA[9];
     __shared__ uint32_t sT[BIN ? GIBBS_THR2 : 1];
@@ -126,10 +126,12 @@ __global__ void __launch_bounds__(GB_THREADS, 4) sweep_gibbs_kernel(const __grid
     const unsigned lt = (1u << lane) - 1u;
     GibbsJob* jobs = s_jobs[warp];
     uint8_t* res = s_res[warp];
-    // rows of this block: Moore-8 visits only rows whose global parity is k >> 1
+    // rows of this block: Moore-8 visits only rows whose global parity is k >> 1 (FUSED: k is
+    // the row parity itself, both colours of the row in one launch)
     const int rstep = NB == 8 ? 2 : 1;
+    const int par = FUSED ? k : (k >> 1);
     int rfirst = p.c.rlo;
-    if (NB == 8 && ((G.row0 + rfirst) & 1) != (k >> 1)) ++rfirst;
+    if (NB == 8 && ((G.row0 + rfirst) & 1) != par) ++rfirst;
     const int rbeg = rfirst + rstep * R * (int)blockIdx.y;
     const int rend = min(rbeg + rstep * R, p.c.rhi);
     if (rbeg >= rend) return;
@@ -160,84 +162,149 @@ __global__ void __launch_bounds__(GB_THREADS, 4) sweep_gibbs_kernel(const __grid
             rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
         }
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+        uint32_t outw = mid[1];  // start from the current labels of the 4 sites
+        // decide the sites in `mask` from the neighbour words (byte b = neighbour of site b)
+        auto decide4 = [&](uint32_t UL, uint32_t UC, uint32_t UR, uint32_t ML, uint32_t MR,
+                           uint32_t DL, uint32_t DC, uint32_t DR, unsigned mask) {
+            if (BIN) {
+                // SWAR over the 4 sites: label-1 neighbours and present neighbours per byte
+                auto one = [](uint32_t w) { return w & ~(w >> 1) & 0x01010101u; };  // 0xFF -> 0
+                auto pres = [](uint32_t w) { return (~w >> 7) & 0x01010101u; };     // 0xFF -> 0
+                uint32_t n1, np;
+                if (NB == 8) {
+                    n1 = one(UL) + one(UC) + one(UR) + one(ML) + one(MR) + one(DL) + one(DC) + one(DR);
+                    np = G.periodic ? 0x08080808u
+                                    : pres(UL) + pres(UC) + pres(UR) + pres(ML) + pres(MR) + pres(DL) + pres(DC) + pres(DR);
+                } else {
+                    n1 = one(UC) + one(ML) + one(MR) + one(DC);
+                    np = G.periodic ? 0x04040404u : pres(UC) + pres(ML) + pres(MR) + pres(DC);
+                }
+                const uint32_t idx4 = ((np * 9u + n1) << 1) | gword;  // (np*9 + n1)*2 + g per byte
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    if ((mask >> b) & 1u) {
+                        const uint32_t w = rr[b] > sT[(idx4 >> (8 * b)) & 0xFFu] ? 1u : 0u;
+                        outw = (outw & ~(0xFFu << (8 * b))) | (w << (8 * b));
+                    }
+                }
+            } else {
+                int qpos[4] = {-1, -1, -1, -1};
+                int qbase = 0;
+                uint32_t D;
+                if (NB == 8)
+                    D = (UL ^ UC) | (UC ^ UR) | (UR ^ ML) | (ML ^ MR) | (MR ^ DL) | (DL ^ DC) | (DC ^ DR);
+                else
+                    D = (UC ^ ML) | (ML ^ MR) | (MR ^ DC);
+                const uint32_t differ = (((D & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | D) & 0x80808080u;
+                const uint32_t S0 = NB == 8 ? UL : UC;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const bool my = (mask >> b) & 1u;
+                    const int gi = (int)((gword >> (8 * b)) & 0xFFu);
+                    const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
+                    const bool uniform = p.uthr != nullptr && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
+                    if (my && uniform) {
+                        const uint32_t* T = p.uthr + (size_t)(s0 * L + gi) * (L - 1);
+                        int w = 0;
+                        for (int kk = 0; kk < L - 1; ++kk) w += (rr[b] > __ldg(T + kk)) ? 1 : 0;
+                        outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)w << (8 * b));
+                    }
+                    const bool need = my && !uniform;
+                    const unsigned m = __ballot_sync(FULL, need);
+                    if (need) {
+                        qpos[b] = qbase + __popc(m & lt);
+                        const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);
+                        GibbsJob jb;
+                        if (NB == 8) {
+                            jb.nb_lo = __byte_perm(__byte_perm(UL, UC, sel), __byte_perm(UR, ML, sel), 0x5410);
+                            jb.nb_hi = __byte_perm(__byte_perm(MR, DL, sel), __byte_perm(DC, DR, sel), 0x5410);
+                        } else {
+                            jb.nb_lo = __byte_perm(__byte_perm(UC, ML, sel), __byte_perm(MR, DC, sel), 0x5410);
+                            jb.nb_hi = 0u;
+                        }
+                        jb.g = (uint32_t)gi;
+                        jb.r = rr[b];
+                        jobs[qpos[b]] = jb;
+                    }
+                    qbase += __popc(m);
+                }
+                if (qbase > 0) {
+                    __syncwarp();
+                    for (int i = lane; i < qbase; i += 32) res[i] = (uint8_t)gibbs_fp64<NB>(p, sA, jobs[i]);
+                    __syncwarp();
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if (qpos[b] >= 0) outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)res[qpos[b]] << (8 * b));
+                    __syncwarp();
+                }
+            }
+        };
+        const unsigned valid = nvalid >= 4 ? 0xFu : ((1u << nvalid) - 1u);
         const uint32_t UL = from_left(up[0], up[1]), UC = up[1], UR = from_right(up[1], up[2]);
         const uint32_t ML = from_left(mid[0], mid[1]), MR = from_right(mid[1], mid[2]);
         const uint32_t DL = from_left(dn[0], dn[1]), DC = dn[1], DR = from_right(dn[1], dn[2]);
-        // sites of colour k in this quad (c0 is a multiple of 4)
-        unsigned mine = NB == 4 ? (((grow + k) & 1) ? 0xAu : 0x5u) : ((k & 1) ? 0xAu : 0x5u);
-        if (nvalid < 4) mine &= (1u << nvalid) - 1u;
-        uint32_t outw = mid[1];  // start from the current labels of the 4 sites
-        int qpos[4] = {-1, -1, -1, -1};
-        int qbase = 0;
-        if (BIN) {
-            // SWAR over the 4 sites: label-1 neighbours and present neighbours per byte
-            auto one = [](uint32_t w) { return w & ~(w >> 1) & 0x01010101u; };  // 0xFF -> 0
-            auto pres = [](uint32_t w) { return (~w >> 7) & 0x01010101u; };     // 0xFF -> 0
-            uint32_t n1, np;
-            if (NB == 8) {
-                n1 = one(UL) + one(UC) + one(UR) + one(ML) + one(MR) + one(DL) + one(DC) + one(DR);
-                np = G.periodic ? 0x08080808u
-                                : pres(UL) + pres(UC) + pres(UR) + pres(ML) + pres(MR) + pres(DL) + pres(DC) + pres(DR);
-            } else {
-                n1 = one(UC) + one(ML) + one(MR) + one(DC);
-                np = G.periodic ? 0x04040404u : pres(UC) + pres(ML) + pres(MR) + pres(DC);
-            }
-            const uint32_t idx4 = ((np * 9u + n1) << 1) | gword;  // (np*9 + n1)*2 + g per byte
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                if ((mine >> b) & 1u) {
-                    const uint32_t w = rr[b] > sT[(idx4 >> (8 * b)) & 0xFFu] ? 1u : 0u;
-                    outw = (outw & ~(0xFFu << (8 * b))) | (w << (8 * b));
-                }
-            }
+        if (!FUSED) {
+            // sites of colour k in this quad (c0 is a multiple of 4)
+            const unsigned mine = (NB == 4 ? (((grow + k) & 1) ? 0xAu : 0x5u) : ((k & 1) ? 0xAu : 0x5u)) & valid;
+            decide4(UL, UC, UR, ML, MR, DL, DC, DR, mine);
         } else {
-            uint32_t D;
-            if (NB == 8)
-                D = (UL ^ UC) | (UC ^ UR) | (UR ^ ML) | (ML ^ MR) | (MR ^ DL) | (DL ^ DC) | (DC ^ DR);
-            else
-                D = (UC ^ ML) | (ML ^ MR) | (MR ^ DC);
-            const uint32_t differ = (((D & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | D) & 0x80808080u;
-            const uint32_t S0 = NB == 8 ? UL : UC;
+            // Moore-8, one row parity per launch: colour 2p (even columns) from the old labels,
+            // then colour 2p+1 (odd columns) from the new even-column labels of the same row
+            // (the rows above and below have the other parity and do not change)
+            decide4(UL, UC, UR, ML, MR, DL, DC, DR, 0x5u & valid);
+            // new label of column c0+4 (colour 2p): from the next lane, or recomputed here when
+            // the next quad belongs to another warp (or wraps around the torus)
+            const uint32_t nb0 = __shfl_down_sync(FULL, outw & 0xFFu, 1);
+            uint32_t v4 = (mid[2] & 0xFFu);  // sentinel 0xFF past a free boundary
+            const bool has_next = c0 + 4 < G.W;
+            const bool wraps = G.periodic && c0 + 4 == G.W;
+            if (active && (has_next || wraps)) {
+                if (lane < 31 && has_next && qd + 1 < nquads) {
+                    v4 = nb0;
+                } else {
+                    // site c0+4 (or column 0 on a torus): neighbours from the window, Philox
+                    // word 0 of its quad, its g
+                    const int qn = wraps ? 0 : qd + 1;
+                    const uint4 rn = philox4x32_10(make_uint4((uint32_t)qn, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+                    const int gn = (int)__ldg(gcol + (long long)(r + GHALO) * G.gpitch + (wraps ? -c0 : 4));
+                    // neighbour bytes of site c0+4: columns c0+3, c0+4, c0+5 of the rows above /
+                    // below and c0+3, c0+5 of this row (old: colour 2p+1 is decided later)
+                    auto b3 = [&](const uint32_t (&w)[3]) { return (w[1] >> 24) & 0xFFu; };
+                    auto b4 = [&](const uint32_t (&w)[3]) { return w[2] & 0xFFu; };
+                    auto b5 = [&](const uint32_t (&w)[3]) { return (w[2] >> 8) & 0xFFu; };
+                    const uint32_t nbs[8] = {b3(up), b4(up), b5(up), b3(mid), b5(mid), b3(dn), b4(dn), b5(dn)};
+                    if (BIN) {
+                        int n1 = 0, np = 0;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const bool my = (mine >> b) & 1u;
-                const int gi = (int)((gword >> (8 * b)) & 0xFFu);
-                const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
-                const bool uniform = p.uthr != nullptr && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
-                if (my && uniform) {
-                    const uint32_t* T = p.uthr + (size_t)(s0 * L + gi) * (L - 1);
-                    int w = 0;
-                    for (int kk = 0; kk < L - 1; ++kk) w += (rr[b] > __ldg(T + kk)) ? 1 : 0;
-                    outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)w << (8 * b));
-                }
-                const bool need = my && !uniform;
-                const unsigned m = __ballot_sync(FULL, need);
-                if (need) {
-                    qpos[b] = qbase + __popc(m & lt);
-                    const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);
-                    GibbsJob jb;
-                    if (NB == 8) {
-                        jb.nb_lo = __byte_perm(__byte_perm(UL, UC, sel), __byte_perm(UR, ML, sel), 0x5410);
-                        jb.nb_hi = __byte_perm(__byte_perm(MR, DL, sel), __byte_perm(DC, DR, sel), 0x5410);
+                        for (int q = 0; q < 8; ++q) {
+                            n1 += nbs[q] == 1u;
+                            np += nbs[q] != 0xFFu;
+                        }
+                        if (G.periodic) np = 8;
+                        v4 = rn.x > sT[(np * 9 + n1) * 2 + gn] ? 1u : 0u;
                     } else {
-                        jb.nb_lo = __byte_perm(__byte_perm(UC, ML, sel), __byte_perm(MR, DC, sel), 0x5410);
-                        jb.nb_hi = 0u;
-                    }
-                    jb.g = (uint32_t)gi;
-                    jb.r = rr[b];
-                    jobs[qpos[b]] = jb;
-                }
-                qbase += __popc(m);
-            }
-            if (qbase > 0) {
-                __syncwarp();
-                for (int i = lane; i < qbase; i += 32) res[i] = (uint8_t)gibbs_fp64<NB>(p, sA, jobs[i]);
-                __syncwarp();
+                        bool uni = p.uthr != nullptr && nbs[0] < (uint32_t)L;
 #pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (qpos[b] >= 0) outw = (outw & ~(0xFFu << (8 * b))) | ((uint32_t)res[qpos[b]] << (8 * b));
-                __syncwarp();
+                        for (int q = 1; q < 8; ++q) uni = uni && nbs[q] == nbs[0];
+                        if (uni) {
+                            const uint32_t* T = p.uthr + (size_t)((int)nbs[0] * L + gn) * (L - 1);
+                            int w = 0;
+                            for (int kk = 0; kk < L - 1; ++kk) w += (rn.x > __ldg(T + kk)) ? 1 : 0;
+                            v4 = (uint32_t)w;
+                        } else {
+                            GibbsJob jb;
+                            jb.nb_lo = nbs[0] | (nbs[1] << 8) | (nbs[2] << 16) | (nbs[3] << 24);
+                            jb.nb_hi = nbs[4] | (nbs[5] << 8) | (nbs[6] << 16) | (nbs[7] << 24);
+                            jb.g = (uint32_t)gn;
+                            jb.r = rn.x;
+                            v4 = (uint32_t)gibbs_fp64<NB>(p, sA, jb);
+                        }
+                    }
+                }
             }
+            const uint32_t MLn = from_left(mid[0], outw);
+            const uint32_t MRn = from_right(outw, (mid[2] & ~0xFFu) | v4);
+            decide4(UL, UC, UR, MLn, MRn, DL, DC, DR, 0xAu & valid);
         }
         if (active) {
             uint8_t* xr = xcol + (long long)(r + HALO) * G.xpitch;
@@ -311,14 +378,14 @@ __global__ void __launch_bounds__(GB_THREADS, 4) sweep_gibbs_kernel(const __grid
     }
 }
 
-template <int NB, bool BIN>
+template <int NB, bool BIN, bool FUSED>
 int launch_gb(const GibbsSweepParams& p, int batch, cudaStream_t s) {
     static int occ = 0, sms = 0;
     if (occ == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_gibbs_kernel<NB, BIN>, GB_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_gibbs_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
         if (occ < 1) occ = 1;
     }
     const Geometry& G = p.c.geo;
@@ -336,7 +403,7 @@ int launch_gb(const GibbsSweepParams& p, int batch, cudaStream_t s) {
         R = (nr + nrb - 1) / nrb;
     }
     dim3 grid((unsigned)xblocks, (unsigned)nrb, batch);
-    sweep_gibbs_kernel<NB, BIN><<<grid, GB_THREADS, 0, s>>>(p, (int)R);
+    sweep_gibbs_kernel<NB, BIN, FUSED><<<grid, GB_THREADS, 0, s>>>(p, (int)R);
     return (int)cudaGetLastError();
 }
 
@@ -346,8 +413,11 @@ int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream) {
     const Geometry& G = p.c.geo;
     cudaStream_t s = (cudaStream_t)stream;
     const bool bin = G.levels == 2;
-    if (G.nbhd == 8) return bin ? launch_gb<8, true>(p, batch, s) : launch_gb<8, false>(p, batch, s);
-    return bin ? launch_gb<4, true>(p, batch, s) : launch_gb<4, false>(p, batch, s);
+    if (G.nbhd == 8) {
+        if (p.fused) return bin ? launch_gb<8, true, true>(p, batch, s) : launch_gb<8, false, true>(p, batch, s);
+        return bin ? launch_gb<8, true, false>(p, batch, s) : launch_gb<8, false, false>(p, batch, s);
+    }
+    return bin ? launch_gb<4, true, false>(p, batch, s) : launch_gb<4, false, false>(p, batch, s);
 }
 
 }  // namespace pcab200

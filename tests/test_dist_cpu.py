@@ -75,9 +75,13 @@ def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q, method="p
                 x = rng.integers(0, levels, (H, W), dtype=np.uint8)  # fresh poison every sweep
                 x[row0:row0 + rows] = new
                 exchange(x)
-            else:  # Gibbs: one colour phase on the strip, then a halo exchange (runtime order)
-                for k in range(4):
-                    new = orc.gibbs_colour_phase(m, x, g, 1.25, 99, 0, t, k, rows=(row0, row0 + rows))
+            else:  # Gibbs (runtime order, Moore-8 fused): the two colours of a row parity on
+                # the strip (no exchange in between: they only meet within a row), then a halo
+                # exchange; twice per sweep
+                for par in range(2):
+                    new = x
+                    for k in (2 * par, 2 * par + 1):
+                        new = orc.gibbs_colour_phase(m, new, g, 1.25, 99, 0, t, k, rows=(row0, row0 + rows))
                     x = rng.integers(0, levels, (H, W), dtype=np.uint8)
                     x[row0:row0 + rows] = new[row0:row0 + rows]
                     exchange(x)
@@ -116,8 +120,9 @@ def test_two_rank_strip_exchange_reproduces_unsharded_chain(periodic):
 
 @pytest.mark.parametrize("periodic", [True, False])
 def test_two_rank_strip_gibbs_reproduces_unsharded_chain(periodic):
-    """pca_gibbs_sweep's strip protocol: every colour phase on the owned rows followed by a
-    halo exchange reproduces the unsharded colour-order scan (even torus sides)."""
+    """pca_gibbs_sweep's strip protocol (Moore-8): the two colours of each row parity on the
+    owned rows, then a halo exchange, reproduces the unsharded colour-order scan (even torus
+    sides)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
