@@ -118,6 +118,17 @@ struct GibbsSweepParams {
     uint32_t thr2[GIBBS_THR2];
 };
 
+// Gibbs, levels == 2, Moore-8, on the binary PCA kernel's data path (sweep_gibbs_binary.cu):
+// one launch per row parity; c.x_in = X (x_t, the updated rows are read from it), x_nb = the
+// buffer holding rows r -+ 1 (X for parity 0, Y for parity 1), c.x_out = Y.
+constexpr int GIBBS_THR_PAD = 164;  // GIBBS_THR2 rounded up to a 16-byte multiple
+struct GibbsBinParams {
+    SweepCommon c;
+    const uint8_t* x_nb;
+    int parity;
+    const uint32_t* thr;  // device [GIBBS_THR_PAD]: the Gibbs thresholds of the stage
+};
+
 struct MetricParams {
     Geometry geo;
     const uint8_t* x;      // padded current state, chain 0 at padded row -HALO
@@ -136,6 +147,7 @@ int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thre
 // cooperative launch, x_in / x_out alternating; the result is in x_in when nsweeps is even.
 int launch_sweep_general(const GeneralSweepParams& p, int batch, int nsweeps, void* stream);
 int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream);
+int launch_gibbs_binary(const GibbsBinParams& p, int batch, void* stream);
 // copy a small host table into device memory through the kernel parameter block (stream
 // ordered, no host synchronisation, no pinned staging buffer to protect)
 constexpr int PARAM_TABLE_MAX = 1024;

@@ -118,6 +118,7 @@ struct Layout {
     size_t off_sparse = 0, sparse_entries = 0;  // W0 and prefix tables (16 < levels <= 64)
     size_t off_gthr = 0, gthr_entries = 0;  // Gibbs uniform-neighbourhood thresholds
     size_t off_bthr = 0;                    // binary PCA thresholds [THR_ENTRIES]
+    size_t off_gbthr = 0;                   // binary Gibbs thresholds [GIBBS_THR_PAD]
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
            off_sums_max = 0, off_flag = 0, off_stage = 0, off_truth = 0;
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
@@ -203,6 +204,7 @@ Layout make_layout(const pca_config* c) {
                          ? (size_t)c->levels * c->levels * (c->levels - 1) : 0;
     L.off_gthr = o; o = align256(o + L.gthr_entries * sizeof(uint32_t));
     L.off_bthr = o; o = align256(o + THR_ENTRIES * sizeof(uint32_t));
+    L.off_gbthr = o; o = align256(o + GIBBS_THR_PAD * sizeof(uint32_t));
     L.off_sums = o; o = align256(o + B * 16 * sizeof(unsigned long long));
     L.off_sums_max = o; o = align256(o + B * 16 * sizeof(unsigned long long));
     L.off_flag = o; o = align256(o + 256);
@@ -241,6 +243,7 @@ struct pca_ctx {
     int64_t tab_stage = -1;
     int64_t gtab_stage = -1;
     GibbsSweepParams gib;
+    GibbsBinParams gbin;
     uint32_t bthr_host[THR_ENTRIES];  // binary thresholds of the current stage (host copy)
     std::vector<uint32_t> gthr_host;
     uint32_t* gthr = nullptr;
@@ -526,6 +529,9 @@ pca_status build_gibbs_tables(pca_ctx* ctx, int64_t t) {
                     const int n[2] = {np - n1, n1};
                     thresholds(n, gl, out);
                 }
+        ParamTable pt;
+        for (int i = 0; i < GIBBS_THR_PAD; ++i) pt.v[i] = i < GIBBS_THR2 ? m.thr2[i] : 0u;
+        LAUNCH(ctx, launch_param_table(pt, GIBBS_THR_PAD, const_cast<uint32_t*>(ctx->gbin.thr), ctx->stream));
     } else if (ctx->lay.gthr_entries) {
         const int NB = c.neighborhood;
         int n[UTHR_MAX_LEVELS];
@@ -741,6 +747,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->bin.thr = (const uint32_t*)(ctx->ws + L.off_bthr);
     ctx->gen.bthr = ctx->bin.thr;
     ctx->gib.dtab = ctx->dtab;
+    ctx->gbin.thr = (const uint32_t*)(ctx->ws + L.off_gbthr);
     ctx->gib.uthr = ctx->gthr;
 
     auto bail = [&](pca_status s) {
@@ -901,8 +908,10 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
     if (strip && !(ctx->comm && ctx->nranks > 1))
         return fail(PCA_EINVAL, "a row-strip Gibbs sweep exchanges halos between colours: attach NCCL");
     // Moore-8: the two colours of a row parity in one launch (2 launches per sweep) when the
-    // right-neighbour recomputation has its columns (free boundary, or 16-column torus pads)
+    // right-neighbour recomputation has its columns (free boundary, or 16-column torus pads);
+    // with two levels on the binary PCA kernel's data path (sweep_gibbs_binary.cu), X -> Y
     const bool fused = c.neighborhood == 8 && (!c.periodic || (c.width % 16) == 0);
+    const bool binpath = fused && c.levels == 2;
     const int nlaunch = c.neighborhood == 4 ? 2 : (fused ? 2 : 4);
     for (int32_t i = 0; i < n; ++i) {
         const int64_t t = ctx->t;
@@ -912,6 +921,29 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
         const int count = (c.mpm_burn_in >= 0 && t >= c.mpm_burn_in) ? 1 : 0;
         if (count && ctx->counted + 1 > 65535)
             return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+        if (binpath) {
+            // X = x[cur] -> Y = x[cur ^ 1]: even rows from X, then odd rows from X and the new
+            // even rows of Y; halos exchanged after each launch on strips
+            fill_common(ctx, ctx->gbin.c, t, count);
+            ctx->gbin.c.rlo = 0;
+            ctx->gbin.c.rhi = ctx->lay.rows;
+            for (int par = 0; par < 2; ++par) {
+                ctx->gbin.parity = par;
+                ctx->gbin.x_nb = par == 0 ? ctx->x[ctx->cur] : ctx->x[ctx->cur ^ 1];
+                ctx->launches++;
+                ctx->sweep_launches++;
+                const int e = launch_gibbs_binary(ctx->gbin, c.batch, ctx->stream);
+                if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep (binary)");
+                if (strip) {
+                    st = exchange(ctx, ctx->x[ctx->cur ^ 1], 1);
+                    if (st != PCA_OK) return st;
+                }
+            }
+            ctx->cur ^= 1;
+            ctx->t = t + 1;
+            ctx->counted += count;
+            continue;
+        }
         fill_common(ctx, ctx->gib.c, t, 0);
         ctx->gib.c.x_out = ctx->x[ctx->cur];  // in place
         ctx->gib.c.rlo = 0;

@@ -127,3 +127,48 @@ def test_gibbs_rejects_odd_torus_and_mixes_with_pca(cuda_device):
         x = orc.gibbs_sweep_coloured(m, x, g, beta_of(cfg, t), 6, 0, t)
     x, _ = orc.pca_sweep(m, x, g, beta_of(cfg, 4), 6, 0, 4)
     assert np.array_equal(ctx.state()[0], x)
+
+
+@pytest.mark.parametrize("per,shape", [(True, (32, 96)), (False, (33, 100)), (True, (6, 16))])
+def test_gibbs_binary_path_counts_and_batch(cuda_device, per, shape):
+    """levels == 2, Moore-8 (the TMA binary Gibbs kernel): free-running chains of a batch with
+    MPM counts equal the oracle's colour-order runs."""
+    H, W = shape
+    B = 3
+    g = np.stack([synth.degrade(synth.smooth_labels(H, W, 2, 10 + b), 2, 0.5, b) for b in range(B)])
+    cfg = P.make_config(H, W, 2, batch=B, periodic=per, sigma=0.5, beta0=1.0, beta_step=0.3,
+                        beta_period=4, seed=21, mpm_burn_in=5)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_gibbs_sweep(13)
+    m = oracle_model(cfg)
+    xs, cs = ctx.state(), ctx.counts()
+    for b in range(B):
+        x_o, cnt_o = orc.gibbs_run(m, g[b], g[b], 13, 1.0, 0.3, 4, 21, chain=b, burn_in=5,
+                                   order="colour")
+        assert np.array_equal(xs[b], x_o)
+        assert np.array_equal(cs[b], cnt_o[1].astype(np.uint16))
+    assert ctx.pca_get_stats().sweep_launches == 2 * 13
+
+
+def test_gibbs_binary_full_size_sampled_rows(cuda_device):
+    """8192^2 Moore-8 torus, two levels: after 2 GPU Gibbs sweeps, sampled even rows are
+    recomputed by the oracle from x_1 (colours 0 and 1), odd rows from x_1 with their new
+    even neighbours (colours 2 and 3)."""
+    H = W = 8192
+    g = synth.degrade(synth.tiled_labels(H, W, 2, seed=3), 2, 0.5, seed=4)
+    cfg = P.make_config(H, W, 2, periodic=True, sigma=0.5, beta0=1.5, beta_step=0.0, seed=9)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_gibbs_sweep(1)
+    x1 = ctx.state()[0]
+    ctx.pca_gibbs_sweep(1)
+    x2 = ctx.state()[0]
+    m = oracle_model(cfg)
+    rng = np.random.default_rng(1)
+    for r in sorted({0, 1, H - 1, H - 2} | set(rng.integers(2, H - 2, 6).tolist())):
+        y = x1.copy()
+        rows = [r] if r % 2 == 0 else [(r - 1) % H, (r + 1) % H, r]
+        for rr in rows:  # even rows first (colours 0, 1), then the odd row (colours 2, 3)
+            ks = (0, 1) if rr % 2 == 0 else (2, 3)
+            for k in ks:
+                y = orc.gibbs_colour_phase(m, y, g, 1.5, cfg.seed, 0, 1, k, rows=(rr, rr + 1))
+        assert np.array_equal(x2[r], y[r]), f"row {r}"
