@@ -216,11 +216,12 @@ pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, d
 /* Enqueue n sweeps of the Gibbs sampler (conditional PAPER.md:417-429,
  * no inertia term) on the same state, schedule, sweep counter t and MPM counts: a
  * systematic scan in checkerboard colour order (4-neighbour: colours (r + c) mod 2;
- * Moore-8: 2 (r mod 2) + (c mod 2); global r), one launch per colour, in place, with the
- * Philox words of tag GIBBS.  The paper's own scan is column-major; the
- * colour order gives another chain with the same stationary law (R21).
- * PCA_EUNSUPPORTED on a torus with odd height or width (the colouring would not be
- * proper); a row strip needs NCCL attached (halos are exchanged after every colour).
+ * Moore-8: 2 (r mod 2) + (c mod 2); global r) with the Philox words of tag GIBBS.  The
+ * paper's own scan is column-major; the colour order gives another chain
+ * with the same stationary law (R21).  Launches: von Neumann-4, one per colour (in
+ * place); Moore-8, one per row parity (both colours of the row), double-buffered for two
+ * levels.  PCA_EUNSUPPORTED on a torus with odd height or width (the colouring would not be
+ * proper); a row strip needs NCCL attached (halos are exchanged after every launch).
  * Asynchronous like pca_sweep. */
 pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n);
 
