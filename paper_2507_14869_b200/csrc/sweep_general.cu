@@ -34,6 +34,11 @@ namespace {
 
 namespace cg = cooperative_groups;
 
+// resident 128-thread blocks per SM the register budget is sized for (measured on C5:
+// 4 -> 262 us, 6 -> 238 us, 8 -> 245 us per sweep)
+#ifndef PCA_GEN_MINB
+#define PCA_GEN_MINB 6
+#endif
 constexpr int GEN_THREADS = 128;
 constexpr int GEN_WARPS = GEN_THREADS / 32;
 constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -494,7 +499,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
 }
 
 template <int NB, int LT>  // LT: levels known at compile time, 0 = any
-__global__ void __launch_bounds__(GEN_THREADS, 4)
+__global__ void __launch_bounds__(GEN_THREADS, PCA_GEN_MINB)
     sweep_general_kernel(const __grid_constant__ GeneralSweepParams p, int R) {
     __shared__ GenSmem<LT> sm;
     gen_load_tables<LT>(p, sm);
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(GEN_THREADS, 4)
 // work).  Work items (x-block, row block, chain) are distributed grid-stride; the double
 // buffer alternates in the kernel.  Same per-site code, same chain.
 template <int NB, int LT>
-__global__ void __launch_bounds__(GEN_THREADS, 4)
+__global__ void __launch_bounds__(GEN_THREADS, PCA_GEN_MINB)
     sweep_multi_kernel(const __grid_constant__ GeneralSweepParams p, int R, int nsweeps, int batch) {
     __shared__ GenSmem<LT> sm;
     gen_load_tables<LT>(p, sm);
