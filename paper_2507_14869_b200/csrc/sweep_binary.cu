@@ -33,14 +33,14 @@ namespace {
 // Ring depth x resident CTAs x where the MPM counts travel, per boundary kind, measured on
 // B200 with tools/tune_variants.py at 8192^2 (us per sweep, MPM on):
 //   torus: counts prefetched into registers one item ahead (stage = x + g rows only),
-//          4 stages x 16 CTAs/SM: 84.8 (counts in the ring, 4 x 12: 86.2; 3 x 20: 94.4;
-//          5 x 16: 94.1; 6 x 14: 97.1; 8 x 12: 93.8)
+//          4 stages x 14 CTAs/SM: 84.3 (4 x 16: 84.8; counts in the ring, 4 x 12: 86.2;
+//          3 x 20: 94.4; 5 x 16: 94.1; 6 x 14: 97.1; 8 x 12: 93.8)
 //   free:  counts in the ring, 4 x 12: 90.8 (registers, 4 x 16: 98.7)
 #ifndef PCA_T_K
 #define PCA_T_K 4
 #endif
 #ifndef PCA_T_CTAS
-#define PCA_T_CTAS 16
+#define PCA_T_CTAS 14  // 14 (84.3 us, MPM off 76.1) edged out 16 (85.1, 78.5) and 18 (97.8)
 #endif
 #ifndef PCA_T_CREG
 #define PCA_T_CREG 1
