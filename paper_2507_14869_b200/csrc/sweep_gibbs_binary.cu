@@ -24,8 +24,16 @@
 namespace pcab200 {
 namespace {
 
-constexpr int GK = 4;                          // ring depth (items of 2 x rows)
-constexpr int GCTAS = 12;                      // resident one-warp CTAs per SM
+// ring depth x resident CTAs, measured at 8192^2 (us per sweep): 3 x 16: 135.5; 3 x 18: 136.9;
+// 3 x 20: 137.7; 4 x 12: 142.8; 4 x 16: 143.2; 2 x 24: 142.3; 6 x 12: 168.2
+#ifndef PCA_GB_K
+#define PCA_GB_K 3
+#endif
+#ifndef PCA_GB_CTAS
+#define PCA_GB_CTAS 16
+#endif
+constexpr int GK = PCA_GB_K;                   // ring depth (items of 2 x rows)
+constexpr int GCTAS = PCA_GB_CTAS;             // resident one-warp CTAs per SM
 constexpr int SEG = 32;                        // 16-site chunks per segment
 constexpr int XROW = 16 * SEG + 32;            // 544: [col0-16, col0+528)
 constexpr int GROWB = 16 * SEG;                // 512
