@@ -28,6 +28,9 @@
 namespace pcab200 {
 namespace {
 
+#ifndef PCA_GB_MINB
+#define PCA_GB_MINB 6  // blocks per SM the register budget is sized for (8192^2 l=5: 4 -> 1465, 6 -> 1265, 8 -> 1324 us)
+#endif
 constexpr int GB_THREADS = 128;
 constexpr int GB_WARPS = GB_THREADS / 32;
 constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -103,7 +106,7 @@ __device__ int gibbs_fp64(const GibbsSweepParams& p, const double* sA, const Gib
 }
 
 template <int NB, bool BIN, bool FUSED>
-__global__ void __launch_bounds__(GB_THREADS, 4) sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
+__global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB) sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
     __shared__ double sA[9];
     __shared__ uint32_t sT[BIN ? GIBBS_THR2 : 1];
     __shared__ GibbsJob s_jobs[GB_WARPS][64];
