@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(TPB) metric_sums_kernel(const MetricParams p) 
     unsigned long long s[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) s[k] = 0;
-    uint32_t mx = 0;
+    uint32_t mx4 = 0;  // bytewise max of the truth
     if (n > 0) {
         for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
             const uint4 tv = load16(truth + (long long)r * G.W, c0, n, vec);
@@ -225,28 +225,44 @@ __global__ void __launch_bounds__(TPB) metric_sums_kernel(const MetricParams p) 
                 yv[0] = p.kind == 0 ? load16(xb + (long long)(r + HALO) * G.xpitch + XOFF, c0, n, true)
                                     : mpm16(G, cc, r, c0, p.nsamp);
             }
-            uint32_t t[NS];  // 16 sites: every partial sum < 2^21
+            // 16 sites by 4-byte dot products (IDP.4A); bytes past the row are masked to 0 in
+            // both images and add nothing.  sum (x-y)^2 = sum x^2 + sum y^2 - 2 sum xy, exactly.
+            uint32_t msk[4] = {~0u, ~0u, ~0u, ~0u};
+            if (n < 16) {
 #pragma unroll
-            for (int k = 0; k < NS; ++k) t[k] = 0;
-            for (int j = 0; j < n; ++j) {
-                const uint32_t x = byte_of(tv, j);
-                mx = x > mx ? x : mx;
-#pragma unroll
-                for (int e = 0; e < (BOTH ? 2 : 1); ++e) {
-                    const uint32_t y = byte_of(yv[e], j);
-                    const int d = (int)x - (int)y;
-                    t[6 * e + 0] += (uint32_t)(d * d);
-                    t[6 * e + 1] += x;
-                    t[6 * e + 2] += y;
-                    t[6 * e + 3] += x * x;
-                    t[6 * e + 4] += y * y;
-                    t[6 * e + 5] += x * y;
+                for (int i = 0; i < 4; ++i) {
+                    const int vb = min(max(n - 4 * i, 0), 4);
+                    msk[i] = vb == 4 ? ~0u : ((1u << (8 * vb)) - 1u);
                 }
             }
+            const uint32_t tw[4] = {tv.x & msk[0], tv.y & msk[1], tv.z & msk[2], tv.w & msk[3]};
+            uint32_t sx = 0, sxx = 0;
 #pragma unroll
-            for (int k = 0; k < NS; ++k) s[k] += t[k];
+            for (int i = 0; i < 4; ++i) {
+                sx = __dp4a(tw[i], 0x01010101u, sx);
+                sxx = __dp4a(tw[i], tw[i], sxx);
+                mx4 = __vmaxu4(mx4, tw[i]);
+            }
+#pragma unroll
+            for (int e = 0; e < (BOTH ? 2 : 1); ++e) {
+                const uint32_t yw[4] = {yv[e].x & msk[0], yv[e].y & msk[1], yv[e].z & msk[2], yv[e].w & msk[3]};
+                uint32_t sy = 0, syy = 0, sxy = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    sy = __dp4a(yw[i], 0x01010101u, sy);
+                    syy = __dp4a(yw[i], yw[i], syy);
+                    sxy = __dp4a(tw[i], yw[i], sxy);
+                }
+                s[6 * e + 0] += sxx + syy - 2u * sxy;
+                s[6 * e + 1] += sx;
+                s[6 * e + 2] += sy;
+                s[6 * e + 3] += sxx;
+                s[6 * e + 4] += syy;
+                s[6 * e + 5] += sxy;
+            }
         }
     }
+    uint32_t mx = max(max(mx4 & 0xFFu, (mx4 >> 8) & 0xFFu), max((mx4 >> 16) & 0xFFu, mx4 >> 24));
     __shared__ unsigned long long red[TPB / 32][NS + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
