@@ -148,6 +148,7 @@ int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thre
 int launch_sweep_general(const GeneralSweepParams& p, int batch, int nsweeps, void* stream);
 int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream);
 int launch_gibbs_binary(const GibbsBinParams& p, int batch, void* stream);
+
 // copy a small host table into device memory through the kernel parameter block (stream
 // ordered, no host synchronisation, no pinned staging buffer to protect)
 constexpr int PARAM_TABLE_MAX = 1024;

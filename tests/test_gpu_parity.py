@@ -25,6 +25,8 @@ SHAPES = [
     (1, 77, 2, 8, False), (77, 1, 2, 8, False), (3, 3, 2, 8, True), (5, 17, 2, 8, False),
     (33, 47, 3, 8, False), (40, 130, 5, 8, False), (29, 61, 9, 4, True), (31, 45, 33, 8, False),
     (9, 23, 255, 8, True), (2, 2, 3, 8, False), (1, 1, 5, 8, False),
+    # W % 16 == 0 with 3, 5, 9 levels: the general sweep's TMA path (several segments, ragged)
+    (21, 48, 3, 8, True), (37, 1040, 5, 8, False), (30, 64, 9, 4, True), (5, 16, 5, 8, False),
 ]
 
 
@@ -53,7 +55,8 @@ def test_lockstep_inertia_extremes(cuda_device, q):
 
 @pytest.mark.parametrize("inertia_p", [1, 2])
 @pytest.mark.parametrize("shape", [(40, 130, 5, 8, False), (29, 61, 9, 4, True),
-                                   (31, 45, 33, 8, False), (33, 47, 2, 8, True)],
+                                   (31, 45, 33, 8, False), (33, 47, 2, 8, True),
+                                   (24, 528, 5, 8, True), (18, 64, 9, 8, False)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("q", [0.51, 4.0, 1e6])
 def test_lockstep_l1_l2_inertia(cuda_device, inertia_p, shape, q):
