@@ -343,7 +343,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_oracle(wl, truth, g, rows=wl["rows"], sweeps=2)
+        cpu = cpu_baseline_oracle(wl, truth, g, rows=wl["rows"], sweeps=3)  # ~14 s of CPU work
 
     if rank == 0:
         line = {
