@@ -507,3 +507,25 @@ def test_maximum_batch_of_tiny_lattices(cuda_device, L):
     tally.check(allow_rate=False)
     with pytest.raises(P.PcaError):
         P.PcaContext(P.make_config(H, W, L, batch=B + 1), np.zeros((B + 1, H, W), np.uint8))
+
+
+@pytest.mark.parametrize("L,nb,per,ip", [(5, 8, False, 0), (3, 4, True, 2), (33, 8, False, 1),
+                                         (2, 8, True, 0)])
+def test_multi_sweep_launches_free_running_vs_oracle(cuda_device, L, nb, per, ip):
+    """Small lattices run runs of sweeps in one cooperative launch (sweep_multi_kernel); the
+    runs split at beta stages and at the burn-in.  Free-running against the oracle's chain:
+    states and counts identical (no near-tie on these inputs)."""
+    H, W = 24, 40
+    truth = synth.smooth_labels(H, W, L, seed=L)
+    g = synth.degrade(truth, L, 0.3, seed=L + 1)
+    cfg = P.make_config(H, W, L, neighborhood=nb, periodic=per, sigma=0.3, beta0=1.0,
+                        beta_step=0.25, beta_period=7, seed=41, mpm_burn_in=11, inertia_p=ip)
+    ctx = make_ctx(cfg, g)
+    ctx.pca_sweep(30)
+    st = ctx.pca_get_stats()
+    assert st.sweeps_done == 30 and st.counted_sweeps == 19
+    assert st.sweep_launches < 30  # runs, not single sweeps
+    x_o, cnt_o = orc.pca_run(oracle_model(cfg), g, g, 30, 1.0, 0.25, 7, 41, burn_in=11)
+    assert np.array_equal(ctx.state()[0], x_o)
+    c = ctx.counts()[0]
+    assert np.array_equal(c, (cnt_o[1] if L == 2 else cnt_o).astype(np.uint16))
