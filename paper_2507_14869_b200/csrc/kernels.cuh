@@ -146,7 +146,9 @@ int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thre
 // nsweeps > 1: consecutive sweeps t .. t+nsweeps-1 (same tables and counting) in one
 // cooperative launch, x_in / x_out alternating; the result is in x_in when nsweeps is even.
 int launch_sweep_general(const GeneralSweepParams& p, int batch, int nsweeps, void* stream);
-int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream);
+// nsweeps > 1: that many Gibbs sweeps (one beta stage, c.count_enable = counting for the run,
+// c.t = first sweep) in one cooperative launch, in place (small lattices)
+int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, int nsweeps, void* stream);
 int launch_gibbs_binary(const GibbsBinParams& p, int batch, void* stream);
 
 // copy a small host table into device memory through the kernel parameter block (stream

@@ -913,6 +913,8 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
     const bool fused = c.neighborhood == 8 && (!c.periodic || (c.width % 16) == 0);
     const bool binpath = fused && c.levels == 2;
     const int nlaunch = c.neighborhood == 4 ? 2 : (fused ? 2 : 4);
+    // small lattices: runs of sweeps in one cooperative launch (in place, the quad kernel)
+    const bool small = !strip && (size_t)ctx->lay.rows * c.width * c.batch <= multi_max_sites();
     for (int32_t i = 0; i < n; ++i) {
         const int64_t t = ctx->t;
         if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
@@ -921,6 +923,28 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
         const int count = (c.mpm_burn_in >= 0 && t >= c.mpm_burn_in) ? 1 : 0;
         if (count && ctx->counted + 1 > 65535)
             return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+        if (small && n - i >= 2) {
+            int64_t run = n - i;
+            run = std::min<int64_t>(run, c.beta_period - t % c.beta_period);
+            if (c.mpm_burn_in >= 0 && t < c.mpm_burn_in) run = std::min<int64_t>(run, c.mpm_burn_in - t);
+            run = std::min<int64_t>(run, (int64_t)0xFFFFFFFFLL - t);
+            if (count) run = std::min<int64_t>(run, 65535 - ctx->counted);
+            if (run >= 2) {
+                fill_common(ctx, ctx->gib.c, t, count);
+                ctx->gib.c.x_out = ctx->x[ctx->cur];  // in place
+                ctx->gib.c.rlo = 0;
+                ctx->gib.c.rhi = ctx->lay.rows;
+                ctx->gib.fused = fused ? 1 : 0;
+                ctx->launches++;
+                ctx->sweep_launches++;
+                const int e = launch_sweep_gibbs(ctx->gib, c.batch, (int)run, ctx->stream);
+                if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep (multi-sweep launch)");
+                ctx->t = t + run;
+                ctx->counted += count * run;
+                i += (int32_t)run - 1;
+                continue;
+            }
+        }
         if (binpath) {
             // X = x[cur] -> Y = x[cur ^ 1]: even rows from X, then odd rows from X and the new
             // even rows of Y; halos exchanged after each launch on strips
@@ -955,7 +979,7 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
             ctx->gib.c.count_enable = count && (fused || (k & 1));
             ctx->launches++;
             ctx->sweep_launches++;
-            const int e = launch_sweep_gibbs(ctx->gib, c.batch, ctx->stream);
+            const int e = launch_sweep_gibbs(ctx->gib, c.batch, 1, ctx->stream);
             if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep");
             if (strip) {
                 st = exchange(ctx, ctx->x[ctx->cur], 1);

@@ -20,6 +20,7 @@
 // launch changes, so concurrent readers see the same neighbour labels either way.  MPM counts
 // are taken in the launch after which a row is final (colours 1 and 3), with fire-and-forget
 // 64-bit reductions.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -27,6 +28,8 @@
 
 namespace pcab200 {
 namespace {
+
+namespace cg = cooperative_groups;
 
 #ifndef PCA_GB_MINB
 #define PCA_GB_MINB 6  // blocks per SM the register budget is sized for (8192^2 l=5: 4 -> 1465, 6 -> 1265, 8 -> 1324 us)
@@ -105,37 +108,39 @@ __device__ int gibbs_fp64(const GibbsSweepParams& p, const double* sA, const Gib
     return L - 1;
 }
 
-template <int NB, bool BIN, bool FUSED>
-__global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB) sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
-    __shared__ double sA[9];
-    __shared__ uint32_t sT[BIN ? GIBBS_THR2 : 1];
-    __shared__ GibbsJob s_jobs[GB_WARPS][64];
-    __shared__ uint8_t s_res[GB_WARPS][64];
-    if (threadIdx.x < 9) sA[threadIdx.x] = p.A[threadIdx.x];
-    if (BIN)
-        for (int i = threadIdx.x; i < GIBBS_THR2; i += GB_THREADS) sT[i] = p.thr2[i];
-    __syncthreads();
+struct GibbsSmem {
+    double A[9];
+    uint32_t T[GIBBS_THR2];
+    GibbsJob jobs[GB_WARPS][64];
+    uint8_t res[GB_WARPS][64];
+};
 
+// One launch's work for x-block xb, row block rb of chain `chain`: colour k (FUSED: row parity
+// k), sweep t.  COH: x is read through L2 (ld.global.cg) because earlier phases of the same
+// cooperative launch wrote it.
+template <int NB, bool BIN, bool FUSED, bool COH>
+__device__ __forceinline__ void gibbs_rows(const GibbsSweepParams& p, GibbsSmem& sm, int k, uint32_t t,
+                                           int count_enable, int xb, int rb, int chain, int R) {
+    const double* sA = sm.A;
+    const uint32_t* sT = sm.T;
     const Geometry& G = p.c.geo;
     const int L = G.levels;
-    const int k = p.colour;
     const int nquads = (G.W + 3) >> 2;
-    const int qd = blockIdx.x * GB_THREADS + threadIdx.x;
+    const int qd = xb * GB_THREADS + threadIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int chain = blockIdx.z;
     const bool active = qd < nquads;
     if (__ballot_sync(FULL, active) == 0) return;
     const uint32_t tagchain = (TAG_GIBBS << 24) | (p.c.chain0 + (uint32_t)chain);
     const unsigned lt = (1u << lane) - 1u;
-    GibbsJob* jobs = s_jobs[warp];
-    uint8_t* res = s_res[warp];
+    GibbsJob* jobs = sm.jobs[warp];
+    uint8_t* res = sm.res[warp];
     // rows of this block: Moore-8 visits only rows whose global parity is k >> 1 (FUSED: k is
     // the row parity itself, both colours of the row in one launch)
     const int rstep = NB == 8 ? 2 : 1;
     const int par = FUSED ? k : (k >> 1);
     int rfirst = p.c.rlo;
     if (NB == 8 && ((G.row0 + rfirst) & 1) != par) ++rfirst;
-    const int rbeg = rfirst + rstep * R * (int)blockIdx.y;
+    const int rbeg = rfirst + rstep * R * rb;
     const int rend = min(rbeg + rstep * R, p.c.rhi);
     if (rbeg >= rend) return;
     const int c0 = 4 * qd;
@@ -145,9 +150,15 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB) sweep_gibbs_kernel(co
     auto load_row = [&](int r, uint32_t (&w)[3]) {
         if (!active) return;
         const uint8_t* xr = xcol + (long long)(r + HALO) * G.xpitch;
-        w[0] = ld4(xr - 4);
-        w[1] = ld4(xr);
-        w[2] = ld4(xr + 4);
+        if (COH) {
+            w[0] = __ldcg(reinterpret_cast<const uint32_t*>(xr - 4));
+            w[1] = __ldcg(reinterpret_cast<const uint32_t*>(xr));
+            w[2] = __ldcg(reinterpret_cast<const uint32_t*>(xr + 4));
+        } else {
+            w[0] = ld4(xr - 4);
+            w[1] = ld4(xr);
+            w[2] = ld4(xr + 4);
+        }
     };
     // rolling window; the rows a launch reads around its rows never change in the launch
     // (4-neighbour: only the other colour's bytes are used; Moore-8: the other row parity)
@@ -162,7 +173,7 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB) sweep_gibbs_kernel(co
         uint4 rnd = make_uint4(0, 0, 0, 0);
         if (active) {
             gword = __ldg(reinterpret_cast<const uint32_t*>(gcol + (long long)(r + GHALO) * G.gpitch));
-            rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+            rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, t, tagchain), p.c.keys);
         }
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
         uint32_t outw = mid[1];  // start from the current labels of the 4 sites
@@ -268,7 +279,7 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB) sweep_gibbs_kernel(co
                     // site c0+4 (or column 0 on a torus): neighbours from the window, Philox
                     // word 0 of its quad, its g
                     const int qn = wraps ? 0 : qd + 1;
-                    const uint4 rn = philox4x32_10(make_uint4((uint32_t)qn, (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+                    const uint4 rn = philox4x32_10(make_uint4((uint32_t)qn, (uint32_t)grow, t, tagchain), p.c.keys);
                     const int gn = (int)__ldg(gcol + (long long)(r + GHALO) * G.gpitch + (wraps ? -c0 : 4));
                     // neighbour bytes of site c0+4: columns c0+3, c0+4, c0+5 of the rows above /
                     // below and c0+3, c0+5 of this row (old: colour 2p+1 is decided later)
@@ -329,7 +340,7 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB) sweep_gibbs_kernel(co
                 if (r < HALO) store(xr + (long long)G.rows * G.xpitch);
                 if (r >= G.rows - HALO) store(xr - (long long)G.rows * G.xpitch);
             }
-            if (p.c.count_enable) {  // the row is final after this colour (1 or 3)
+            if (count_enable) {  // the row is final after this colour (1 or 3) / parity launch
                 uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
                 if (nvalid == 4) {
                     if (L == 2) {
@@ -382,14 +393,58 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB) sweep_gibbs_kernel(co
 }
 
 template <int NB, bool BIN, bool FUSED>
-int launch_gb(const GibbsSweepParams& p, int batch, cudaStream_t s) {
-    static int occ = 0, sms = 0;
+__global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
+    sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
+    __shared__ GibbsSmem sm;
+    if (threadIdx.x < 9) sm.A[threadIdx.x] = p.A[threadIdx.x];
+    if (BIN)
+        for (int i = threadIdx.x; i < GIBBS_THR2; i += GB_THREADS) sm.T[i] = p.thr2[i];
+    __syncthreads();
+    gibbs_rows<NB, BIN, FUSED, false>(p, sm, p.colour, p.c.t, p.c.count_enable, blockIdx.x,
+                                      blockIdx.y, blockIdx.z, R);
+}
+
+// Small lattices: `nsweeps` Gibbs sweeps (one beta stage; p.c.count_enable = counting in the
+// whole run) in one cooperative launch, every colour phase followed by a grid barrier.
+template <int NB, bool BIN, bool FUSED>
+__global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
+    gibbs_multi_kernel(const __grid_constant__ GibbsSweepParams p, int R, int nrb, int nsweeps, int batch) {
+    __shared__ GibbsSmem sm;
+    if (threadIdx.x < 9) sm.A[threadIdx.x] = p.A[threadIdx.x];
+    if (BIN)
+        for (int i = threadIdx.x; i < GIBBS_THR2; i += GB_THREADS) sm.T[i] = p.thr2[i];
+    __syncthreads();
+    const int xblocks = (((p.c.geo.W + 3) >> 2) + GB_THREADS - 1) / GB_THREADS;
+    const int items = xblocks * nrb * batch;
+    const int nph = (NB == 4 || FUSED) ? 2 : 4;
+    for (int sw = 0; sw < nsweeps; ++sw) {
+        for (int k = 0; k < nph; ++k) {
+            const int cnt = p.c.count_enable && (FUSED || (k & 1));
+            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+                const int xb = it % xblocks, rb = (it / xblocks) % nrb, chain = it / (xblocks * nrb);
+                gibbs_rows<NB, BIN, FUSED, true>(p, sm, k, p.c.t + (uint32_t)sw, cnt, xb, rb, chain, R);
+            }
+            if (gridDim.x == 1) {
+                __syncthreads();
+            } else {
+                __threadfence();
+                cg::this_grid().sync();
+            }
+        }
+    }
+}
+
+template <int NB, bool BIN, bool FUSED>
+int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s) {
+    static int occ = 0, mocc = 0, sms = 0;
     if (occ == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_gibbs_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, gibbs_multi_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
         if (occ < 1) occ = 1;
+        if (mocc < 1) mocc = 1;
     }
     const Geometry& G = p.c.geo;
     const int nquads = (G.W + 3) / 4;
@@ -397,13 +452,23 @@ int launch_gb(const GibbsSweepParams& p, int batch, cudaStream_t s) {
     if (G.nbhd == 8) nr = (nr + 1) / 2;  // rows of one parity
     if (nr <= 0) return 0;
     const long long xblocks = (nquads + GB_THREADS - 1) / GB_THREADS;
-    const long long target = 4LL * sms * occ;
+    const long long target = nsweeps > 1 ? (long long)sms * mocc : 4LL * sms * occ;
     long long R = ((long long)nr * xblocks * batch + target - 1) / target;
     if (R < 1) R = 1;
     long long nrb = (nr + R - 1) / R;
     if (nrb > 65535) {
         nrb = 65535;
         R = (nr + nrb - 1) / nrb;
+    }
+    if (nsweeps > 1) {
+        const long long items = xblocks * nrb * batch;
+        const long long slots = (long long)sms * mocc;
+        const int grid = (int)(items < slots ? items : slots);
+        GibbsSweepParams pp = p;
+        int Ri = (int)R, nrbi = (int)nrb, ns = nsweeps, b = batch;
+        void* args[] = {&pp, &Ri, &nrbi, &ns, &b};
+        return (int)cudaLaunchCooperativeKernel((const void*)gibbs_multi_kernel<NB, BIN, FUSED>, dim3(grid),
+                                                dim3(GB_THREADS), args, 0, s);
     }
     dim3 grid((unsigned)xblocks, (unsigned)nrb, batch);
     sweep_gibbs_kernel<NB, BIN, FUSED><<<grid, GB_THREADS, 0, s>>>(p, (int)R);
@@ -412,15 +477,16 @@ int launch_gb(const GibbsSweepParams& p, int batch, cudaStream_t s) {
 
 }  // namespace
 
-int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, void* stream) {
+int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, int nsweeps, void* stream) {
     const Geometry& G = p.c.geo;
     cudaStream_t s = (cudaStream_t)stream;
     const bool bin = G.levels == 2;
     if (G.nbhd == 8) {
-        if (p.fused) return bin ? launch_gb<8, true, true>(p, batch, s) : launch_gb<8, false, true>(p, batch, s);
-        return bin ? launch_gb<8, true, false>(p, batch, s) : launch_gb<8, false, false>(p, batch, s);
+        if (p.fused)
+            return bin ? launch_gb<8, true, true>(p, batch, nsweeps, s) : launch_gb<8, false, true>(p, batch, nsweeps, s);
+        return bin ? launch_gb<8, true, false>(p, batch, nsweeps, s) : launch_gb<8, false, false>(p, batch, nsweeps, s);
     }
-    return bin ? launch_gb<4, true, false>(p, batch, s) : launch_gb<4, false, false>(p, batch, s);
+    return bin ? launch_gb<4, true, false>(p, batch, nsweeps, s) : launch_gb<4, false, false>(p, batch, nsweeps, s);
 }
 
 }  // namespace pcab200

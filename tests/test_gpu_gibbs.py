@@ -139,7 +139,8 @@ def test_gibbs_binary_path_counts_and_batch(cuda_device, per, shape):
     cfg = P.make_config(H, W, 2, batch=B, periodic=per, sigma=0.5, beta0=1.0, beta_step=0.3,
                         beta_period=4, seed=21, mpm_burn_in=5)
     ctx = make_ctx(cfg, g)
-    ctx.pca_gibbs_sweep(13)
+    for _ in range(13):  # one sweep per call: the per-sweep launches (runs would go multi-sweep)
+        ctx.pca_gibbs_sweep(1)
     m = oracle_model(cfg)
     xs, cs = ctx.state(), ctx.counts()
     for b in range(B):
