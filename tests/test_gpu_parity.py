@@ -336,6 +336,9 @@ def test_error_paths(cuda_device):
     black = np.zeros((1, H, W), np.uint8)
     with pytest.raises(P.PcaError):
         ctx.pca_psnr_ssim(black, P.EST_LAST)
+    # the estimate equal to the truth: MSE 0, PSNR +inf, SSIM 1
+    p_eq, s_eq = ctx.pca_psnr_ssim(ctx.state(), P.EST_LAST)
+    assert math.isinf(p_eq[0]) and p_eq[0] > 0 and abs(s_eq[0] - 1.0) < 1e-15
     # finalisation needs counted sweeps; a staged truth needs a non-NULL image
     with pytest.raises(P.PcaError, match="counted"):
         ctx.pca_finalize(g[None].copy())
