@@ -173,3 +173,26 @@ def test_gibbs_binary_full_size_sampled_rows(cuda_device):
             for k in ks:
                 y = orc.gibbs_colour_phase(m, y, g, 1.5, cfg.seed, 0, 1, k, rows=(rr, rr + 1))
         assert np.array_equal(x2[r], y[r]), f"row {r}"
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_gibbs_randomised_configurations_lockstep(cuda_device, case):
+    """Random shapes (even sides on a torus), levels, neighbourhoods, schedules and batches:
+    3 Gibbs sweeps in lockstep with the oracle's colour order, exact."""
+    rng = np.random.default_rng(777 + case)
+    L = int(rng.choice([2, 2, 3, 5, 9, 33]))
+    nb = int(rng.choice([4, 8]))
+    per = bool(rng.integers(2))
+    H = int(rng.integers(2, 40)) * (2 if per else 1) + (0 if per else int(rng.integers(0, 2)))
+    W = int(rng.integers(2, 300)) * (2 if per else 1) + (0 if per else int(rng.integers(0, 2)))
+    if rng.integers(3) == 0:
+        W = 16 * int(rng.integers(1, 40))  # the fused / TMA paths
+    H = max(H, 4 if per else 1)
+    B = int(rng.integers(1, 3))
+    cfg = P.make_config(H, W, L, batch=B, neighborhood=nb, periodic=per,
+                        sigma=float(rng.uniform(0.1, 0.6)), beta0=float(rng.uniform(0.5, 2.5)),
+                        beta_step=float(rng.uniform(0, 0.5)), beta_period=2,
+                        seed=int(rng.integers(1 << 30)), chain0=int(rng.integers(0, 99)))
+    g = np.stack([synth.random_labels((H, W), L, seed=case * 7 + b) for b in range(B)])
+    x0 = np.stack([synth.random_labels((H, W), L, seed=case * 7 + 3 + b) for b in range(B)])
+    gibbs_lockstep(make_ctx(cfg, g, x0), cfg, 3)

@@ -532,3 +532,37 @@ def test_multi_sweep_launches_free_running_vs_oracle(cuda_device, L, nb, per, ip
     assert np.array_equal(ctx.state()[0], x_o)
     c = ctx.counts()[0]
     assert np.array_equal(c, (cnt_o[1] if L == 2 else cnt_o).astype(np.uint16))
+
+
+def _random_configs(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        L = int(rng.choice([2, 2, 3, 4, 5, 7, 9, 12, 16, 17, 33, 64, 100]))
+        nb = int(rng.choice([4, 8]))
+        per = bool(rng.integers(2))
+        H = int(rng.integers(3 if per else 1, 70))
+        W = int(rng.integers(3 if per else 1, 700))
+        kw = dict(neighborhood=nb, periodic=per, sigma=float(rng.uniform(0.05, 0.8)),
+                  q=float(rng.choice([0.0, 0.51, rng.uniform(0, 5)])), beta0=float(rng.uniform(0.3, 3)),
+                  beta_step=float(rng.uniform(0, 1)), beta_period=int(rng.integers(1, 4)),
+                  coef_scale=float(rng.choice([1.0, 0.5])), inertia_p=int(rng.integers(0, 3)),
+                  J=float(rng.uniform(0.1, 1.0)), seed=int(rng.integers(1 << 40)),
+                  chain0=int(rng.integers(0, 1000)), batch=int(rng.integers(1, 4)),
+                  mpm_burn_in=int(rng.integers(-1, 3)),
+                  kernel=int(rng.choice([P.KERNEL_AUTO, P.KERNEL_GENERAL])))
+        out.append((H, W, L, kw))
+    return out
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_randomised_configurations_lockstep(cuda_device, case):
+    """Random shapes, levels, neighbourhoods, boundaries, schedules, coefficients, inertia
+    norms, batches and kernels: 4 lockstep sweeps against the oracle (R19 tolerance)."""
+    H, W, L, kw = _random_configs(24, 2026)[case]
+    cfg = P.make_config(H, W, L, **kw)
+    B = kw["batch"]
+    g = np.stack([synth.random_labels((H, W), L, seed=case * 10 + b) for b in range(B)])
+    x0 = np.stack([synth.random_labels((H, W), L, seed=case * 10 + 5 + b) for b in range(B)])
+    ctx = make_ctx(cfg, g, x0)
+    lockstep(ctx, cfg, 4).check()

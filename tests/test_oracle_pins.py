@@ -429,3 +429,24 @@ def test_coloured_gibbs_run_counts():
             for k in range(3):
                 ref[k] += (y == k)
     assert np.array_equal(x, y) and np.array_equal(cnt, ref)
+
+
+def test_windowed_ssim_against_filter_implementation():
+    """orc_ssim_windowed (explicit 7x7 loops) against an independent filter formulation:
+    window means and sample (co)variances from scipy.ndimage.uniform_filter over the valid
+    window centres, then the mean of the SSIM map (Wang et al.'s definition, R16)."""
+    from scipy.ndimage import uniform_filter
+
+    rng = np.random.default_rng(12)
+    for L, shape in [(5, (23, 31)), (2, (7, 40)), (33, (16, 16))]:
+        x = rng.integers(0, L, shape).astype(np.uint8)
+        y = np.clip(x.astype(int) + rng.integers(-1, 2, shape), 0, L - 1).astype(np.uint8)
+        a, b = x / (L - 1.0), y / (L - 1.0)
+        n = 49.0
+        f = lambda z: uniform_filter(z, size=7, mode="constant")[3:-3, 3:-3]  # valid centres
+        mx, my = f(a), f(b)
+        vx = (f(a * a) - mx * mx) * n / (n - 1)
+        vy = (f(b * b) - my * my) * n / (n - 1)
+        cxy = (f(a * b) - mx * my) * n / (n - 1)
+        ssim_map = ((2 * mx * my + 1e-4) * (2 * cxy + 9e-4)) / ((mx ** 2 + my ** 2 + 1e-4) * (vx + vy + 9e-4))
+        assert orc.ssim_windowed(x, y, L) == pytest.approx(float(ssim_map.mean()), abs=1e-12)
