@@ -566,3 +566,25 @@ def test_randomised_configurations_lockstep(cuda_device, case):
     x0 = np.stack([synth.random_labels((H, W), L, seed=case * 10 + 5 + b) for b in range(B)])
     ctx = make_ctx(cfg, g, x0)
     lockstep(ctx, cfg, 4).check()
+
+
+def test_restore_api_matches_the_step_by_step_calls(cuda_device):
+    """paper_2507_14869_b200.api.restore (the paper protocol in one call) equals the explicit
+    sequence of ABI calls and the oracle's chain."""
+    from paper_2507_14869_b200.api import restore
+
+    L, H, W = 5, 40, 56
+    truth = synth.smooth_labels(H, W, L, seed=3)
+    g = synth.degrade(truth, L, 0.25, seed=4)
+    res = restore(g, L, truth=truth, sweeps=60, beta_period=20, seed=9, windowed=True)
+    assert res.sweeps == 60 and res.counted_sweeps == 20
+    cfg = P.make_config(H, W, L, sigma=0.25, beta_period=20, seed=9, mpm_burn_in=40)
+    x_o, cnt_o = orc.pca_run(oracle_model(cfg), g, g, 60, 1.25, 0.25, 20, 9, burn_in=40)
+    assert np.array_equal(res.last[0], x_o) and np.array_equal(res.mpm[0], orc.mpm(cnt_o))
+    for e, est in enumerate((x_o, orc.mpm(cnt_o))):
+        _, p_o, s_o, _ = orc.metrics(truth, est, L)
+        assert abs(res.psnr[0, e] - p_o) < 1e-9 and abs(res.ssim[0, e] - s_o) < 1e-9
+        assert abs(res.ssim_windowed[0, e] - orc.ssim_windowed(truth, est, L)) < 1e-12
+    gb = restore(g, L, method="gibbs", sweeps=30, beta_period=20, seed=9)
+    x_g, _ = orc.gibbs_run(oracle_model(cfg), g, g, 30, 1.25, 0.25, 20, 9, order="colour")
+    assert np.array_equal(gb.last[0], x_g)
