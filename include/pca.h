@@ -238,6 +238,12 @@ pca_status pca_set_step(pca_ctx* ctx, int64_t t);
 
 pca_status pca_get_stats(pca_ctx* ctx, pca_stats* out);
 
+/* Number of sites whose label changed in the most recent sweep, per chain (changed[batch]),
+ * for the strip this context owns: x_t against x_{t-1}, which the double buffer still holds
+ * after PCA sweeps (and two-level Moore Gibbs sweeps).  PCA_EINVAL before the first sweep,
+ * after pca_reset / pca_write_state, or after an in-place Gibbs sweep.  Synchronises. */
+pca_status pca_changed_sites(pca_ctx* ctx, int64_t* changed);
+
 /* Device pointers of the halo rows of the current state (loopback exchange). */
 pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out);
 

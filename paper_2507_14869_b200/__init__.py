@@ -30,7 +30,7 @@ STATUS_NAMES = {0: "PCA_OK", -1: "PCA_EINVAL", -2: "PCA_ESTATE", -3: "PCA_ECUDA"
 # every symbol include/pca.h declares
 EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "pca_sweep",
            "pca_gibbs_sweep", "pca_estimate", "pca_metric_sums", "pca_psnr_ssim", "pca_finalize",
-           "pca_stage_truth",
+           "pca_stage_truth", "pca_changed_sites",
            "pca_ssim_windowed", "pca_read_state",
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
@@ -98,6 +98,7 @@ def lib():
             "pca_ssim_windowed": (i32, [vp, vp, i32, vp]),
             "pca_finalize": (i32, [vp, vp, vp, vp, vp]),
             "pca_stage_truth": (i32, [vp, vp]),
+            "pca_changed_sites": (i32, [vp, vp]),
             "pca_read_state": (i32, [vp, vp]),
             "pca_write_state": (i32, [vp, vp]),
             "pca_read_counts": (i32, [vp, vp]),
@@ -260,6 +261,12 @@ class PcaContext:
 
     def pca_set_step(self, t: int):
         _check(lib().pca_set_step(self.handle, int(t)), "pca_set_step")
+
+    def pca_changed_sites(self) -> np.ndarray:
+        """Sites whose label changed in the most recent sweep, per chain."""
+        out = np.zeros(self.cfg.batch, np.int64)
+        _check(lib().pca_changed_sites(self.handle, out.ctypes.data), "pca_changed_sites")
+        return out
 
     def pca_get_stats(self) -> pca_stats:
         st = pca_stats()

@@ -364,6 +364,31 @@ __global__ void __launch_bounds__(SSIM_TPB) ssim_windowed_kernel(const WinSsimPa
     }
 }
 
+// Sites whose label differs between two padded state buffers (x_t and x_{t-1}), per chain:
+// 16 sites per thread, nonzero bytes of the XOR counted with a SWAR test and popc.
+__global__ void __launch_bounds__(TPB) changed_kernel(Geometry G, const uint8_t* __restrict__ xa,
+                                                      const uint8_t* __restrict__ xb,
+                                                      unsigned long long* __restrict__ out) {
+    const int chain = blockIdx.z;
+    const int c0 = 16 * (blockIdx.x * TPB + threadIdx.x);
+    const int n = c0 < G.W ? min(16, G.W - c0) : 0;
+    unsigned long long cnt = 0;
+    if (n > 0) {
+        const uint8_t* a = xa + chain * G.xchain + XOFF;
+        const uint8_t* b = xb + chain * G.xchain + XOFF;
+        for (int r = blockIdx.y; r < G.rows; r += gridDim.y) {
+            const long long off = (long long)(r + HALO) * G.xpitch;
+            const uint4 va = load16(a + off, c0, n, true), vb = load16(b + off, c0, n, true);
+            const uint32_t z[4] = {va.x ^ vb.x, va.y ^ vb.y, va.z ^ vb.z, va.w ^ vb.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                cnt += __popc((((z[i] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z[i]) & 0x80808080u);
+        }
+    }
+    cnt = warp_sum(cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out + chain, cnt);
+}
+
 __global__ void param_table_kernel(const __grid_constant__ ParamTable t, int n, uint32_t* dst) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = t.v[i];
 }
@@ -401,6 +426,12 @@ int launch_check_levels(const uint8_t* p, size_t n, int levels, int* bad, void* 
     if (blocks > 2048) blocks = 2048;
     if (blocks == 0) blocks = 1;
     check_levels_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(p, n, levels, bad);
+    return (int)cudaGetLastError();
+}
+
+int launch_changed(const Geometry& G, const uint8_t* xa, const uint8_t* xb,
+                   unsigned long long* out, int batch, void* stream) {
+    changed_kernel<<<chunk_grid(G, batch, 512), TPB, 0, (cudaStream_t)stream>>>(G, xa, xb, out);
     return (int)cudaGetLastError();
 }
 

@@ -172,6 +172,9 @@ int launch_mpm(const Geometry& geo, const uint16_t* counts, int nsamp, uint8_t* 
 int launch_marginals(const Geometry& geo, const uint16_t* counts, int nsamp, float* out,
                      long long out_chain_stride, int k, int batch, void* stream);
 int launch_metric_sums(const MetricParams& p, int batch, void* stream);  // kind 0, 1 or 2
+// out[chain] += number of sites whose label differs between padded buffers xa and xb
+int launch_changed(const Geometry& geo, const uint8_t* xa, const uint8_t* xb,
+                   unsigned long long* out, int batch, void* stream);
 
 // windowed SSIM: 7x7 uniform windows at every position inside the image, sample moments
 constexpr int SSIM_WIN = 7, SSIM_TPB = 128, SSIM_ROWS_PER_BLOCK = 64;

@@ -240,6 +240,7 @@ struct pca_ctx {
     int rows_per_thread = 8;
     int poisoned = 0;
     int x_initialized = 0;
+    int prev_valid = 0;  // x[cur ^ 1] holds x_{t-1} (after a PCA or double-buffered Gibbs sweep)
     int64_t tab_stage = -1;
     int64_t gtab_stage = -1;
     GibbsSweepParams gib;
@@ -609,6 +610,7 @@ pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
 
 pca_status load_state(pca_ctx* ctx, const uint8_t* src, int pitch, long long chain_stride,
                       const char* what) {
+    ctx->prev_valid = 0;
     CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
     LAUNCH(ctx, launch_pack_state(ctx->geo, src, pitch, chain_stride, ctx->x[ctx->cur],
                                   ctx->cfg.batch, ctx->flag, ctx->stream));
@@ -642,6 +644,7 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
     }
     CK(ctx, cudaMemsetAsync(ctx->counts, 0, L.counts_bytes, ctx->stream));
     ctx->cur = 0;
+    ctx->prev_valid = 0;
     ctx->t = 0;
     ctx->counted = 0;
     ctx->tab_stage = -1;
@@ -812,6 +815,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
                 const int e = launch_sweep_general(ctx->gen, ctx->cfg.batch, (int)run, ctx->stream);
                 if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (multi-sweep launch)");
                 ctx->cur ^= (int)(run & 1);
+                ctx->prev_valid = 1;
                 ctx->t = t + run;
                 ctx->counted += count * run;
                 i += (int32_t)run - 1;
@@ -837,6 +841,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             const int e = launch_sweep_binary2(ctx->bin2, ctx->cfg.batch, 0, ctx->stream);
             if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (two per pass)");
             ctx->cur ^= 1;
+            ctx->prev_valid = 1;
             ctx->t = t + 2;
             ctx->counted += c0 + c1;
             ++i;
@@ -891,6 +896,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             if (st != PCA_OK) return st;
         }
         ctx->cur ^= 1;
+        ctx->prev_valid = 1;
         ctx->t = t + 1;
         ctx->counted += count;
     }
@@ -939,6 +945,7 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
                 ctx->sweep_launches++;
                 const int e = launch_sweep_gibbs(ctx->gib, c.batch, (int)run, ctx->stream);
                 if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep (multi-sweep launch)");
+                ctx->prev_valid = 0;  // in place
                 ctx->t = t + run;
                 ctx->counted += count * run;
                 i += (int32_t)run - 1;
@@ -964,6 +971,7 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
                 }
             }
             ctx->cur ^= 1;
+            ctx->prev_valid = 1;
             ctx->t = t + 1;
             ctx->counted += count;
             continue;
@@ -981,6 +989,7 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
             ctx->sweep_launches++;
             const int e = launch_sweep_gibbs(ctx->gib, c.batch, 1, ctx->stream);
             if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep");
+            ctx->prev_valid = 0;  // in place
             if (strip) {
                 st = exchange(ctx, ctx->x[ctx->cur], 1);
                 if (st != PCA_OK) return st;
@@ -1254,6 +1263,24 @@ pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, d
         for (size_t i = 0; i < per; ++i) t += h[(size_t)b * per + i];
         ssim[b] = t / nwin;
     }
+    return PCA_OK;
+}
+
+pca_status pca_changed_sites(pca_ctx* ctx, int64_t* changed) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!changed) return fail(PCA_EINVAL, "changed is NULL");
+    if (!ctx->prev_valid)
+        return fail(PCA_EINVAL, "no previous state: sweep first (in-place Gibbs sweeps keep none)");
+    const size_t nb = (size_t)ctx->cfg.batch * sizeof(unsigned long long);
+    CK(ctx, cudaMemsetAsync(ctx->sums, 0, nb, ctx->stream));
+    LAUNCH(ctx, launch_changed(ctx->geo, ctx->x[ctx->cur], ctx->x[ctx->cur ^ 1], ctx->sums,
+                               ctx->cfg.batch, ctx->stream));
+    std::vector<unsigned long long> h(ctx->cfg.batch);
+    CK(ctx, cudaMemcpyAsync(h.data(), ctx->sums, nb, cudaMemcpyDeviceToHost, ctx->stream));
+    st = sync(ctx);
+    if (st != PCA_OK) return st;
+    for (int b = 0; b < ctx->cfg.batch; ++b) changed[b] = (int64_t)h[b];
     return PCA_OK;
 }
 

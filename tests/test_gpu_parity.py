@@ -588,3 +588,31 @@ def test_restore_api_matches_the_step_by_step_calls(cuda_device):
     gb = restore(g, L, method="gibbs", sweeps=30, beta_period=20, seed=9)
     x_g, _ = orc.gibbs_run(oracle_model(cfg), g, g, 30, 1.25, 0.25, 20, 9, order="colour")
     assert np.array_equal(gb.last[0], x_g)
+
+
+@pytest.mark.parametrize("shape,L,n", [((64, 64, 4, True), 2, 1), ((37, 531, 8, False), 2, 3),
+                                       ((40, 130, 8, False), 5, 1), ((600, 600, 8, True), 5, 2)])
+def test_changed_sites_counts_the_last_sweep(cuda_device, shape, L, n):
+    """pca_changed_sites = number of sites with x_t != x_{t-1} (the double buffer), per chain,
+    after single-sweep and multi-sweep launches; unavailable after a reset."""
+    H, W, nb, per = shape
+    B = 2
+    g = np.stack([synth.random_labels((H, W), L, seed=b) for b in range(B)])
+    cfg = P.make_config(H, W, L, batch=B, neighborhood=nb, periodic=per, sigma=0.4, seed=8)
+    ctx = make_ctx(cfg, g)
+    with pytest.raises(P.PcaError, match="previous"):
+        ctx.pca_changed_sites()
+    ctx.pca_sweep(4)
+    prev = ctx.state()
+    ctx.pca_sweep(n)
+    if n > 1:
+        m = oracle_model(cfg)
+        x = prev
+        for t in range(4, 4 + n - 1):
+            x = np.stack([orc.pca_sweep(m, x[b], g[b], beta_of(cfg, t), cfg.seed, b, t)[0] for b in range(B)])
+        prev = x
+    cur = ctx.state()
+    assert np.array_equal(ctx.pca_changed_sites(), (cur != prev).reshape(B, -1).sum(1))
+    ctx.pca_reset(None, None)
+    with pytest.raises(P.PcaError):
+        ctx.pca_changed_sites()
