@@ -196,3 +196,37 @@ def test_gibbs_randomised_configurations_lockstep(cuda_device, case):
     g = np.stack([synth.random_labels((H, W), L, seed=case * 7 + b) for b in range(B)])
     x0 = np.stack([synth.random_labels((H, W), L, seed=case * 7 + 3 + b) for b in range(B)])
     gibbs_lockstep(make_ctx(cfg, g, x0), cfg, 3)
+
+
+def test_gibbs_checkpoint_and_pca_interleaving_on_the_binary_path(cuda_device):
+    """Two levels, Moore-8 torus, W % 16 == 0 (the double-buffered binary Gibbs kernel):
+    PCA and Gibbs sweeps interleaved one call at a time equal the oracle's sequence, and a
+    checkpoint (state, counts, step) resumed in a fresh context continues the same chain."""
+    H, W = 32, 64
+    g = synth.degrade(synth.smooth_labels(H, W, 2, 3), 2, 0.5, 4)
+    cfg = P.make_config(H, W, 2, periodic=True, sigma=0.5, beta0=1.2, beta_step=0.2,
+                        beta_period=3, seed=13, mpm_burn_in=2)
+    ctx = make_ctx(cfg, g)
+    plan = ["pca", "gibbs", "gibbs", "pca", "gibbs", "pca", "gibbs"]
+    for step in plan[:4]:
+        (ctx.pca_sweep if step == "pca" else ctx.pca_gibbs_sweep)(1)
+    # checkpoint after 4 sweeps
+    x4, c4 = ctx.state(), ctx.counts()
+    resumed = make_ctx(cfg, g, x4)
+    resumed.pca_write_counts(c4, ctx.pca_get_stats().counted_sweeps)
+    resumed.pca_set_step(4)
+    for step in plan[4:]:
+        for c in (ctx, resumed):
+            (c.pca_sweep if step == "pca" else c.pca_gibbs_sweep)(1)
+    assert np.array_equal(ctx.state(), resumed.state())
+    assert np.array_equal(ctx.counts(), resumed.counts())
+    m = oracle_model(cfg)
+    x = g.copy()
+    cnt = np.zeros((H, W), np.uint16)
+    for t, step in enumerate(plan):
+        beta = beta_of(cfg, t)
+        x = orc.pca_sweep(m, x, g, beta, 13, 0, t)[0] if step == "pca" else \
+            orc.gibbs_sweep_coloured(m, x, g, beta, 13, 0, t)
+        if t >= 2:
+            cnt += x
+    assert np.array_equal(ctx.state()[0], x) and np.array_equal(ctx.counts()[0], cnt)
