@@ -47,6 +47,9 @@ namespace {
 #endif
 // PCA_T_RED = 1: torus counts by fire-and-forget 64-bit reductions (no load): measured
 // 138 us per sweep (16.8 M RED.64 per sweep saturate the L2 atomic units), so it stays off.
+#ifndef PCA_CARRY
+#define PCA_CARRY 1  // decisions as borrow bits (sub.cc / addc): 84.5 -> 83.8 us (0 = compare)
+#endif
 #ifndef PCA_T_RED
 #define PCA_T_RED 0
 #endif
@@ -230,9 +233,11 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
             const uint4 rnd = philox4x32_10(
                 make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain), p.c.keys);
             const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
-            uint32_t o = 0u;
+            // sub.cc sets the carry of T + ~r + 1, i.e. T >= r: the complement of the decision
+            // w = (r > T); shifted into a 4-bit word (site b -> bit b, sites taken 3..0)
+            uint32_t bits = 0u;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 3; b >= 0; --b) {
                 uint32_t off = __byte_perm(IDX4[i], 0u, 0x4440 + b);
                 if (PER) {
                     off += NB * 36 * 4;
@@ -241,9 +246,12 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
                     off += (uint32_t)np * 144u;
                 }
                 const uint32_t T = *reinterpret_cast<const uint32_t*>(thr_b + off);
-                if (rw[b] > T) o += 1u << (8 * b);
+                uint32_t dummy;
+                asm("sub.cc.u32 %1, %2, %3;\n\taddc.u32 %0, %0, %0;"
+                    : "+r"(bits), "=r"(dummy)
+                    : "r"(T), "r"(rw[b]));
             }
-            O[i] = o;
+            O[i] = ((~bits & 0xFu) * 0x00204081u) & 0x01010101u;  // bit b -> byte b
         }
         // ---- fused MPM counts of label 1 (uint16 per site) ----
         if (cbytes) {
@@ -323,6 +331,28 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
             const uint4 rnd = philox4x32_10(
                 make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain), p.c.keys);
             const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
+#if PCA_CARRY
+            // sub.cc sets the carry of T + ~r + 1, i.e. T >= r: the complement of the decision
+            // w = (r > T); shifted into a 4-bit word (site b -> bit b, sites taken 3..0), then
+            // complemented and spread to bytes
+            uint32_t bits = 0u;
+#pragma unroll
+            for (int b = 3; b >= 0; --b) {
+                uint32_t off = __byte_perm(IDX4[q][i], 0u, 0x4440 + b);
+                if (PER) {
+                    off += NB * 36 * 4;
+                } else {
+                    const int np = edge[q] ? neighbours_present<NB>(grow, G.H, ccol + 4 * i + b, G.W) : NB;
+                    off += (uint32_t)np * 144u;
+                }
+                const uint32_t T = *reinterpret_cast<const uint32_t*>(thr_b + off);
+                uint32_t dummy;
+                asm("sub.cc.u32 %1, %2, %3;\n\taddc.u32 %0, %0, %0;"
+                    : "+r"(bits), "=r"(dummy)
+                    : "r"(T), "r"(rw[b]));
+            }
+            O[q][i] = ((~bits & 0xFu) * 0x00204081u) & 0x01010101u;
+#else
             uint32_t o = 0u;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
@@ -337,6 +367,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
                 if (rw[b] > T) o += 1u << (8 * b);
             }
             O[q][i] = o;
+#endif
         };
 #pragma unroll
         for (int i = 0; i < 4; ++i)
