@@ -16,6 +16,8 @@
 //   sums   : uint64 [batch][8] metric accumulators
 //   stage  : uint8 [batch][rows][W] (+ fp32 space for MARGINALS/CM) host<->device staging
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstddef>
 #include <cstdint>
 
@@ -139,6 +141,19 @@ struct MetricParams {
     int nsamp;             // counted sweeps (MPM ties for levels == 2)
     uint8_t* mpm_out;      // kind 2: dense MPM image [batch][rows][W], or nullptr
 };
+
+// Per-device launch facts (occupancy, SM count) cached on first use on each device:
+// cudaFuncSetAttribute and occupancy are per device, so one process may drive several GPUs.
+struct LaunchInfo {
+    bool ok = false;
+    int occ = 1, mocc = 1, sms = 1;
+};
+constexpr int MAX_DEVICES = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 ? 0 : (d >= MAX_DEVICES ? MAX_DEVICES - 1 : d);
+}
 
 // ---- launchers (return cudaError_t as int) ----
 int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread,

@@ -289,20 +289,21 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
 template <int NB, bool PER>
 int launch_t(const Binary2SweepParams& p, int batch, int R, cudaStream_t s) {
     const Geometry& G = p.c.geo;
-    static bool configured = false;
-    static int occ = 0, sms = 0;
-    if (!configured) {
+    static LaunchInfo info[MAX_DEVICES];
+    LaunchInfo& li = info[current_device()];
+    if (!li.ok) {
         cudaError_t e = cudaFuncSetAttribute(sweep_binary2_kernel<NB, PER>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         if (e != cudaSuccess) return (int)e;
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_binary2_kernel<NB, PER>, 32,
+        cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_binary2_kernel<NB, PER>, 32,
                                                       SMEM_BYTES);
-        if (occ < 1) occ = 1;
-        configured = true;
+        if (li.occ < 1) li.occ = 1;
+        li.ok = true;
     }
+    const int occ = li.occ, sms = li.sms;
     if (R <= 0) {
         const long long segs = (G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
         const long long target = (long long)sms * occ;

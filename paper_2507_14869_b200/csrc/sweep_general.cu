@@ -438,26 +438,30 @@ __global__ void __launch_bounds__(GEN_THREADS, PCA_GEN_MINB)
 
 template <int NB, int LT>
 struct GenLaunch {
-    static int occ, sms, mocc;
-    static void init() {
-        if (occ) return;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_general_kernel<NB, LT>, GEN_THREADS, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, sweep_multi_kernel<NB, LT>, GEN_THREADS, 0);
-        if (occ < 1) occ = 1;
-        if (mocc < 1) mocc = 1;
+    // per device: occupancy of both kernels at their dynamic shared memory, SM count
+    static LaunchInfo& get() {
+        static LaunchInfo info[MAX_DEVICES];
+        LaunchInfo& li = info[current_device()];
+        if (!li.ok) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+            const int smem = (int)sizeof(GenSmem<LT>);
+            cudaFuncSetAttribute(sweep_general_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(sweep_multi_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_general_kernel<NB, LT>, GEN_THREADS, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, sweep_multi_kernel<NB, LT>, GEN_THREADS, smem);
+            if (li.occ < 1) li.occ = 1;
+            if (li.mocc < 1) li.mocc = 1;
+            li.ok = true;
+        }
+        return li;
     }
 };
-template <int NB, int LT> int GenLaunch<NB, LT>::occ = 0;
-template <int NB, int LT> int GenLaunch<NB, LT>::sms = 0;
-template <int NB, int LT> int GenLaunch<NB, LT>::mocc = 0;
 
 template <int NB, int LT>
 int launch_g(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t s) {
-    using GL = GenLaunch<NB, LT>;
-    GL::init();
+    const LaunchInfo& GL = GenLaunch<NB, LT>::get();
     const Geometry& G = p.c.geo;
     const int nquads = (G.W + 3) / 4;
     const int nr = p.c.rhi - p.c.rlo;
@@ -466,7 +470,7 @@ int launch_g(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t s
     const long long quadrows = (long long)d1.nxb * d1.QW * nr * batch;  // thread-rows of work
     if (nsweeps > 1) {
         // spread the thread-rows over the co-resident blocks, one row per thread when they fit
-        const long long slots = (long long)GL::sms * GL::mocc;
+        const long long slots = (long long)GL.sms * GL.mocc;
         long long R = (quadrows + slots * GEN_THREADS - 1) / (slots * GEN_THREADS);
         if (R < 1) R = 1;
         const Decomp d = make_decomp(nquads, nr, (int)R);
@@ -480,7 +484,7 @@ int launch_g(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t s
     }
     // rows per run: about four waves of blocks (the fp64 share of a row varies, so several
     // waves balance the tail), each thread walking a run of rows with a rolling window
-    const long long target = 4LL * GL::sms * GL::occ * GEN_THREADS;
+    const long long target = 4LL * GL.sms * GL.occ * GEN_THREADS;
     long long R = (quadrows + target - 1) / target;
     if (R < 1) R = 1;
     Decomp d = make_decomp(nquads, nr, (int)R);

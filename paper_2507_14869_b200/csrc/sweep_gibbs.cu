@@ -436,16 +436,19 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
 
 template <int NB, bool BIN, bool FUSED>
 int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s) {
-    static int occ = 0, mocc = 0, sms = 0;
-    if (occ == 0) {
+    static LaunchInfo info[MAX_DEVICES];
+    LaunchInfo& li = info[current_device()];
+    if (!li.ok) {
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_gibbs_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, gibbs_multi_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
-        if (occ < 1) occ = 1;
-        if (mocc < 1) mocc = 1;
+        cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_gibbs_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, gibbs_multi_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
+        if (li.occ < 1) li.occ = 1;
+        if (li.mocc < 1) li.mocc = 1;
+        li.ok = true;
     }
+    const int occ = li.occ, mocc = li.mocc, sms = li.sms;
     const Geometry& G = p.c.geo;
     const int nquads = (G.W + 3) / 4;
     int nr = p.c.rhi - p.c.rlo;

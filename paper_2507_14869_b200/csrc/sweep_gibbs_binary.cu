@@ -256,18 +256,19 @@ __global__ void __launch_bounds__(32, GCTAS)
 
 template <bool PER>
 int launch_gb2(const GibbsBinParams& p, int batch, cudaStream_t s) {
-    static bool configured = false;
-    static int occ = 0, sms = 0;
-    if (!configured) {
+    static LaunchInfo info[MAX_DEVICES];
+    LaunchInfo& li = info[current_device()];
+    if (!li.ok) {
         cudaError_t e = cudaFuncSetAttribute(gibbs_binary_kernel<PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
         if (e != cudaSuccess) return (int)e;
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gibbs_binary_kernel<PER>, 32, GSMEM);
-        if (occ < 1) occ = 1;
-        configured = true;
+        cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, gibbs_binary_kernel<PER>, 32, GSMEM);
+        if (li.occ < 1) li.occ = 1;
+        li.ok = true;
     }
+    const int occ = li.occ, sms = li.sms;
     const Geometry& G = p.c.geo;
     int rfirst = p.c.rlo;
     if (((G.row0 + rfirst) & 1) != p.parity) ++rfirst;
