@@ -297,12 +297,27 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// device memory of another GPU than the context's cannot be used by its kernels
+pca_status check_same_device(const pca_ctx* ctx, const void* p, const char* what) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return PCA_OK;  // plain host memory
+    }
+    if (a.type == cudaMemoryTypeDevice && a.device != ctx->device)
+        return fail(PCA_EINVAL, "%s is on device %d, the context on device %d", what, a.device,
+                    ctx->device);
+    return PCA_OK;
+}
+
 size_t dense_bytes(const pca_ctx* ctx) {
     return (size_t)ctx->cfg.batch * ctx->lay.rows * (size_t)ctx->cfg.width;
 }
 
 // device view of a dense uint8 image argument (host data staged through `stage`)
 pca_status device_input(pca_ctx* ctx, const uint8_t* p, const uint8_t** out) {
+    pca_status st = check_same_device(ctx, p, "input image");
+    if (st != PCA_OK) return st;
     if (is_device_ptr(p)) {
         *out = p;
         return PCA_OK;
@@ -1009,6 +1024,8 @@ pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
     const pca_config& c = ctx->cfg;
     if (kind != PCA_EST_LAST && ctx->counted < 1)
         return fail(PCA_EINVAL, "MPM/marginal/CM estimates need counted sweeps (mpm_burn_in)");
+    st = check_same_device(ctx, out, "out");
+    if (st != PCA_OK) return st;
     const bool dev = is_device_ptr(out);
     const size_t plane = (size_t)ctx->lay.rows * c.width;
     if (kind == PCA_EST_LAST || kind == PCA_EST_MPM) {
@@ -1160,6 +1177,10 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
     } else {
         CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_truth_ready, 0));
         dt = ctx->truth;
+    }
+    if (mpm_out) {
+        st = check_same_device(ctx, mpm_out, "mpm_out");
+        if (st != PCA_OK) return st;
     }
     const bool dev_out = mpm_out && is_device_ptr(mpm_out);
     uint8_t* mo = mpm_out ? (dev_out ? mpm_out : ctx->stage + align256(dense_bytes(ctx))) : nullptr;
