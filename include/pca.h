@@ -115,7 +115,11 @@ typedef struct pca_config {
     int32_t inertia_p;     /* inertia norm p: 0 = L0 1{s != x_i} (paper), 1 = |lum x_i - lum s|,*/
                            /* 2 = (lum x_i - lum s)^2; identical for   */
                            /* levels == 2                                                      */
-    int32_t reserved[5];   /* must be zero                                                     */
+    int32_t packed_io;     /* levels == 2 only: 1 = every image argument and result (g, x0,     */
+                           /* truth, LAST / MPM estimates, state) is bit-packed: each row is     */
+                           /* ceil(width/8) bytes, column c at bit c%8 (LSB first) of byte c/8;  */
+                           /* 8x fewer host<->device bytes.  The sweep itself runs on uint8.    */
+    int32_t reserved[4];   /* must be zero                                                     */
 } pca_config;
 
 typedef struct pca_stats {

@@ -56,7 +56,7 @@ class pca_config(ctypes.Structure):
         ("mpm_burn_in", ctypes.c_int32), ("row0", ctypes.c_int32), ("rows", ctypes.c_int32),
         ("kernel", ctypes.c_int32), ("rows_per_thread", ctypes.c_int32),
         ("sweeps_per_pass", ctypes.c_int32), ("inertia_p", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 5),
+        ("packed_io", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4),
     ]
 
 
@@ -128,7 +128,7 @@ def _check(status: int, where: str):
 def make_config(height, width, levels, *, batch=1, neighborhood=8, periodic=False, J=1.0 / 3.0,
                 q=0.51, sigma=0.25, beta0=1.25, beta_step=0.25, beta_period=250, chain0=0,
                 coef_scale=1.0, seed=0, mpm_burn_in=-1, row0=0, rows=0, kernel=KERNEL_AUTO,
-                rows_per_thread=0, sweeps_per_pass=0, inertia_p=0) -> pca_config:
+                rows_per_thread=0, sweeps_per_pass=0, inertia_p=0, packed_io=0) -> pca_config:
     """pca_config with the paper's defaults (J = 1/3, q = 0.51, beta
     1.25 + 0.25 every 250 sweeps; Moore-8 neighbourhood, free boundary)."""
     c = pca_config()
@@ -141,6 +141,7 @@ def make_config(height, width, levels, *, batch=1, neighborhood=8, periodic=Fals
     c.kernel, c.rows_per_thread = int(kernel), int(rows_per_thread)
     c.sweeps_per_pass = int(sweeps_per_pass)
     c.inertia_p = int(inertia_p)
+    c.packed_io = int(packed_io)
     return c
 
 
@@ -155,6 +156,16 @@ def pca_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().pca_nccl_unique_id(buf), "pca_nccl_unique_id")
     return buf.raw
+
+
+def pack_bits(img) -> np.ndarray:
+    """Dense 0/1 labels [..., W] -> the packed_io layout [..., ceil(W/8)] (LSB = first column)."""
+    return np.packbits(np.asarray(img, np.uint8) & 1, axis=-1, bitorder="little")
+
+
+def unpack_bits(bits, width: int) -> np.ndarray:
+    """The packed_io layout -> dense 0/1 labels [..., width]."""
+    return np.unpackbits(np.asarray(bits, np.uint8), axis=-1, count=width, bitorder="little")
 
 
 def _ptr(a) -> int:
@@ -183,6 +194,8 @@ class PcaContext:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.rows = cfg.rows if cfg.rows else cfg.height
         self.shape = (cfg.batch, self.rows, cfg.width)
+        # image arguments / results: dense uint8, or bit-packed rows when cfg.packed_io
+        self.image_shape = (cfg.batch, self.rows, (cfg.width + 7) // 8) if cfg.packed_io else self.shape
         nbytes = pca_workspace_bytes(cfg)
         with torch.cuda.device(self.device):
             self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
@@ -292,7 +305,7 @@ class PcaContext:
 
     # ---- conveniences (host NumPy results) ----
     def state(self) -> np.ndarray:
-        return self.pca_read_state(np.empty(self.shape, np.uint8))
+        return self.pca_read_state(np.empty(self.image_shape, np.uint8))
 
     def counts(self) -> np.ndarray:
         planes = 1 if self.cfg.levels == 2 else self.cfg.levels
@@ -302,7 +315,7 @@ class PcaContext:
 
     def estimate(self, kind: int) -> np.ndarray:
         if kind in (EST_LAST, EST_MPM):
-            out = np.empty(self.shape, np.uint8)
+            out = np.empty(self.image_shape, np.uint8)
         elif kind == EST_CM:
             out = np.empty(self.shape, np.float32)
         else:

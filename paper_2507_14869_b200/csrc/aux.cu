@@ -389,6 +389,45 @@ __global__ void __launch_bounds__(TPB) changed_kernel(Geometry G, const uint8_t*
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out + chain, cnt);
 }
 
+// Bit-packed binary images (packed_io): rows of pb = ceil(W/8) bytes, column c at bit c%8 of
+// byte c/8.  One thread per packed byte.
+__global__ void unpack_bits_kernel(const uint8_t* __restrict__ bits, uint8_t* __restrict__ dense,
+                                   int W, long long nrows) {
+    const int pb = (W + 7) >> 3;
+    const long long n = nrows * pb;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / pb;
+        const int k = (int)(i - row * pb);
+        const uint32_t v = bits[i];
+        uint8_t* d = dense + row * W + 8 * k;
+        const int m = min(8, W - 8 * k);
+        if (m == 8 && (((uintptr_t)d) & 7) == 0) {
+            const uint32_t lo = ((v & 0xFu) * 0x00204081u) & 0x01010101u;
+            const uint32_t hi = ((v >> 4) * 0x00204081u) & 0x01010101u;
+            *reinterpret_cast<uint2*>(d) = make_uint2(lo, hi);
+        } else {
+            for (int j = 0; j < m; ++j) d[j] = (uint8_t)((v >> j) & 1u);
+        }
+    }
+}
+
+__global__ void pack_bits_kernel(const uint8_t* __restrict__ dense, uint8_t* __restrict__ bits, int W,
+                                 long long nrows) {
+    const int pb = (W + 7) >> 3;
+    const long long n = nrows * pb;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / pb;
+        const int k = (int)(i - row * pb);
+        const uint8_t* d = dense + row * W + 8 * k;
+        const int m = min(8, W - 8 * k);
+        uint32_t v = 0;
+        for (int j = 0; j < m; ++j) v |= (uint32_t)(d[j] & 1u) << j;
+        bits[i] = (uint8_t)v;
+    }
+}
+
 __global__ void param_table_kernel(const __grid_constant__ ParamTable t, int n, uint32_t* dst) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = t.v[i];
 }
@@ -398,6 +437,22 @@ __global__ void param_table_kernel(const __grid_constant__ ParamTable t, int n, 
 int launch_param_table(const ParamTable& t, int n, uint32_t* dst, void* stream) {
     if (n < 0 || n > PARAM_TABLE_MAX) return (int)cudaErrorInvalidValue;
     param_table_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(t, n, dst);
+    return (int)cudaGetLastError();
+}
+
+int launch_unpack_bits(const uint8_t* bits, uint8_t* dense, int W, long long nrows, void* stream) {
+    const long long n = nrows * ((W + 7) / 8);
+    if (n <= 0) return 0;
+    const int blocks = (int)((n + 255) / 256 < 65535 ? (n + 255) / 256 : 65535);
+    unpack_bits_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(bits, dense, W, nrows);
+    return (int)cudaGetLastError();
+}
+
+int launch_pack_bits(const uint8_t* dense, uint8_t* bits, int W, long long nrows, void* stream) {
+    const long long n = nrows * ((W + 7) / 8);
+    if (n <= 0) return 0;
+    const int blocks = (int)((n + 255) / 256 < 65535 ? (n + 255) / 256 : 65535);
+    pack_bits_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(dense, bits, W, nrows);
     return (int)cudaGetLastError();
 }
 

@@ -188,6 +188,9 @@ int launch_marginals(const Geometry& geo, const uint16_t* counts, int nsamp, flo
                      long long out_chain_stride, int k, int batch, void* stream);
 int launch_metric_sums(const MetricParams& p, int batch, void* stream);  // kind 0, 1 or 2
 // out[chain] += number of sites whose label differs between padded buffers xa and xb
+// bit-packed binary images <-> dense uint8 [nrows][W] (packed rows of ceil(W/8) bytes)
+int launch_unpack_bits(const uint8_t* bits, uint8_t* dense, int W, long long nrows, void* stream);
+int launch_pack_bits(const uint8_t* dense, uint8_t* bits, int W, long long nrows, void* stream);
 int launch_changed(const Geometry& geo, const uint8_t* xa, const uint8_t* xb,
                    unsigned long long* out, int batch, void* stream);
 

@@ -120,7 +120,8 @@ struct Layout {
     size_t off_bthr = 0;                    // binary PCA thresholds [THR_ENTRIES]
     size_t off_gbthr = 0;                   // binary Gibbs thresholds [GIBBS_THR_PAD]
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
-           off_sums_max = 0, off_flag = 0, off_stage = 0, off_truth = 0;
+           off_sums_max = 0, off_flag = 0, off_stage = 0, off_truth = 0, off_io = 0;
+    size_t io_bytes = 0;  // one bit-packed image set (packed_io), 0 otherwise
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
 };
 
@@ -165,7 +166,10 @@ pca_status validate(const pca_config* c) {
         return fail(PCA_EINVAL, "sweeps_per_pass must be 0, 1 or 2");
     if (c->inertia_p < 0 || c->inertia_p > 2)
         return fail(PCA_EINVAL, "inertia_p must be 0 (L0), 1 (L1) or 2 (L2)");
-    for (int i = 0; i < 5; ++i)
+    if (c->packed_io != 0 && c->packed_io != 1) return fail(PCA_EINVAL, "packed_io must be 0 or 1");
+    if (c->packed_io && c->levels != 2)
+        return fail(PCA_EUNSUPPORTED, "bit-packed images need levels == 2");
+    for (int i = 0; i < 4; ++i)
         if (c->reserved[i] != 0) return fail(PCA_EINVAL, "reserved fields must be zero");
     return PCA_OK;
 }
@@ -210,6 +214,8 @@ Layout make_layout(const pca_config* c) {
     L.off_flag = o; o = align256(o + 256);
     L.off_stage = o; o = align256(o + L.stage_bytes);
     L.off_truth = o; o = align256(o + B * R * W);  // staged truth (pca_stage_truth)
+    L.io_bytes = c->packed_io ? B * R * (size_t)((c->width + 7) / 8) : 0;
+    L.off_io = o; o = align256(o + 3 * align256(L.io_bytes));  // packed in / out / truth
     L.total = o;
     return L;
 }
@@ -260,6 +266,9 @@ struct pca_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // pca_stage_truth: the truth copied on its own stream, overlapping the sweeps
     uint8_t* truth = nullptr;
+    uint8_t* io_in = nullptr;     // packed_io: a bit-packed argument, before unpacking
+    uint8_t* io_out = nullptr;    // packed_io: a bit-packed result, before the copy out
+    uint8_t* io_truth = nullptr;  // packed_io: the staged truth, bit-packed
     int truth_staged = 0;
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_truth_ready = nullptr, ev_truth_free = nullptr;
@@ -276,6 +285,13 @@ pca_status cuda_fail(pca_ctx* ctx, cudaError_t e, const char* where) {
     do {                                                              \
         cudaError_t e_ = (cudaError_t)(expr);                         \
         if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #expr);    \
+    } while (0)
+
+#define LAUNCH(ctx, expr)                                                        \
+    do {                                                                         \
+        int e_ = (expr);                                                         \
+        (ctx)->launches++;                                                       \
+        if (e_ != 0) return cuda_fail((ctx), (cudaError_t)e_, #expr);            \
     } while (0)
 
 pca_status usable(pca_ctx* ctx) {
@@ -318,6 +334,13 @@ size_t dense_bytes(const pca_ctx* ctx) {
 pca_status device_input(pca_ctx* ctx, const uint8_t* p, const uint8_t** out) {
     pca_status st = check_same_device(ctx, p, "input image");
     if (st != PCA_OK) return st;
+    if (ctx->cfg.packed_io) {  // bit-packed argument: copy, then unpack into the stage
+        CK(ctx, cudaMemcpyAsync(ctx->io_in, p, ctx->lay.io_bytes, cudaMemcpyDefault, ctx->stream));
+        LAUNCH(ctx, launch_unpack_bits(ctx->io_in, ctx->stage, ctx->cfg.width,
+                                       (long long)ctx->cfg.batch * ctx->lay.rows, ctx->stream));
+        *out = ctx->stage;
+        return PCA_OK;
+    }
     if (is_device_ptr(p)) {
         *out = p;
         return PCA_OK;
@@ -349,13 +372,6 @@ pca_status check_flag(pca_ctx* ctx, const char* what) {
     if (h) return fail(PCA_EINVAL, "%s contains a value >= levels", what);
     return PCA_OK;
 }
-
-#define LAUNCH(ctx, expr)                                                        \
-    do {                                                                         \
-        int e_ = (expr);                                                         \
-        (ctx)->launches++;                                                       \
-        if (e_ != 0) return cuda_fail((ctx), (cudaError_t)e_, #expr);            \
-    } while (0)
 
 double beta_at(const pca_config& c, int64_t t) {
     return c.beta0 + c.beta_step * (double)(t / c.beta_period);
@@ -720,6 +736,9 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->flag = (int*)(ctx->ws + L.off_flag);
     ctx->stage = ctx->ws + L.off_stage;
     ctx->truth = ctx->ws + L.off_truth;
+    ctx->io_in = ctx->ws + L.off_io;
+    ctx->io_out = ctx->io_in + align256(L.io_bytes);
+    ctx->io_truth = ctx->io_out + align256(L.io_bytes);
     ctx->uthr = L.uthr_entries ? (uint32_t*)(ctx->ws + L.off_uthr) : nullptr;
     ctx->uthr_host.resize(L.uthr_entries);
     ctx->sparse_host.resize(2 * L.sparse_entries);
@@ -1029,14 +1048,19 @@ pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
     const bool dev = is_device_ptr(out);
     const size_t plane = (size_t)ctx->lay.rows * c.width;
     if (kind == PCA_EST_LAST || kind == PCA_EST_MPM) {
-        uint8_t* dst = dev ? (uint8_t*)out : ctx->stage;
+        uint8_t* dst = (dev && !c.packed_io) ? (uint8_t*)out : ctx->stage;
         if (kind == PCA_EST_LAST)
             LAUNCH(ctx, launch_unpack_state(ctx->geo, ctx->x[ctx->cur], dst, c.batch, ctx->stream));
         else
             LAUNCH(ctx, launch_mpm(ctx->geo, ctx->counts, (int)ctx->counted, dst, c.batch, ctx->stream));
-        if (!dev)
+        if (c.packed_io) {  // bit-packed result
+            LAUNCH(ctx, launch_pack_bits(ctx->stage, ctx->io_out, c.width,
+                                         (long long)c.batch * ctx->lay.rows, ctx->stream));
+            CK(ctx, cudaMemcpyAsync(out, ctx->io_out, ctx->lay.io_bytes, cudaMemcpyDefault, ctx->stream));
+        } else if (!dev) {
             CK(ctx, cudaMemcpyAsync(out, ctx->stage, dense_bytes(ctx), cudaMemcpyDeviceToHost,
                                     ctx->stream));
+        }
         return sync(ctx);
     }
     // float outputs: CM [B][rows][W]; MARGINALS [B][levels][rows][W], one label plane per pass
@@ -1155,7 +1179,13 @@ pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth) {
     }
     // the previous finalize's read of the buffer comes first
     CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev_truth_free, 0));
-    CK(ctx, cudaMemcpyAsync(ctx->truth, truth, dense_bytes(ctx), cudaMemcpyDefault, ctx->copy));
+    if (ctx->cfg.packed_io) {
+        CK(ctx, cudaMemcpyAsync(ctx->io_truth, truth, ctx->lay.io_bytes, cudaMemcpyDefault, ctx->copy));
+        LAUNCH(ctx, launch_unpack_bits(ctx->io_truth, ctx->truth, ctx->cfg.width,
+                                       (long long)ctx->cfg.batch * ctx->lay.rows, ctx->copy));
+    } else {
+        CK(ctx, cudaMemcpyAsync(ctx->truth, truth, dense_bytes(ctx), cudaMemcpyDefault, ctx->copy));
+    }
     CK(ctx, cudaEventRecord(ctx->ev_truth_ready, ctx->copy));
     ctx->truth_staged = 1;
     return PCA_OK;
@@ -1182,7 +1212,7 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
         st = check_same_device(ctx, mpm_out, "mpm_out");
         if (st != PCA_OK) return st;
     }
-    const bool dev_out = mpm_out && is_device_ptr(mpm_out);
+    const bool dev_out = mpm_out && is_device_ptr(mpm_out) && !c.packed_io;
     uint8_t* mo = mpm_out ? (dev_out ? mpm_out : ctx->stage + align256(dense_bytes(ctx))) : nullptr;
     const size_t nb = (size_t)c.batch * 16 * sizeof(unsigned long long);
     CK(ctx, cudaMemsetAsync(ctx->sums, 0, nb, ctx->stream));
@@ -1214,8 +1244,13 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
     CK(ctx, cudaMemcpyAsync(h.data(), ctx->sums, nb, cudaMemcpyDeviceToHost, ctx->stream));
     if (ctx->comm && ctx->nranks > 1)
         CK(ctx, cudaMemcpyAsync(hm.data(), ctx->sums_max, nb, cudaMemcpyDeviceToHost, ctx->stream));
-    if (mpm_out && !dev_out)
+    if (mpm_out && c.packed_io) {  // bit-packed MPM image
+        LAUNCH(ctx, launch_pack_bits(mo, ctx->io_out, c.width, (long long)c.batch * ctx->lay.rows,
+                                     ctx->stream));
+        CK(ctx, cudaMemcpyAsync(mpm_out, ctx->io_out, ctx->lay.io_bytes, cudaMemcpyDefault, ctx->stream));
+    } else if (mpm_out && !dev_out) {
         CK(ctx, cudaMemcpyAsync(mpm_out, mo, dense_bytes(ctx), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     st = sync(ctx);
     if (st != PCA_OK) return st;
     bool black = false;

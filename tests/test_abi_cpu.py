@@ -34,9 +34,9 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_config_struct_layout_matches_header():
-    # 6 int32, 5 double, 2 int32, double, uint64, 7 int32, 5 int32 reserved (natural alignment)
+    # 6 int32, 5 double, 2 int32, double, uint64, 8 int32, 4 int32 reserved (natural alignment)
     assert ctypes.sizeof(P.pca_config) == 24 + 40 + 8 + 8 + 8 + 20 + 28
-    assert P.pca_config.seed.offset == 80 and P.pca_config.inertia_p.offset == 112 and P.pca_config.reserved.offset == 116
+    assert P.pca_config.seed.offset == 80 and P.pca_config.inertia_p.offset == 112 and P.pca_config.packed_io.offset == 116 and P.pca_config.reserved.offset == 120
 
 
 def test_workspace_and_validation(lib):
@@ -46,7 +46,8 @@ def test_workspace_and_validation(lib):
         dict(levels=1), dict(levels=256), dict(neighborhood=6), dict(periodic=True, height=2),
         dict(J=0.0), dict(q=-1.0), dict(sigma=0.0), dict(beta0=0.0), dict(beta_step=-0.1),
         dict(beta_period=0), dict(coef_scale=0.0), dict(rows=10, row0=60), dict(batch=0),
-        dict(kernel=P.KERNEL_BINARY, levels=3), dict(rows_per_thread=-3), dict(batch=70000), dict(kernel=3), dict(inertia_p=3), dict(inertia_p=-1),
+        dict(kernel=P.KERNEL_BINARY, levels=3), dict(rows_per_thread=-3), dict(batch=70000), dict(kernel=3), dict(inertia_p=3), dict(inertia_p=-1), dict(packed_io=2),
+        dict(packed_io=1, levels=5),
     ]
     for kw in bad:
         args = dict(height=64, width=64, levels=2)

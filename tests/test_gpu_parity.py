@@ -616,3 +616,38 @@ def test_changed_sites_counts_the_last_sweep(cuda_device, shape, L, n):
     ctx.pca_reset(None, None)
     with pytest.raises(P.PcaError):
         ctx.pca_changed_sites()
+
+
+@pytest.mark.parametrize("W", [64, 77])
+def test_packed_io_matches_dense_io(cuda_device, W):
+    """packed_io (two levels): bit-packed g / x0 / truth in, bit-packed LAST / MPM / state out,
+    host and device buffers, staged truth -- the same chain and metrics as dense I/O."""
+    import torch
+
+    H, B = 40, 2
+    truth = np.stack([synth.smooth_labels(H, W, 2, seed=b) for b in range(B)])
+    g = np.stack([synth.degrade(truth[b], 2, 0.5, seed=9 + b) for b in range(B)])
+    kw = dict(batch=B, neighborhood=8, periodic=False, sigma=0.5, seed=17, mpm_burn_in=3)
+    dense = make_ctx(P.make_config(H, W, 2, **kw), g)
+    packed = P.PcaContext(P.make_config(H, W, 2, packed_io=1, **kw),
+                          torch.from_numpy(P.pack_bits(g)).cuda())
+    for c in (dense, packed):
+        c.pca_sweep(9)
+    assert np.array_equal(P.unpack_bits(packed.state(), W), dense.state())
+    assert np.array_equal(P.unpack_bits(packed.estimate(P.EST_MPM), W), dense.estimate(P.EST_MPM))
+    assert np.array_equal(packed.counts(), dense.counts())
+    mpm_d = np.zeros((B, H, W), np.uint8)
+    pd, sd = dense.pca_finalize(truth, mpm_d)
+    mpm_p = torch.zeros((B, H, (W + 7) // 8), dtype=torch.uint8, device="cuda")
+    pp, sp = packed.pca_finalize(torch.from_numpy(P.pack_bits(truth)).cuda(), mpm_p)
+    assert np.array_equal(pp, pd) and np.array_equal(sp, sd)
+    assert np.array_equal(P.unpack_bits(mpm_p.cpu().numpy(), W), mpm_d)
+    packed.pca_stage_truth(P.pack_bits(truth))
+    assert np.array_equal(packed.pca_finalize(None)[0], pd)
+    # write a packed state and continue: same as the dense context written with the same state
+    x = synth.random_labels((B, H, W), 2, seed=3)
+    packed.pca_write_state(P.pack_bits(x))
+    dense.pca_write_state(x)
+    for c in (dense, packed):
+        c.pca_sweep(2)
+    assert np.array_equal(P.unpack_bits(packed.state(), W), dense.state())
