@@ -289,18 +289,26 @@ def run_ours(args):
     achieved = alg_bytes / sweep_s / 1e9
     traffic, traffic_src = load_traffic()
 
-    # ---- end-to-end through the C ABI with pinned host buffers ----
+    # ---- end-to-end through the C ABI with pinned host buffers.  Two-level images travel
+    # bit-packed (pca_config.packed_io): 1 bit per site in each direction ----
     e2e = None
     if not args.no_e2e:
-        g_h = torch.from_numpy(g).reshape(1, rows, W).pin_memory()
-        t_h = torch.from_numpy(truth).reshape(1, rows, W).pin_memory()
-        mpm_h = torch.empty((1, rows, W), dtype=torch.uint8).pin_memory()
+        packed = wl["levels"] == 2
+        kw_e = dict(kw, packed_io=int(packed))
+        pk = P.pack_bits if packed else (lambda a: a)
+        g_h = torch.from_numpy(np.ascontiguousarray(pk(g))).reshape(1, rows, -1).pin_memory()
+        t_h = torch.from_numpy(np.ascontiguousarray(pk(truth))).reshape(1, rows, -1).pin_memory()
+        mpm_h = torch.empty(tuple(t_h.shape), dtype=torch.uint8).pin_memory()
+        if world > 1:
+            ectx = pdist.strip_context(kw_e, wl["H"], W, wl["levels"], g_h, stream=stream)
+        else:
+            ectx = P.PcaContext(P.make_config(wl["H"], W, wl["levels"], **kw_e), g_h, stream=stream)
 
         def step_e2e():
-            ctx.pca_reset(g_h, None)            # H2D of g inside the step
-            ctx.pca_stage_truth(t_h)            # H2D of the truth, overlapping the sweeps
-            ctx.pca_sweep(S)
-            return ctx.pca_finalize(None, mpm_h)  # D2H of the MPM image
+            ectx.pca_reset(g_h, None)            # H2D of g inside the step
+            ectx.pca_stage_truth(t_h)            # H2D of the truth, overlapping the sweeps
+            ectx.pca_sweep(S)
+            return ectx.pca_finalize(None, mpm_h)  # D2H of the MPM image
 
         for _ in range(max(1, args.warmup)):
             step_e2e()
@@ -308,14 +316,18 @@ def run_ours(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            step_e2e()
+            pe, se = step_e2e()
         e1.record(stream)
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
+        assert abs(pe[0, 1] - psnr[0, 1]) < 1e-9 and abs(se[0, 1] - ssim[0, 1]) < 1e-12  # same chain
         e2e = {"value": sites_all * S * args.steps / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(g_h.numel() + t_h.numel()),
                "d2h_bytes_per_step": int(mpm_h.numel() + 4 * 8),
-               "ms_per_step": ems / args.steps}
+               "ms_per_step": ems / args.steps,
+               "io": ("bit-packed images (packed_io): g and truth in, MPM image out, 1 bit per site"
+                      if packed else "dense uint8 images")}
+        ectx.pca_destroy()
 
     clk = clocks.stop()
 

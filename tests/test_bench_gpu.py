@@ -30,6 +30,8 @@ def test_bench_contract_line(cuda_device):
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     assert d["gpu_launches"] >= 2 * (S + 2)
     e2e = d["e2e"]
-    assert e2e["h2d_bytes_per_step"] == 2 * H * W and e2e["d2h_bytes_per_step"] >= H * W
+    # two levels: images cross PCIe bit-packed (packed_io), rows of ceil(W/8) bytes
+    assert e2e["h2d_bytes_per_step"] == 2 * H * ((W + 7) // 8)
+    assert e2e["d2h_bytes_per_step"] >= H * ((W + 7) // 8) and "packed" in e2e["io"]
     assert 0 < e2e["value"] <= d["value"] * 1.05
     assert d["clocks"]["sm_max_mhz"] > 0
