@@ -115,11 +115,17 @@ __device__ int decide_sparse(const GeneralSweepParams& p, const double* sA, cons
 // Uniform-neighbourhood thresholds staged in shared memory when the table is small.
 __host__ __device__ constexpr int uthr_smem_entries(int LT) { return (LT > 0 && LT <= 9) ? LT * LT * LT * (LT - 1) : 1; }
 
+// levels <= 8 known at compile time: the fp64 queue uses W0[g][x][s] = D[g][s] I[x][s] (the
+// part of the weight that does not depend on the neighbours), built per block in shared
+// memory (at 9 levels the table would cost a resident block per SM)
+__host__ __device__ constexpr bool w0_smem(int LT) { return LT > 2 && LT <= 8; }
+
 template <int LT>
 struct GenSmem {
     double A[9];
     double D[LT > 2 ? LT * LT : 1];
     double I[LT > 2 ? LT * LT : 1];
+    double W0[w0_smem(LT) ? LT * LT * LT : 1];
     uint32_t U[LT == 2 ? THR_ENTRIES : uthr_smem_entries(LT)];  // levels == 2: binary table
     SiteJob jobs[GEN_WARPS][128];
     uint8_t res[GEN_WARPS][128];
@@ -132,6 +138,12 @@ __device__ __forceinline__ void gen_load_tables(const GeneralSweepParams& p, Gen
         for (int i = threadIdx.x; i < LT * LT; i += blockDim.x) {
             sm.D[i] = p.dtab[i];
             sm.I[i] = p.inertia_p != 0 ? p.itab[i] : 0.0;
+        }
+    if (w0_smem(LT))
+        for (int i = threadIdx.x; i < LT * LT * LT; i += blockDim.x) {
+            const int g = i / (LT * LT), x = (i / LT) % LT, s = i % LT;
+            const double I = p.inertia_p != 0 ? p.itab[x * LT + s] : (s == x ? 1.0 : p.Cw);
+            sm.W0[i] = p.dtab[g * LT + s] * I;
         }
     if (LT == 2)
         for (int i = threadIdx.x; i < THR_ENTRIES; i += blockDim.x) sm.U[i] = p.bthr[i];
@@ -268,14 +280,24 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
                 const bool valid = act && b < nvalid;
                 const bool uniform = use_u && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
-                if (valid && uniform) {
+                if (SMEM_U) {
+                    // branch-free: every lane reads a table row (row 0 when its site is not a
+                    // valid uniform one) and counts the thresholds T_k >= r with borrow bits
+                    const bool uni = valid && uniform;
+                    const uint32_t* T = U + (uni ? ((s0 * LT + gi) * LT + xi) * (LT - 1) : 0);
+                    uint32_t ge = 0;
+#pragma unroll
+                    for (int k = 0; k < (SMEM_U ? LT - 1 : 1); ++k)
+                        asm("{\n\t.reg .u32 d;\n\tsub.cc.u32 d, %1, %2;\n\taddc.u32 %0, %0, 0;\n\t}"
+                            : "+r"(ge) : "r"(T[k]), "r"(rr[b]));
+                    outw |= (uni ? (uint32_t)(LT - 1) - ge : 0u) << (8 * b);
+                } else if (valid && uniform) {
                     // every neighbour carries s* = s0 (so all NB exist): integer thresholds
                     const uint32_t* T = U + (size_t)((s0 * L + gi) * L + xi) * (L - 1);
                     int w = 0;
                     if (LT > 0) {
 #pragma unroll
-                        for (int k = 0; k < (LT > 0 ? LT - 1 : 1); ++k)
-                            w += (rr[b] > (SMEM_U ? T[k] : __ldg(T + k))) ? 1 : 0;
+                        for (int k = 0; k < (LT > 0 ? LT - 1 : 1); ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
                     } else {
                         for (int k = 0; k < L - 1; ++k) w += (rr[b] > __ldg(T + k)) ? 1 : 0;
                     }
@@ -284,8 +306,9 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 // compact the fp64 sites of the warp into its queue
                 const bool need = valid && !uniform;
                 const unsigned m = __ballot_sync(FULL, need);
-                qpos[b] = qbase + __popc(m & lt);
-                if (need) {
+                const int pos = qbase + __popc(m & lt);
+                qpos[b] = need ? pos : -1;
+                if (m) {  // warp-uniform: the job is built by every lane, stored by the needy
                     const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);  // byte b of a, of b
                     SiteJob jb;
                     if (NB == 8) {
@@ -297,9 +320,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                     }
                     jb.xg = (uint32_t)xi | ((uint32_t)gi << 8);
                     jb.r = rr[b];
-                    jobs[qpos[b]] = jb;
-                } else {
-                    qpos[b] = -1;
+                    if (need) jobs[pos] = jb;
                 }
                 qbase += __popc(m);
             }
@@ -307,7 +328,8 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 __syncwarp();
                 for (int i = lane; i < qbase; i += 32) {
                     int w = -1;
-                    if (LT > 2) w = decide_fp64_fixed<NB, (LT > 2 ? LT : 3)>(p, sm.A, sm.D, sm.I, jobs[i]);
+                    if (w0_smem(LT)) w = decide_fp64_w0<NB, (w0_smem(LT) ? LT : 3)>(sm.A, sm.W0, jobs[i]);
+                    else if (LT > 2) w = decide_fp64_fixed<NB, (LT > 2 ? LT : 3)>(p, sm.A, sm.D, sm.I, jobs[i]);
                     else if (LT == 0 && p.pfx != nullptr) w = decide_sparse<NB>(p, sm.A, jobs[i]);
                     if (w < 0) w = decide_fp64<NB>(p, sm.A, jobs[i]);
                     res[i] = (uint8_t)w;
