@@ -57,8 +57,9 @@ __device__ __forceinline__ int decide_fp64_fixed(const GeneralSweepParams& p, co
 }
 
 // L <= 8 known at compile time, W0[g][x][s] = D[g][s] I[x][s] staged in shared memory:
-// w_s = A[n_s] W0[g][x][s].  The neighbour histogram (one nibble per label, L <= 8 fits 32
-// bits) uses the PTX shift's clamp: the free-boundary sentinel 0xFF shifts the 1 out.
+// w_s = A[n_s] W0[g][x][s].  The site is byte sb of the staged quad words (w0 = UL UC UR ML,
+// w1 = MR DL DC DR; 4 neighbours: UC ML MR DC).  The neighbour histogram (one nibble per
+// label, L <= 8 fits 32 bits) uses the PTX shift's clamp: the sentinel 0xFF shifts the 1 out.
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t n) {
     uint32_t r;
     asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(n));
@@ -66,41 +67,34 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t n) {
 }
 
 template <int NB, int L>
-__device__ __forceinline__ int decide_fp64_w0(const double* sA, const double* sW0, const SiteJob& j) {
-    uint64_t hist = 0;
-    if (L <= 8) {
-        uint32_t h = 0;
-#pragma unroll
-        for (int q = 0; q < NB; ++q) {
-            const uint32_t w = q < 4 ? j.nb_lo : j.nb_hi;
-            const uint32_t sh = (q & 3) == 0 ? (w << 2) & 0x3FCu : (w >> (8 * (q & 3) - 2)) & 0x3FCu;
-            h += shl_clamp(1u, sh);  // labels < L <= 8 stay below bit 32; 0xFF -> 0
-        }
-        hist = h;
-    } else {
-#pragma unroll
-        for (int q = 0; q < NB; ++q) {
-            const uint32_t v = ((q < 4 ? j.nb_lo : j.nb_hi) >> (8 * (q & 3))) & 0xFFu;
-            hist += (v < (uint32_t)L) ? (1ull << (4 * v)) : 0ull;
-        }
-    }
-    const int xi = (int)(j.xg & 0xFFu), gi = (int)((j.xg >> 8) & 0xFFu);
+__device__ __forceinline__ int decide_fp64_w0(const double* sA, const double* sW0, uint4 w0, uint4 w1,
+                                              uint32_t xw, uint32_t gw, uint32_t r, int sb) {
+    static_assert(L <= 8, "nibble histogram in 32 bits");
+    const uint32_t sel = 0x4440u + (uint32_t)sb;
+    auto one = [&](uint32_t w) { return shl_clamp(1u, __byte_perm(w, 0u, sel) << 2); };
+    uint32_t h;
+    if (NB == 8)
+        h = one(w0.x) + one(w0.y) + one(w0.z) + one(w0.w) + one(w1.x) + one(w1.y) + one(w1.z) + one(w1.w);
+    else
+        h = one(w0.y) + one(w0.w) + one(w1.x) + one(w1.z);
+    const int xi = (int)__byte_perm(xw, 0u, sel), gi = (int)__byte_perm(gw, 0u, sel);
     const double* Wrow = sW0 + (gi * L + xi) * L;
     double w[L];
     double Z = 0.0;
 #pragma unroll
     for (int s = 0; s < L; ++s) {
-        w[s] = sA[(int)((hist >> (4 * s)) & 0xFull)] * Wrow[s];
+        w[s] = sA[(h >> (4 * s)) & 0xFu] * Wrow[s];
         Z += w[s];
     }
     if (!(Z >= 1e-290 && Z <= 1e290)) return -1;  // caller takes the log-domain path
-    const double target = (double)j.r * (1.0 / 4294967296.0) * Z;
+    const double target = (double)r * (1.0 / 4294967296.0) * Z;
+    // F_k is non-decreasing, so min{k < L-1 : target < F_k} (else L-1) = #{k < L-1 : F_k <= target}
     double F = 0.0;
-    int res = L - 1;
+    int res = 0;
 #pragma unroll
     for (int s = 0; s < L - 1; ++s) {
         F += w[s];
-        res = (res == L - 1 && target < F) ? s : res;
+        res += (F <= target) ? 1 : 0;
     }
     return res;
 }

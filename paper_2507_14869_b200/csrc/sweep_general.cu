@@ -127,7 +127,11 @@ struct GenSmem {
     double I[LT > 2 ? LT * LT : 1];
     double W0[w0_smem(LT) ? LT * LT * LT : 1];
     uint32_t U[LT == 2 ? THR_ENTRIES : uthr_smem_entries(LT)];  // levels == 2: binary table
-    SiteJob jobs[GEN_WARPS][128];
+    // per lane, the quad's words a queued site needs (STAGE_WORDS: a stride that keeps the
+    // 128-bit stores of a quarter-warp on distinct banks): UL UC UR ML | MR DL DC DR | x g - - |
+    // r0 r1 r2 r3; the per-warp queue holds lane*4 + site
+    alignas(16) uint32_t stage[GEN_WARPS][32 * 20];
+    uint8_t queue[GEN_WARPS][128];
     uint8_t res[GEN_WARPS][128];
 };
 
@@ -189,7 +193,8 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
     if (__ballot_sync(FULL, active) == 0) return;  // warp-uniform exit
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const unsigned lt = (1u << lane) - 1u;
-    SiteJob* jobs = sm.jobs[warp];
+    uint32_t* stage = sm.stage[warp];
+    uint8_t* queue = sm.queue[warp];
     uint8_t* res = sm.res[warp];
     const bool use_u = LT == 2 || p.uthr != nullptr;
     const uint32_t* U = (SMEM_U || LT == 2) ? sm.U : p.uthr;
@@ -200,8 +205,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
 
     // rolling 3-row window of the words left of / at / right of the quad
     uint32_t up[3] = {0, 0, 0}, mid[3] = {0, 0, 0}, dn[3] = {0, 0, 0};
-    auto load_row = [&](int r, uint32_t (&w)[3]) {
-        const uint8_t* xr = xcol + (long long)(r + HALO) * G.xpitch;
+    auto load_row = [&](const uint8_t* xr, uint32_t (&w)[3]) {
         if (COH) {
             w[0] = __ldcg(reinterpret_cast<const uint32_t*>(xr - 4));
             w[1] = __ldcg(reinterpret_cast<const uint32_t*>(xr));
@@ -214,13 +218,21 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
     };
     // software pipeline: the x row r+2 and the g row r+1 are loaded one iteration ahead, so
     // the load latency overlaps a row of work (rows rbeg-1 .. rend+1 exist: HALO = 2)
+    // (running row pointers: the next x row to fetch, the next g row, this row's output and
+    // count words)
     uint32_t nxt[3] = {0, 0, 0}, gnext = 0;
+    const uint8_t* xp = xcol + (long long)(rbeg - 1 + HALO) * G.xpitch;
+    const uint8_t* gp = gcol + (long long)(rbeg + GHALO) * G.gpitch;
     if (active) {
-        load_row(rbeg - 1, up);
-        load_row(rbeg, mid);
-        load_row(rbeg + 1, nxt);
-        gnext = ldg4(gcol + (long long)(rbeg + GHALO) * G.gpitch);
+        load_row(xp, up);
+        load_row(xp + G.xpitch, mid);
+        load_row(xp + 2 * G.xpitch, nxt);
+        gnext = ldg4(gp);
     }
+    xp += 3 * G.xpitch;
+    gp += G.gpitch;
+    uint8_t* op = x_out + chain * G.xchain + (long long)(rbeg + HALO) * G.xpitch + XOFF + c0;
+    uint16_t* cp = p.c.counts + chain * G.cchain + (long long)rbeg * G.cpitch + c0;
 
     for (int it = 0; it < iters; ++it) {
         const int r = rbeg + it;
@@ -229,9 +241,11 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
         for (int j = 0; j < 3; ++j) dn[j] = nxt[j];
         const uint32_t gword = gnext;
         if (act && r + 1 < rend) {
-            load_row(r + 2, nxt);
-            gnext = ldg4(gcol + (long long)(r + 1 + GHALO) * G.gpitch);
+            load_row(xp, nxt);
+            gnext = ldg4(gp);
         }
+        xp += G.xpitch;
+        gp += G.gpitch;
         const int grow = G.row0 + r;
         uint4 rnd = make_uint4(0, 0, 0, 0);
         if (act)
@@ -271,20 +285,28 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 D = (UC ^ ML) | (ML ^ MR) | (MR ^ DC);
             const uint32_t differ = (((D & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | D) & 0x80808080u;
             const uint32_t S0 = NB == 8 ? UL : UC;  // s* when uniform
-            int qpos[4];
-            int qbase = 0;
+            // <= 5 levels: the uniform-table rows (s*, g, x) of the 4 sites in one SWAR word
+            // (s* masked to 3 bits: a non-uniform site's byte may be the sentinel; <= 199)
+            const uint32_t IDX4 = LT > 2 && LT <= 5 ? (S0 & 0x07070707u) * (uint32_t)(LT * LT) + gword * (uint32_t)LT + xw : 0u;
+            uint32_t needm = 0;  // bit b: site b goes to the warp's fp64 queue
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                const int xi = (int)((xw >> (8 * b)) & 0xFFu);
-                const int gi = (int)((gword >> (8 * b)) & 0xFFu);
-                const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
+                const int s0 = (int)__byte_perm(S0, 0u, 0x4440 + b);
                 const bool valid = act && b < nvalid;
                 const bool uniform = use_u && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
                 if (SMEM_U) {
                     // branch-free: every lane reads a table row (row 0 when its site is not a
                     // valid uniform one) and counts the thresholds T_k >= r with borrow bits
                     const bool uni = valid && uniform;
-                    const uint32_t* T = U + (uni ? ((s0 * LT + gi) * LT + xi) * (LT - 1) : 0);
+                    int row;
+                    if (LT <= 5) {
+                        row = (int)__byte_perm(IDX4, 0u, 0x4440 + b);
+                    } else {
+                        const int xi = (int)__byte_perm(xw, 0u, 0x4440 + b);
+                        const int gi = (int)__byte_perm(gword, 0u, 0x4440 + b);
+                        row = (s0 * LT + gi) * LT + xi;
+                    }
+                    const uint32_t* T = U + (uni ? row * (LT - 1) : 0);
                     uint32_t ge = 0;
 #pragma unroll
                     for (int k = 0; k < (SMEM_U ? LT - 1 : 1); ++k)
@@ -293,6 +315,8 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                     outw |= (uni ? (uint32_t)(LT - 1) - ge : 0u) << (8 * b);
                 } else if (valid && uniform) {
                     // every neighbour carries s* = s0 (so all NB exist): integer thresholds
+                    const int xi = (int)__byte_perm(xw, 0u, 0x4440 + b);
+                    const int gi = (int)__byte_perm(gword, 0u, 0x4440 + b);
                     const uint32_t* T = U + (size_t)((s0 * L + gi) * L + xi) * (L - 1);
                     int w = 0;
                     if (LT > 0) {
@@ -303,35 +327,57 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                     }
                     outw |= (uint32_t)w << (8 * b);
                 }
-                // compact the fp64 sites of the warp into its queue
-                const bool need = valid && !uniform;
-                const unsigned m = __ballot_sync(FULL, need);
-                const int pos = qbase + __popc(m & lt);
-                qpos[b] = need ? pos : -1;
-                if (m) {  // warp-uniform: the job is built by every lane, stored by the needy
-                    const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);  // byte b of a, of b
-                    SiteJob jb;
-                    if (NB == 8) {
-                        jb.nb_lo = __byte_perm(__byte_perm(UL, UC, sel), __byte_perm(UR, ML, sel), 0x5410);
-                        jb.nb_hi = __byte_perm(__byte_perm(MR, DL, sel), __byte_perm(DC, DR, sel), 0x5410);
-                    } else {
-                        jb.nb_lo = __byte_perm(__byte_perm(UC, ML, sel), __byte_perm(MR, DC, sel), 0x5410);
-                        jb.nb_hi = 0u;
-                    }
-                    jb.xg = (uint32_t)xi | ((uint32_t)gi << 8);
-                    jb.r = rr[b];
-                    if (need) jobs[pos] = jb;
-                }
-                qbase += __popc(m);
+                needm |= (valid && !uniform) ? 1u << b : 0u;
             }
-            if (qbase > 0) {  // warp-uniform
+            if (__ballot_sync(FULL, needm != 0u)) {  // warp-uniform
+                // a lane with queued sites stages its quad's words once; the queue holds
+                // (lane, site) and the consumer lane reads the words it needs
+                if (needm) {
+                    uint4* st = reinterpret_cast<uint4*>(stage + lane * 20);
+                    st[0] = make_uint4(UL, UC, UR, ML);
+                    st[1] = make_uint4(MR, DL, DC, DR);
+                    st[2] = make_uint4(xw, gword, 0u, 0u);
+                    st[3] = make_uint4(rnd.x, rnd.y, rnd.z, rnd.w);
+                }
+                int qpos[4];
+                int qbase = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const bool need = (needm >> b) & 1u;
+                    const unsigned m = __ballot_sync(FULL, need);
+                    const int pos = qbase + __popc(m & lt);
+                    if (need) queue[pos] = (uint8_t)(lane * 4 + b);
+                    qpos[b] = need ? pos : -1;
+                    qbase += __popc(m);
+                }
                 __syncwarp();
                 for (int i = lane; i < qbase; i += 32) {
+                    const int e = queue[i];
+                    const int sb = e & 3;
+                    const uint32_t* sw = stage + (e >> 2) * 20;
+                    const uint4 w0 = *reinterpret_cast<const uint4*>(sw);
+                    const uint4 w1 = *reinterpret_cast<const uint4*>(sw + 4);
+                    const uint2 xg = *reinterpret_cast<const uint2*>(sw + 8);
+                    const uint32_t rs = sw[12 + sb];
                     int w = -1;
-                    if (w0_smem(LT)) w = decide_fp64_w0<NB, (w0_smem(LT) ? LT : 3)>(sm.A, sm.W0, jobs[i]);
-                    else if (LT > 2) w = decide_fp64_fixed<NB, (LT > 2 ? LT : 3)>(p, sm.A, sm.D, sm.I, jobs[i]);
-                    else if (LT == 0 && p.pfx != nullptr) w = decide_sparse<NB>(p, sm.A, jobs[i]);
-                    if (w < 0) w = decide_fp64<NB>(p, sm.A, jobs[i]);
+                    if (w0_smem(LT))
+                        w = decide_fp64_w0<NB, (w0_smem(LT) ? LT : 3)>(sm.A, sm.W0, w0, w1, xg.x, xg.y, rs, sb);
+                    if (w < 0) {
+                        const uint32_t sel = (uint32_t)sb | ((uint32_t)(sb + 4) << 4);  // byte sb of a, of b
+                        SiteJob jb;
+                        if (NB == 8) {
+                            jb.nb_lo = __byte_perm(__byte_perm(w0.x, w0.y, sel), __byte_perm(w0.z, w0.w, sel), 0x5410);
+                            jb.nb_hi = __byte_perm(__byte_perm(w1.x, w1.y, sel), __byte_perm(w1.z, w1.w, sel), 0x5410);
+                        } else {  // UC, ML, MR, DC
+                            jb.nb_lo = __byte_perm(__byte_perm(w0.y, w0.w, sel), __byte_perm(w1.x, w1.z, sel), 0x5410);
+                            jb.nb_hi = 0u;
+                        }
+                        jb.xg = __byte_perm(xg.x, xg.y, sel) & 0xFFFFu;
+                        jb.r = rs;
+                        if (!w0_smem(LT) && LT > 2) w = decide_fp64_fixed<NB, (LT > 2 ? LT : 3)>(p, sm.A, sm.D, sm.I, jb);
+                        else if (LT == 0 && p.pfx != nullptr) w = decide_sparse<NB>(p, sm.A, jb);
+                        if (w < 0) w = decide_fp64<NB>(p, sm.A, jb);
+                    }
                     res[i] = (uint8_t)w;
                 }
                 __syncwarp();
@@ -342,7 +388,6 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
             }
         }
         if (act) {
-            uint8_t* op = x_out + chain * G.xchain + (long long)(r + HALO) * G.xpitch + XOFF + c0;
             auto store = [&](uint8_t* dst) {
                 if (nvalid == 4) *reinterpret_cast<uint32_t*>(dst) = outw;
                 else for (int b = 0; b < nvalid; ++b) dst[b] = (uint8_t)(outw >> (8 * b));
@@ -362,7 +407,6 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 if (r >= G.rows - HALO) store(op - (long long)G.rows * G.xpitch);
             }
             if (count_enable) {
-                uint16_t* cp = p.c.counts + chain * G.cchain + (long long)r * G.cpitch + c0;
                 if (nvalid == 4) {
                     // the quad's 4 counters of a plane form one 8-byte word; each distinct label
                     // of the quad adds its per-site increments with one fire-and-forget 64-bit
@@ -374,10 +418,9 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                             ((unsigned long long)__byte_perm(outw, 0u, 0x4342) << 32);
                         if (inc) atomicAdd(reinterpret_cast<unsigned long long*>(cp), inc);
                     } else {
-                        unsigned todo = 0xFu;
-                        while (todo) {
-                            const int b0 = __ffs(todo) - 1;
-                            const uint32_t k = (outw >> (8 * b0)) & 0xFFu;
+                        uint32_t rem = 0x01010101u;  // bit 8b: site b still to count
+                        do {
+                            const uint32_t k = __byte_perm(outw, 0u, 0x4440u + ((__ffs(rem) - 1) >> 3));
                             // bytes equal to k -> 0x01 per byte
                             const uint32_t e = outw ^ (k * 0x01010101u);
                             const uint32_t nz = (((e & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | e) & 0x80808080u;
@@ -386,9 +429,8 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                                 (unsigned long long)__byte_perm(eq, 0u, 0x4140) |
                                 ((unsigned long long)__byte_perm(eq, 0u, 0x4342) << 32);
                             atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)k * G.cplane), inc);
-                            todo &= ~(unsigned)(((eq & 1u) ? 1u : 0u) | ((eq & 0x100u) ? 2u : 0u) |
-                                                ((eq & 0x10000u) ? 4u : 0u) | ((eq & 0x1000000u) ? 8u : 0u));
-                        }
+                            rem &= ~eq;
+                        } while (rem);
                     }
                 } else {
                     for (int b = 0; b < nvalid; ++b) {
@@ -404,6 +446,8 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
             up[j] = mid[j];
             mid[j] = dn[j];
         }
+        op += G.xpitch;
+        cp += G.cpitch;
     }
 }
 
