@@ -10,7 +10,8 @@
 // (no inertia term), inverse-CDF draw with the site's Philox word of tag
 // GIBBS.  levels == 2: integer thresholds for every (n_present, n_1,
 // g_i) -- exact; levels > 2: the uniform-neighbourhood threshold table (levels <= 16) or
-// fp64 weights, as in sweep_general.cu.
+// fp64 weights, as in sweep_general.cu, specialised at compile time for 3, 5, 9 and 16
+// levels (tables in shared memory, unrolled fp64 path).
 //
 // Thread = 4 consecutive sites of a row (one Philox call), walking a run of rows with a
 // rolling window (as sweep_general.cu).  Moore-8 launches cover only the rows of the
@@ -108,19 +109,71 @@ __device__ int gibbs_fp64(const GibbsSweepParams& p, const double* sA, const Gib
     return L - 1;
 }
 
+// levels known at compile time (3, 5, 9, 16): the neighbour histogram is built once as
+// nibbles, the weights A[n_s] D[g][s] stay in registers, the CDF scan is branch-free (the
+// products and sums are those of gibbs_fp64, so the decisions are the same).  Returns -1 when
+// Z under/overflows (the caller takes the log-domain path).
+constexpr int GB_LMAX = 16;   // D table in shared memory up to 16 levels
+constexpr int GB_UMAX = 9;    // uniform thresholds in shared memory up to 9 levels
+template <int NB, int L>
+__device__ __forceinline__ int gibbs_fp64_fixed(const double* sA, const double* sD, const GibbsJob& j) {
+    uint64_t hist = 0;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const uint32_t v = ((q < 4 ? j.nb_lo : j.nb_hi) >> (8 * (q & 3))) & 0xFFu;
+        hist += (v < (uint32_t)L) ? (1ull << (4 * v)) : 0ull;  // sentinel 0xFF never counts
+    }
+    const double* Drow = sD + (int)j.g * L;
+    double w[L];
+    double Z = 0.0;
+#pragma unroll
+    for (int s = 0; s < L; ++s) {
+        w[s] = sA[(int)((hist >> (4 * s)) & 0xFull)] * Drow[s];
+        Z += w[s];
+    }
+    if (!(Z >= 1e-290 && Z <= 1e290)) return -1;
+    const double target = (double)j.r * (1.0 / 4294967296.0) * Z;
+    // F_k is non-decreasing: min{k < L-1 : target < F_k} (else L-1) = #{k < L-1 : F_k <= target}
+    double F = 0.0;
+    int res = 0;
+#pragma unroll
+    for (int s = 0; s < L - 1; ++s) {
+        F += w[s];
+        res += (F <= target) ? 1 : 0;
+    }
+    return res;
+}
+
 struct GibbsSmem {
     double A[9];
+    double D[GB_LMAX * GB_LMAX];
     uint32_t T[GIBBS_THR2];
+    uint32_t U[GB_UMAX * GB_UMAX * (GB_UMAX - 1)];
     GibbsJob jobs[GB_WARPS][64];
     uint8_t res[GB_WARPS][64];
 };
 
+// stage the launch's tables: A, and per level count the binary thresholds, or D and the
+// uniform-neighbourhood thresholds
+template <int LT>
+__device__ __forceinline__ void gibbs_load_tables(const GibbsSweepParams& p, GibbsSmem& sm) {
+    if (threadIdx.x < 9) sm.A[threadIdx.x] = p.A[threadIdx.x];
+    if (LT == 2)
+        for (int i = threadIdx.x; i < GIBBS_THR2; i += GB_THREADS) sm.T[i] = p.thr2[i];
+    if (LT > 2 && LT <= GB_LMAX)
+        for (int i = threadIdx.x; i < LT * LT; i += GB_THREADS) sm.D[i] = p.dtab[i];
+    if (LT > 2 && LT <= GB_UMAX && p.uthr != nullptr)
+        for (int i = threadIdx.x; i < LT * LT * (LT - 1); i += GB_THREADS) sm.U[i] = p.uthr[i];
+}
+
 // One launch's work for x-block xb, row block rb of chain `chain`: colour k (FUSED: row parity
 // k), sweep t.  COH: x is read through L2 (ld.global.cg) because earlier phases of the same
 // cooperative launch wrote it.
-template <int NB, bool BIN, bool FUSED, bool COH>
+template <int NB, int LT, bool FUSED, bool COH>  // LT: levels at compile time (2 = binary), 0 = any
 __device__ __forceinline__ void gibbs_rows(const GibbsSweepParams& p, GibbsSmem& sm, int k, uint32_t t,
                                            int count_enable, int xb, int rb, int chain, int R) {
+    constexpr bool BIN = LT == 2;
+    constexpr bool SMEM_U = LT > 2 && LT <= GB_UMAX;
     const double* sA = sm.A;
     const uint32_t* sT = sm.T;
     const Geometry& G = p.c.geo;
@@ -217,7 +270,18 @@ __device__ __forceinline__ void gibbs_rows(const GibbsSweepParams& p, GibbsSmem&
                     const int gi = (int)((gword >> (8 * b)) & 0xFFu);
                     const int s0 = (int)((S0 >> (8 * b)) & 0xFFu);
                     const bool uniform = p.uthr != nullptr && ((differ >> (8 * b + 7)) & 1u) == 0u && s0 < L;
-                    if (my && uniform) {
+                    if (SMEM_U) {
+                        // branch-free: every lane reads a row (row 0 unless its site is a uniform
+                        // one of this colour) and counts the thresholds T_k >= r with borrow bits
+                        const bool uni = my && uniform;
+                        const uint32_t* T = sm.U + (uni ? (s0 * LT + gi) * (LT - 1) : 0);
+                        uint32_t ge = 0;
+#pragma unroll
+                        for (int kk = 0; kk < (SMEM_U ? LT - 1 : 1); ++kk)
+                            asm("{\n\t.reg .u32 d;\n\tsub.cc.u32 d, %1, %2;\n\taddc.u32 %0, %0, 0;\n\t}"
+                                : "+r"(ge) : "r"(T[kk]), "r"(rr[b]));
+                        if (uni) outw = (outw & ~(0xFFu << (8 * b))) | (((uint32_t)(LT - 1) - ge) << (8 * b));
+                    } else if (my && uniform) {
                         const uint32_t* T = p.uthr + (size_t)(s0 * L + gi) * (L - 1);
                         int w = 0;
                         for (int kk = 0; kk < L - 1; ++kk) w += (rr[b] > __ldg(T + kk)) ? 1 : 0;
@@ -244,7 +308,12 @@ __device__ __forceinline__ void gibbs_rows(const GibbsSweepParams& p, GibbsSmem&
                 }
                 if (qbase > 0) {
                     __syncwarp();
-                    for (int i = lane; i < qbase; i += 32) res[i] = (uint8_t)gibbs_fp64<NB>(p, sA, jobs[i]);
+                    for (int i = lane; i < qbase; i += 32) {
+                        int w = -1;
+                        if (LT > 2) w = gibbs_fp64_fixed<NB, (LT > 2 ? LT : 3)>(sA, sm.D, jobs[i]);
+                        if (w < 0) w = gibbs_fp64<NB>(p, sA, jobs[i]);
+                        res[i] = (uint8_t)w;
+                    }
                     __syncwarp();
 #pragma unroll
                     for (int b = 0; b < 4; ++b)
@@ -392,27 +461,23 @@ __device__ __forceinline__ void gibbs_rows(const GibbsSweepParams& p, GibbsSmem&
     }
 }
 
-template <int NB, bool BIN, bool FUSED>
+template <int NB, int LT, bool FUSED>
 __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
     sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
     __shared__ GibbsSmem sm;
-    if (threadIdx.x < 9) sm.A[threadIdx.x] = p.A[threadIdx.x];
-    if (BIN)
-        for (int i = threadIdx.x; i < GIBBS_THR2; i += GB_THREADS) sm.T[i] = p.thr2[i];
+    gibbs_load_tables<LT>(p, sm);
     __syncthreads();
-    gibbs_rows<NB, BIN, FUSED, false>(p, sm, p.colour, p.c.t, p.c.count_enable, blockIdx.x,
+    gibbs_rows<NB, LT, FUSED, false>(p, sm, p.colour, p.c.t, p.c.count_enable, blockIdx.x,
                                       blockIdx.y, blockIdx.z, R);
 }
 
 // Small lattices: `nsweeps` Gibbs sweeps (one beta stage; p.c.count_enable = counting in the
 // whole run) in one cooperative launch, every colour phase followed by a grid barrier.
-template <int NB, bool BIN, bool FUSED>
+template <int NB, int LT, bool FUSED>
 __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
     gibbs_multi_kernel(const __grid_constant__ GibbsSweepParams p, int R, int nrb, int nsweeps, int batch) {
     __shared__ GibbsSmem sm;
-    if (threadIdx.x < 9) sm.A[threadIdx.x] = p.A[threadIdx.x];
-    if (BIN)
-        for (int i = threadIdx.x; i < GIBBS_THR2; i += GB_THREADS) sm.T[i] = p.thr2[i];
+    gibbs_load_tables<LT>(p, sm);
     __syncthreads();
     const int xblocks = (((p.c.geo.W + 3) >> 2) + GB_THREADS - 1) / GB_THREADS;
     const int items = xblocks * nrb * batch;
@@ -422,7 +487,7 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
             const int cnt = p.c.count_enable && (FUSED || (k & 1));
             for (int it = blockIdx.x; it < items; it += gridDim.x) {
                 const int xb = it % xblocks, rb = (it / xblocks) % nrb, chain = it / (xblocks * nrb);
-                gibbs_rows<NB, BIN, FUSED, true>(p, sm, k, p.c.t + (uint32_t)sw, cnt, xb, rb, chain, R);
+                gibbs_rows<NB, LT, FUSED, true>(p, sm, k, p.c.t + (uint32_t)sw, cnt, xb, rb, chain, R);
             }
             if (gridDim.x == 1) {
                 __syncthreads();
@@ -434,7 +499,7 @@ __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
     }
 }
 
-template <int NB, bool BIN, bool FUSED>
+template <int NB, int LT, bool FUSED>
 int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s) {
     static LaunchInfo info[MAX_DEVICES];
     LaunchInfo& li = info[current_device()];
@@ -442,8 +507,8 @@ int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s)
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_gibbs_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, gibbs_multi_kernel<NB, BIN, FUSED>, GB_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_gibbs_kernel<NB, LT, FUSED>, GB_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, gibbs_multi_kernel<NB, LT, FUSED>, GB_THREADS, 0);
         if (li.occ < 1) li.occ = 1;
         if (li.mocc < 1) li.mocc = 1;
         li.ok = true;
@@ -470,11 +535,11 @@ int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s)
         GibbsSweepParams pp = p;
         int Ri = (int)R, nrbi = (int)nrb, ns = nsweeps, b = batch;
         void* args[] = {&pp, &Ri, &nrbi, &ns, &b};
-        return (int)cudaLaunchCooperativeKernel((const void*)gibbs_multi_kernel<NB, BIN, FUSED>, dim3(grid),
+        return (int)cudaLaunchCooperativeKernel((const void*)gibbs_multi_kernel<NB, LT, FUSED>, dim3(grid),
                                                 dim3(GB_THREADS), args, 0, s);
     }
     dim3 grid((unsigned)xblocks, (unsigned)nrb, batch);
-    sweep_gibbs_kernel<NB, BIN, FUSED><<<grid, GB_THREADS, 0, s>>>(p, (int)R);
+    sweep_gibbs_kernel<NB, LT, FUSED><<<grid, GB_THREADS, 0, s>>>(p, (int)R);
     return (int)cudaGetLastError();
 }
 
@@ -483,13 +548,19 @@ int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s)
 int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, int nsweeps, void* stream) {
     const Geometry& G = p.c.geo;
     cudaStream_t s = (cudaStream_t)stream;
-    const bool bin = G.levels == 2;
-    if (G.nbhd == 8) {
-        if (p.fused)
-            return bin ? launch_gb<8, true, true>(p, batch, nsweeps, s) : launch_gb<8, false, true>(p, batch, nsweeps, s);
-        return bin ? launch_gb<8, true, false>(p, batch, nsweeps, s) : launch_gb<8, false, false>(p, batch, nsweeps, s);
+#define PCA_GB_LAUNCH(LTV)                                                                     \
+    return G.nbhd == 8 ? (p.fused ? launch_gb<8, LTV, true>(p, batch, nsweeps, s)              \
+                                  : launch_gb<8, LTV, false>(p, batch, nsweeps, s))            \
+                       : launch_gb<4, LTV, false>(p, batch, nsweeps, s)
+    switch (G.levels) {  // two levels: the exact binary path; the paper's level counts (and 3)
+        case 2: PCA_GB_LAUNCH(2);  // get fully unrolled fp64 paths
+        case 3: PCA_GB_LAUNCH(3);
+        case 5: PCA_GB_LAUNCH(5);
+        case 9: PCA_GB_LAUNCH(9);
+        case 16: PCA_GB_LAUNCH(16);
+        default: PCA_GB_LAUNCH(0);
     }
-    return bin ? launch_gb<4, true, false>(p, batch, nsweeps, s) : launch_gb<4, false, false>(p, batch, nsweeps, s);
+#undef PCA_GB_LAUNCH
 }
 
 }  // namespace pcab200
