@@ -18,6 +18,8 @@ SHAPES = [
     (64, 64, 2, 4, True), (64, 64, 2, 8, True), (37, 531, 2, 8, False), (19, 1000, 2, 4, False),
     (40, 130, 5, 8, False), (30, 62, 9, 4, True), (31, 45, 33, 8, False), (1, 77, 2, 8, False),
     (77, 1, 5, 4, False), (2, 2, 3, 8, False), (8, 48, 2, 8, True), (6, 10, 255, 8, True),
+    # compile-time level counts: 3 and 9 (tables in shared memory), 16 (D only), 4 and 8 nbrs
+    (20, 36, 3, 4, True), (22, 40, 9, 8, False), (20, 36, 16, 8, True), (18, 41, 16, 4, False),
 ]
 
 
@@ -95,7 +97,7 @@ def test_gibbs_batch_equals_independent_chains(cuda_device):
 
 
 @pytest.mark.parametrize("extreme", [dict(sigma=0.01), dict(beta0=300.0)])
-@pytest.mark.parametrize("L", [2, 5, 33])
+@pytest.mark.parametrize("L", [2, 3, 5, 9, 16, 33])
 def test_gibbs_extreme_parameters(cuda_device, extreme, L):
     """Weights that under/overflow the factorised fp64 form take the log-domain path."""
     H, W = 24, 40

@@ -27,6 +27,9 @@ SHAPES = [
     (9, 23, 255, 8, True), (2, 2, 3, 8, False), (1, 1, 5, 8, False),
     # W % 16 == 0 with 3, 5, 9 levels: the general sweep's TMA path (several segments, ragged)
     (21, 48, 3, 8, True), (37, 1040, 5, 8, False), (30, 64, 9, 4, True), (5, 16, 5, 8, False),
+    # the compile-time level counts with 4 neighbours (shared-memory W0 weights, SWAR table
+    # rows) and 16 levels (the largest fixed path)
+    (26, 70, 5, 4, False), (20, 36, 3, 4, True), (23, 50, 16, 8, True), (18, 41, 16, 4, False),
 ]
 
 
@@ -356,7 +359,7 @@ def test_error_paths(cuda_device):
 
 
 @pytest.mark.parametrize("kernel", [P.KERNEL_AUTO, P.KERNEL_GENERAL])
-@pytest.mark.parametrize("levels", [2, 5, 33])
+@pytest.mark.parametrize("levels", [2, 3, 5, 9, 16, 33])
 @pytest.mark.parametrize("extreme", [dict(sigma=0.01), dict(q=1e6), dict(beta0=300.0),
                                      dict(sigma=0.02, q=500.0)])
 def test_lockstep_extreme_parameters(cuda_device, kernel, levels, extreme):
