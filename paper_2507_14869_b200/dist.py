@@ -6,6 +6,10 @@
   (pca_nccl_unique_id) and torch.distributed broadcasts its 128 bytes.
 * ``strip_context``: a PcaContext for this rank's strip with NCCL attached.
 * ``chain_range``: the batch-mode partition of independent chains (replicas only).
+* ``batch_context``: a PcaContext for this rank's chain range (chain0 = its first global
+  chain, so every chain draws the same Philox words whatever the world size).
+* ``gather_chain_metrics``: the per-chain PSNR/SSIM of every rank, assembled on rank 0 in
+  global chain order (C5's final gather).
 
 The per-sweep halo exchange itself runs inside the library (runtime.cu ``exchange``):
 after each sweep a rank sends its first owned row to ``up`` and its last to ``down`` and
@@ -61,3 +65,41 @@ def strip_context(cfg_kwargs: dict, H: int, W: int, levels: int, g_strip, *, str
     if world > 1:
         ctx.pca_attach_nccl(broadcast_unique_id(group), world, rank)
     return ctx
+
+
+def batch_context(cfg_kwargs: dict, H: int, W: int, levels: int, g_all, n_chains: int, *,
+                  world: int | None = None, rank: int | None = None, stream=None, group=None):
+    """Batch mode (replicas only): this rank's contiguous range of the `n_chains` independent
+    chains.  `g_all` holds every chain's observed image ([n_chains][H][W], host or device);
+    only this rank's slice is uploaded.  Returns (context, chain0).  `world` / `rank` default
+    to the process group's."""
+    from . import PcaContext, make_config
+
+    if world is None or rank is None:
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    chain0, batch = chain_range(n_chains, world, rank)
+    cfg = make_config(H, W, levels, batch=batch, chain0=chain0, **cfg_kwargs)
+    return PcaContext(cfg, g_all[chain0:chain0 + batch], stream=stream), chain0
+
+
+def gather_chain_metrics(chain0: int, psnr, ssim, n_chains: int, group=None):
+    """Every rank passes its chain0 and its [batch][2] PSNR / SSIM arrays (LAST, MPM); rank 0
+    returns the [n_chains][2] arrays in global chain order, the other ranks (None, None)."""
+    import numpy as np
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    parts = [None] * world
+    dist.all_gather_object(parts, (int(chain0), np.asarray(psnr), np.asarray(ssim)), group=group)
+    if rank != 0:
+        return None, None
+    P = np.full((n_chains, 2), np.nan)
+    S = np.full((n_chains, 2), np.nan)
+    for c0, p, s in parts:
+        P[c0:c0 + len(p)] = p
+        S[c0:c0 + len(s)] = s
+    if np.isnan(S).any():
+        raise ValueError("the ranks' chain ranges do not cover every chain")
+    return P, S

@@ -156,3 +156,40 @@ def test_partition_and_peers():
     assert pdist.chain_range(1024, 8, 3) == (384, 128)
     with pytest.raises(ValueError):
         pdist.strip_rows(2, 3, 0)
+
+
+def _gather_worker(rank, world, port, n_chains, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        chain0, batch = pdist.chain_range(n_chains, world, rank)
+        chains = np.arange(chain0, chain0 + batch, dtype=float)
+        psnr = np.stack([chains, chains + 0.5], axis=1)       # a value that names its chain
+        ssim = np.stack([chains / 100, chains / 100 + 0.005], axis=1)
+        P, S = pdist.gather_chain_metrics(chain0, psnr, ssim, n_chains)
+        if rank == 0:
+            want = np.arange(n_chains, dtype=float)
+            out_q.put(bool(np.array_equal(P[:, 0], want) and np.array_equal(P[:, 1], want + 0.5)
+                           and np.allclose(S[:, 0], want / 100)))
+        else:
+            out_q.put(P is None and S is None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_chains", [(2, 7), (3, 1024)])
+def test_batch_mode_gathers_chain_metrics_in_global_order(world, n_chains):
+    """C5's final gather: each rank's chain range, metrics assembled on rank 0."""
+    if world > n_chains:
+        pytest.skip("fewer chains than ranks")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n_chains, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res)

@@ -654,3 +654,31 @@ def test_packed_io_matches_dense_io(cuda_device, W):
     for c in (dense, packed):
         c.pca_sweep(2)
     assert np.array_equal(P.unpack_bits(packed.state(), W), dense.state())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_mode_ranks_equal_one_context(cuda_device, world):
+    """Batch mode (replicas only): splitting the chains over `world` rank
+    contexts (dist.batch_context; here in one process, the contexts never wait on each other)
+    gives every chain the same trajectory, counts and metrics as one context holding them
+    all -- the chain0 offset keys the Philox words by global chain index."""
+    from paper_2507_14869_b200 import dist as pdist
+
+    n, H, W, L = 7, 40, 72, 5
+    truth = np.stack([synth.smooth_labels(H, W, L, seed=10 + c % 3) for c in range(n)])
+    g = np.stack([synth.degrade(truth[c], L, 0.25, seed=50 + c) for c in range(n)])
+    kw = dict(sigma=0.25, beta_period=6, mpm_burn_in=8, seed=77)
+    whole = P.PcaContext(P.make_config(H, W, L, batch=n, **kw), g)
+    whole.pca_sweep(14)
+    psnr_w, ssim_w = whole.pca_finalize(truth)
+    x_w, c_w = whole.state(), whole.counts()
+    psnr, ssim = np.zeros((n, 2)), np.zeros((n, 2))
+    for r in range(world):
+        ctx, c0 = pdist.batch_context(kw, H, W, L, g, n, world=world, rank=r)
+        b = ctx.cfg.batch
+        ctx.pca_sweep(14)
+        psnr[c0:c0 + b], ssim[c0:c0 + b] = ctx.pca_finalize(truth[c0:c0 + b])
+        assert np.array_equal(ctx.state(), x_w[c0:c0 + b])
+        assert np.array_equal(ctx.counts(), c_w[c0:c0 + b])
+        ctx.pca_destroy()
+    assert np.array_equal(psnr, psnr_w) and np.array_equal(ssim, ssim_w)
