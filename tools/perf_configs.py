@@ -3,7 +3,8 @@
     python tools/perf_configs.py [--quick]
 
 config 1 (64x64 binary torus), config 2 (256x256 Moore free, l = 5/9/33, paper schedule),
-config 3 variants (8192^2: l = 2 MPM on/off, 4-neighbour, free boundary; l = 5),
+config 3 variants (8192^2: l = 2 MPM on/off, 4-neighbour, free boundary; l = 5), the config-4
+per-GPU shape (4096 x 32768) on one GPU,
 config 5 per GPU (128 chains of 512x512, l = 5, paper protocol).
 """
 import json
@@ -55,6 +56,10 @@ def main():
         kw2 = dict(neighborhood=8, periodic=True)
         kw2.update(kw)
         out.append(time_cfg(name, P.make_config(8192, 8192, 2, sigma=0.5, beta0=1.5, beta_step=0, **kw2), big, 50))
+    c4 = synth.degrade(synth.tiled_labels(4096, 32768, 2, 1), 2, 0.5, 2)[None]
+    out.append(time_cfg("c4 per-GPU shape 4096x32768 l2 moore torus mpm (1 GPU, whole torus)",
+                        P.make_config(4096, 32768, 2, periodic=True, sigma=0.5, beta0=1.5, beta_step=0,
+                                      mpm_burn_in=0), c4, 50))
     if not quick:
         big5 = synth.degrade(synth.tiled_labels(8192, 8192, 5, 1), 5, 0.25, 2)[None]
         out.append(time_cfg("c3 l5 moore torus mpm", P.make_config(8192, 8192, 5, periodic=True, sigma=0.25, beta0=1.5, beta_step=0, mpm_burn_in=0), big5, 10))
