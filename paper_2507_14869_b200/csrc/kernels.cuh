@@ -16,6 +16,8 @@
 //   sums   : uint64 [batch][8] metric accumulators
 //   stage  : uint8 [batch][rows][W] (+ fp32 space for MARGINALS/CM) host<->device staging
 #pragma once
+#include <atomic>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -144,10 +146,16 @@ struct MetricParams {
 
 // Per-device launch facts (occupancy, SM count) cached on first use on each device:
 // cudaFuncSetAttribute and occupancy are per device, so one process may drive several GPUs.
+// Filled once per device under launch_info_mutex() (double-checked: `ok` is released after
+// the fields are written), so host threads may launch concurrently.
 struct LaunchInfo {
-    bool ok = false;
+    std::atomic<bool> ok{false};
     int occ = 1, mocc = 1, sms = 1;
 };
+inline std::mutex& launch_info_mutex() {
+    static std::mutex m;
+    return m;
+}
 constexpr int MAX_DEVICES = 64;
 inline int current_device() {
     int d = 0;

@@ -454,17 +454,20 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     const Geometry& G = p.c.geo;
     static LaunchInfo info[MAX_DEVICES];
     LaunchInfo& li = info[current_device()];
-    if (!li.ok) {
-        cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, RingCfg<PER>::SMEM);
-        if (e != cudaSuccess) return (int)e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_binary_kernel<NB, PER>, 32,
-                                                      RingCfg<PER>::SMEM);
-        if (li.occ < 1) li.occ = 1;
-        li.ok = true;
+    if (!li.ok.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lock(launch_info_mutex());
+        if (!li.ok.load(std::memory_order_relaxed)) {
+            cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, RingCfg<PER>::SMEM);
+            if (e != cudaSuccess) return (int)e;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_binary_kernel<NB, PER>, 32,
+                                                          RingCfg<PER>::SMEM);
+            if (li.occ < 1) li.occ = 1;
+            li.ok.store(true, std::memory_order_release);
+        }
     }
     const int occ = li.occ, sms = li.sms;
     if (R <= 0) {

@@ -508,18 +508,21 @@ struct GenLaunch {
     static LaunchInfo& get() {
         static LaunchInfo info[MAX_DEVICES];
         LaunchInfo& li = info[current_device()];
-        if (!li.ok) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
-            const int smem = (int)sizeof(GenSmem<LT>);
-            cudaFuncSetAttribute(sweep_general_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            cudaFuncSetAttribute(sweep_multi_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_general_kernel<NB, LT>, GEN_THREADS, smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, sweep_multi_kernel<NB, LT>, GEN_THREADS, smem);
-            if (li.occ < 1) li.occ = 1;
-            if (li.mocc < 1) li.mocc = 1;
-            li.ok = true;
+        if (!li.ok.load(std::memory_order_acquire)) {
+            std::lock_guard<std::mutex> lock(launch_info_mutex());
+            if (!li.ok.load(std::memory_order_relaxed)) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+                const int smem = (int)sizeof(GenSmem<LT>);
+                cudaFuncSetAttribute(sweep_general_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                cudaFuncSetAttribute(sweep_multi_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_general_kernel<NB, LT>, GEN_THREADS, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, sweep_multi_kernel<NB, LT>, GEN_THREADS, smem);
+                if (li.occ < 1) li.occ = 1;
+                if (li.mocc < 1) li.mocc = 1;
+                li.ok.store(true, std::memory_order_release);
+            }
         }
         return li;
     }

@@ -503,15 +503,18 @@ template <int NB, int LT, bool FUSED>
 int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s) {
     static LaunchInfo info[MAX_DEVICES];
     LaunchInfo& li = info[current_device()];
-    if (!li.ok) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_gibbs_kernel<NB, LT, FUSED>, GB_THREADS, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, gibbs_multi_kernel<NB, LT, FUSED>, GB_THREADS, 0);
-        if (li.occ < 1) li.occ = 1;
-        if (li.mocc < 1) li.mocc = 1;
-        li.ok = true;
+    if (!li.ok.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lock(launch_info_mutex());
+        if (!li.ok.load(std::memory_order_relaxed)) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_gibbs_kernel<NB, LT, FUSED>, GB_THREADS, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, gibbs_multi_kernel<NB, LT, FUSED>, GB_THREADS, 0);
+            if (li.occ < 1) li.occ = 1;
+            if (li.mocc < 1) li.mocc = 1;
+            li.ok.store(true, std::memory_order_release);
+        }
     }
     const int occ = li.occ, mocc = li.mocc, sms = li.sms;
     const Geometry& G = p.c.geo;

@@ -258,15 +258,18 @@ template <bool PER>
 int launch_gb2(const GibbsBinParams& p, int batch, cudaStream_t s) {
     static LaunchInfo info[MAX_DEVICES];
     LaunchInfo& li = info[current_device()];
-    if (!li.ok) {
-        cudaError_t e = cudaFuncSetAttribute(gibbs_binary_kernel<PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
-        if (e != cudaSuccess) return (int)e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, gibbs_binary_kernel<PER>, 32, GSMEM);
-        if (li.occ < 1) li.occ = 1;
-        li.ok = true;
+    if (!li.ok.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lock(launch_info_mutex());
+        if (!li.ok.load(std::memory_order_relaxed)) {
+            cudaError_t e = cudaFuncSetAttribute(gibbs_binary_kernel<PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
+            if (e != cudaSuccess) return (int)e;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, gibbs_binary_kernel<PER>, 32, GSMEM);
+            if (li.occ < 1) li.occ = 1;
+            li.ok.store(true, std::memory_order_release);
+        }
     }
     const int occ = li.occ, sms = li.sms;
     const Geometry& G = p.c.geo;
