@@ -682,3 +682,34 @@ def test_batch_mode_ranks_equal_one_context(cuda_device, world):
         assert np.array_equal(ctx.counts(), c_w[c0:c0 + b])
         ctx.pca_destroy()
     assert np.array_equal(psnr, psnr_w) and np.array_equal(ssim, ssim_w)
+
+
+def test_contexts_driven_from_concurrent_host_threads(cuda_device):
+    """Independent contexts may be driven from several host threads at once (ctypes drops
+    the GIL around every ABI call; the per-device launch caches initialise under a lock):
+    each thread's chain equals the same chain run alone."""
+    import threading
+
+    shapes = [(48, 96, 2, 8, True), (40, 72, 5, 8, False), (34, 64, 9, 4, True), (64, 128, 2, 4, False)]
+    def run(shape, out, i):
+        H, W, L, nb, per = shape
+        cfg = P.make_config(H, W, L, neighborhood=nb, periodic=per, sigma=0.3, seed=100 + i,
+                            mpm_burn_in=3, beta_period=4)
+        g = synth.degrade(synth.smooth_labels(H, W, L, seed=i), L, 0.3, seed=20 + i)
+        ctx = P.PcaContext(cfg, g)
+        ctx.pca_sweep(9)
+        ctx.pca_gibbs_sweep(2)
+        out[i] = (ctx.state(), ctx.counts())
+        ctx.pca_destroy()
+
+    alone = {}
+    for i, sh in enumerate(shapes):
+        run(sh, alone, i)
+    together = {}
+    threads = [threading.Thread(target=run, args=(sh, together, i)) for i, sh in enumerate(shapes)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for i in range(len(shapes)):
+        assert np.array_equal(alone[i][0], together[i][0]) and np.array_equal(alone[i][1], together[i][1])
