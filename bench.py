@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rows-per-thread", type=int, default=0)
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: halo rows by NCCL send/recv (default) or stored by the sweep "
+                         "kernel straight into the neighbours' memory (pca_attach_peers, CUDA IPC)")
     return ap.parse_args()
 
 
@@ -231,8 +234,11 @@ def run_ours(args):
     kw = dict(neighborhood=wl["nbhd"], periodic=wl["periodic"], sigma=wl["sigma"], q=0.51,
               beta0=wl["beta"], beta_step=0.0, beta_period=1 << 30, seed=11, mpm_burn_in=0,
               rows_per_thread=args.rows_per_thread)
+    peers = []
     if world > 1:  # this rank's row strip, NCCL attached (unique id broadcast by torch.distributed)
         ctx = pdist.strip_context(kw, wl["H"], W, wl["levels"], g_dev, stream=stream)
+        if args.halo == "p2p":  # halo rows stored by the sweep kernels into the neighbours' memory
+            peers += pdist.attach_peers_ipc(ctx, kw, wl["H"], W, wl["levels"])
     else:
         ctx = P.PcaContext(P.make_config(wl["H"], W, wl["levels"], **kw), g_dev, stream=stream)
     S = args.sweeps
@@ -301,6 +307,8 @@ def run_ours(args):
         mpm_h = torch.empty(tuple(t_h.shape), dtype=torch.uint8).pin_memory()
         if world > 1:
             ectx = pdist.strip_context(kw_e, wl["H"], W, wl["levels"], g_h, stream=stream)
+            if args.halo == "p2p":
+                peers += pdist.attach_peers_ipc(ectx, kw_e, wl["H"], W, wl["levels"])
         else:
             ectx = P.PcaContext(P.make_config(wl["H"], W, wl["levels"], **kw_e), g_h, stream=stream)
 
@@ -349,9 +357,13 @@ def run_ours(args):
         halo = {"sweep_us_sharded": sweep_s * 1e6, "sweep_us_local_only": local_us,
                 "exposed_us_per_sweep": sweep_s * 1e6 - local_us,
                 "messages_per_sweep_per_rank": 4, "bytes_per_message": 16 * ((W + 15) // 16) + 32,  # one padded row (depth 1)
-                "method": "max over ranks of S sharded sweeps (edge rows + NCCL send/recv "
-                          "overlapping the interior) minus S sweeps of the same strip as an "
-                          "isolated torus (no exchange)"}
+                "halo_exchange": args.halo,
+                "method": ("max over ranks of S sharded sweeps (edge rows + NCCL send/recv "
+                           "overlapping the interior)" if args.halo == "nccl" else
+                           "max over ranks of S sharded sweeps (one launch per sweep storing the "
+                           "edge rows into the neighbours' halo rows over peer memory, stream "
+                           "waits/writes of phase words)") +
+                          " minus S sweeps of the same strip as an isolated torus (no exchange)"}
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
@@ -367,7 +379,7 @@ def run_ours(args):
                        "step": "reset + S fused sweeps (MPM on) + fused finalisation (MPM image, "
                                "PSNR/SSIM of LAST and MPM in one pass)",
                        "l2": "working set ~320 MiB/GPU > 126 MB L2: inputs larger than L2, no flush",
-                       "parallelism": wl["parallelism"],
+                       "parallelism": wl["parallelism"] + (f", halo {args.halo}" if world > 1 else ""),
                        "psnr_ssim_last": [float(psnr[0, 0]), float(ssim[0, 0])],
                        "psnr_ssim_mpm": [float(psnr[0, 1]), float(ssim[0, 1])]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -386,7 +398,9 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     ctx.pca_destroy()
     if dist:
-        dist.barrier()
+        dist.barrier()  # every rank's stores into its neighbours' memory are complete
+        for q in peers:
+            P.pca_close_peer(q)
         dist.destroy_process_group()
     return 0
 

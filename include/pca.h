@@ -146,6 +146,20 @@ typedef struct pca_halo {
     size_t chain_stride;
 } pca_halo;
 
+/* Device-initiated halo exchange: what a strip context needs to know
+ * about a neighbouring rank's context.  x[0], x[1]: the peer's two state buffers (padded row
+ * -2 of chain 0, device pointers valid in THIS process); flags: the peer's two phase words;
+ * chain_stride: bytes between its chains; ipc_base: the mapping pca_open_peer made (release
+ * it with pca_close_peer), NULL for an in-process peer from pca_peer_info. */
+typedef struct pca_peer {
+    uint8_t* x[2];
+    uint32_t* flags;
+    void* ipc_base;
+    int32_t rows;
+    int32_t batch;
+    int64_t chain_stride;
+} pca_peer;
+
 /* Version of this ABI (PCA_ABI_VERSION). */
 int32_t pca_abi_version(void);
 
@@ -256,6 +270,34 @@ pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out);
  * pca_attach_nccl creates the communicator owned by the context. */
 pca_status pca_nccl_unique_id(void* id128);
 pca_status pca_attach_nccl(pca_ctx* ctx, const void* id128, int32_t nranks, int32_t rank);
+
+/* Device-initiated halo exchange over peer memory (the per-sweep
+ * exchange of PAPER.md's synchronous update across row strips), an alternative
+ * to NCCL for PCA sweeps on row strips:
+ *   pca_peer_info   this context's buffers and phase words (for a peer in the same process);
+ *   pca_ipc_handle  the CUDA IPC handle (64 bytes) of the allocation holding the workspace and
+ *                   the workspace's byte offset in it, for a peer in another process;
+ *   pca_open_peer   maps another process's workspace (handle, offset, and that rank's config:
+ *                   same height, width, batch) into this context's device;
+ *   pca_close_peer  unmaps it (after the contexts using it are destroyed);
+ *   pca_attach_peers  up = the rank owning the rows above this strip, down = below (NULL at a
+ *                   free-boundary end; a torus strip needs both).  Pushes the current state's
+ *                   edge rows (phase 1) and synchronises.
+ * Once attached, every PCA sweep is ONE launch whose edge-row CTAs also store the new rows
+ * into the peers' halo rows; every sweep and state load is a phase k, preceded on the stream by
+ * a wait until both peers completed phase k-1 (cuStreamWaitValue32 on this context's phase
+ * words; no kernel spins) and followed by a write of k into the peers' phase words
+ * (cuStreamWriteValue32, fenced).  Every rank must issue the same sequence of sweeps and state
+ * loads (SPMD).  Row-strip Gibbs sweeps need NCCL (PCA_EUNSUPPORTED with peers attached).  The
+ * metric reductions still use NCCL when it is attached, else they cover this strip only.
+ * Errors: PCA_EINVAL (not a strip, already attached, layout mismatch), PCA_ECUDA (IPC or
+ * stream memory operations unavailable / failed), PCA_EUNSUPPORTED (no stream memory ops). */
+pca_status pca_peer_info(pca_ctx* ctx, pca_peer* out);
+pca_status pca_ipc_handle(pca_ctx* ctx, void* handle64, uint64_t* offset);
+pca_status pca_open_peer(pca_ctx* ctx, const void* handle64, uint64_t offset, const pca_config* peer_cfg,
+                         pca_peer* out);
+pca_status pca_close_peer(pca_peer* peer);
+pca_status pca_attach_peers(pca_ctx* ctx, const pca_peer* up, const pca_peer* down);
 
 /* Synchronise the context's stream and report any pending asynchronous error. */
 pca_status pca_sync(pca_ctx* ctx);

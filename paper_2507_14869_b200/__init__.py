@@ -34,7 +34,8 @@ EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "p
            "pca_ssim_windowed", "pca_read_state",
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
-           "pca_destroy", "pca_last_error"]
+           "pca_destroy", "pca_last_error", "pca_peer_info", "pca_ipc_handle", "pca_open_peer",
+           "pca_close_peer", "pca_attach_peers"]
 
 
 class PcaError(RuntimeError):
@@ -64,6 +65,12 @@ class pca_stats(ctypes.Structure):
     _fields_ = [("sweeps_done", ctypes.c_int64), ("counted_sweeps", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("sweep_launches", ctypes.c_int64),
                 ("beta", ctypes.c_double), ("kernel", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+
+
+class pca_peer(ctypes.Structure):
+    """A neighbouring rank's buffers and phase words (device-initiated halo exchange)."""
+    _fields_ = [("x", ctypes.c_void_p * 2), ("flags", ctypes.c_void_p), ("ipc_base", ctypes.c_void_p),
+                ("rows", ctypes.c_int32), ("batch", ctypes.c_int32), ("chain_stride", ctypes.c_int64)]
 
 
 class pca_halo(ctypes.Structure):
@@ -106,6 +113,11 @@ def lib():
             "pca_set_step": (i32, [vp, i64]),
             "pca_get_stats": (i32, [vp, ctypes.POINTER(pca_stats)]),
             "pca_halo_ptrs": (i32, [vp, ctypes.POINTER(pca_halo)]),
+            "pca_peer_info": (i32, [vp, ctypes.POINTER(pca_peer)]),
+            "pca_ipc_handle": (i32, [vp, vp, ctypes.POINTER(ctypes.c_uint64)]),
+            "pca_open_peer": (i32, [vp, vp, ctypes.c_uint64, ctypes.POINTER(pca_config), ctypes.POINTER(pca_peer)]),
+            "pca_close_peer": (i32, [ctypes.POINTER(pca_peer)]),
+            "pca_attach_peers": (i32, [vp, ctypes.POINTER(pca_peer), ctypes.POINTER(pca_peer)]),
             "pca_nccl_unique_id": (i32, [vp]),
             "pca_attach_nccl": (i32, [vp, vp, i32, i32]),
             "pca_sync": (i32, [vp]),
@@ -150,6 +162,10 @@ def pca_workspace_bytes(cfg: pca_config) -> int:
     if n == 0:
         raise PcaError(PCA_EINVAL, "pca_workspace_bytes", lib().pca_last_error().decode())
     return int(n)
+
+
+def pca_close_peer(peer: pca_peer):
+    _check(lib().pca_close_peer(ctypes.byref(peer)), "pca_close_peer")
 
 
 def pca_nccl_unique_id() -> bytes:
@@ -290,6 +306,31 @@ class PcaContext:
         h = pca_halo()
         _check(lib().pca_halo_ptrs(self.handle, ctypes.byref(h)), "pca_halo_ptrs")
         return h
+
+    def pca_peer_info(self) -> pca_peer:
+        q = pca_peer()
+        _check(lib().pca_peer_info(self.handle, ctypes.byref(q)), "pca_peer_info")
+        return q
+
+    def pca_ipc_handle(self) -> tuple[bytes, int]:
+        """(64-byte CUDA IPC handle of the workspace's allocation, workspace offset in it)."""
+        buf = ctypes.create_string_buffer(64)
+        off = ctypes.c_uint64()
+        _check(lib().pca_ipc_handle(self.handle, buf, ctypes.byref(off)), "pca_ipc_handle")
+        return buf.raw, int(off.value)
+
+    def pca_open_peer(self, handle: bytes, offset: int, peer_cfg: pca_config) -> pca_peer:
+        """Map another process's workspace (its pca_ipc_handle) into this context's device."""
+        q = pca_peer()
+        buf = ctypes.create_string_buffer(handle, 64)
+        _check(lib().pca_open_peer(self.handle, buf, int(offset), ctypes.byref(peer_cfg), ctypes.byref(q)),
+               "pca_open_peer")
+        return q
+
+    def pca_attach_peers(self, up: pca_peer | None, down: pca_peer | None):
+        """Device-initiated halo exchange with the ranks above (up) / below (down) this strip."""
+        _check(lib().pca_attach_peers(self.handle, ctypes.byref(up) if up is not None else None,
+                                      ctypes.byref(down) if down is not None else None), "pca_attach_peers")
 
     def pca_attach_nccl(self, uid: bytes, nranks: int, rank: int):
         buf = ctypes.create_string_buffer(uid, 128)

@@ -65,6 +65,14 @@ struct SweepCommon {
     uint32_t chain0;       // chain id of batch entry 0
     int count_enable;      // accumulate MPM counts this sweep
     int rlo, rhi;          // local rows [rlo, rhi) updated by this launch
+    // device-initiated halo exchange (row strips with peers attached, pca_attach_peers): the
+    // new row 0 is also stored into peer_up (the up-peer's output-buffer row below its
+    // strip, padded row base of chain 0) and the new row rows-1 into peer_dn (the
+    // down-peer's row above its strip), over NVLink peer memory, by the CTAs that compute
+    // them; nullptr = no such peer.  *_chain: the peers' chain strides in bytes.
+    uint8_t* peer_up;
+    uint8_t* peer_dn;
+    long long peer_up_chain, peer_dn_chain;
 };
 
 // levels == 2 fast path: thr[((np*9 + n1)*2 + g)*2 + x] = ceil(p0 * 2^32) - 1, the

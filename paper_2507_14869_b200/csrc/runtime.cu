@@ -6,6 +6,7 @@
 // communicator for row-strip sharding (halo exchange of one padded row per neighbour
 // per sweep).  NCCL is loaded with dlopen on first use, so the library
 // has no link-time dependency beyond libc/libdl (cudart is linked statically).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -272,6 +273,12 @@ struct pca_ctx {
     int truth_staged = 0;
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_truth_ready = nullptr, ev_truth_free = nullptr;
+    // device-initiated halo exchange (pca_attach_peers)
+    int p2p = 0;
+    int has_up = 0, has_dn = 0;
+    pca_peer up{}, dn{};
+    uint32_t* pflags = nullptr;  // [0]: phase completed by the up peer, [1]: by the down peer
+    uint32_t phase = 0;          // phases (state loads, sweeps) this context has completed
 };
 
 namespace {
@@ -595,6 +602,95 @@ void fill_common(pca_ctx* ctx, SweepCommon& sc, int64_t t, int count) {
     sc.t = (uint32_t)t;
     sc.chain0 = (uint32_t)ctx->cfg.chain0;
     sc.count_enable = count;
+    sc.peer_up = sc.peer_dn = nullptr;
+    sc.peer_up_chain = sc.peer_dn_chain = 0;
+}
+
+// ---- device-initiated halo exchange (pca_attach_peers) ----
+// Phase protocol, per context: every state load and every sweep is one phase k = ++phase.
+// Before a phase touches peer memory or reads its own halo rows it waits (on the stream, no
+// spinning kernel) until both peers have completed phase k-1: their pushes into our halo
+// rows are then complete, and they no longer read the halo rows of the buffer we are about
+// to write into (the double buffer alternates, so that is the buffer they read in phase
+// k-1).  After the phase's work, a stream write (with a system-wide fence before it) tells
+// each peer that we completed phase k.
+struct StreamMemOps {
+    using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    WaitFn wait = nullptr;
+    WriteFn write = nullptr;
+    std::string why;
+};
+StreamMemOps& memops() {
+    static StreamMemOps m = [] {
+        StreamMemOps o;
+        cudaDriverEntryPointQueryResult q1, q2;
+        void* w = nullptr;
+        void* x = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+            q1 != cudaDriverEntryPointSuccess ||
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", &x, cudaEnableDefault, &q2) != cudaSuccess ||
+            q2 != cudaDriverEntryPointSuccess) {
+            o.why = "cuStreamWaitValue32 / cuStreamWriteValue32 unavailable";
+            return o;
+        }
+        o.wait = (StreamMemOps::WaitFn)w;
+        o.write = (StreamMemOps::WriteFn)x;
+        return o;
+    }();
+    return m;
+}
+
+pca_status p2p_begin(pca_ctx* ctx, uint32_t k) {
+    StreamMemOps& M = memops();
+    for (int i = 0; i < 2; ++i) {
+        if (!(i == 0 ? ctx->has_up : ctx->has_dn)) continue;
+        const CUresult r = M.wait((CUstream)ctx->stream, (CUdeviceptr)(ctx->pflags + i), k - 1,
+                                  CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) {
+            ctx->poisoned = 1;
+            return fail(PCA_ECUDA, "cuStreamWaitValue32 (peer phase): CUresult %d", (int)r);
+        }
+    }
+    return PCA_OK;
+}
+
+pca_status p2p_end(pca_ctx* ctx, uint32_t k) {
+    StreamMemOps& M = memops();
+    // we are the up peer's down peer (its slot 1) and the down peer's up peer (its slot 0)
+    if (ctx->has_up) {
+        const CUresult r = M.write((CUstream)ctx->stream, (CUdeviceptr)(ctx->up.flags + 1), k, 0);
+        if (r != CUDA_SUCCESS) return fail(PCA_ECUDA, "cuStreamWriteValue32 (up peer): CUresult %d", (int)r);
+    }
+    if (ctx->has_dn) {
+        const CUresult r = M.write((CUstream)ctx->stream, (CUdeviceptr)(ctx->dn.flags + 0), k, 0);
+        if (r != CUDA_SUCCESS) return fail(PCA_ECUDA, "cuStreamWriteValue32 (down peer): CUresult %d", (int)r);
+    }
+    ctx->phase = k;
+    return PCA_OK;
+}
+
+// A phase that rewrote buffer `b` outside a sweep kernel (a state load): copy its first /
+// last HALO owned rows into the peers' halo rows of their buffer b, with the protocol.
+pca_status p2p_push(pca_ctx* ctx, int b) {
+    const uint32_t k = ctx->phase + 1;
+    pca_status st = p2p_begin(ctx, k);
+    if (st != PCA_OK) return st;
+    const size_t pitch = (size_t)ctx->lay.xpitch, R = (size_t)ctx->lay.rows;
+    const size_t rb = HALO * pitch;
+    uint8_t* mine = ctx->x[b];
+    for (int c = 0; c < ctx->cfg.batch; ++c) {
+        uint8_t* base = mine + (size_t)c * ctx->geo.xchain;
+        if (ctx->has_up) {  // our rows 0..HALO-1 -> the up peer's rows below its strip
+            uint8_t* dst = ctx->up.x[b] + (size_t)c * ctx->up.chain_stride + (HALO + (size_t)ctx->up.rows) * pitch;
+            CK(ctx, cudaMemcpyAsync(dst, base + HALO * pitch, rb, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        if (ctx->has_dn) {  // our last HALO rows -> the down peer's rows above its strip
+            uint8_t* dst = ctx->dn.x[b] + (size_t)c * ctx->dn.chain_stride;
+            CK(ctx, cudaMemcpyAsync(dst, base + R * pitch, rb, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+    }
+    return p2p_end(ctx, k);
 }
 
 // Halo exchange of buffer `buf` with the neighbouring ranks (row strips): send the first
@@ -647,6 +743,7 @@ pca_status load_state(pca_ctx* ctx, const uint8_t* src, int pitch, long long cha
                                   ctx->cfg.batch, ctx->flag, ctx->stream));
     pca_status st = check_flag(ctx, what);
     if (st != PCA_OK) return st;
+    if (ctx->p2p) return p2p_push(ctx, ctx->cur);
     return exchange(ctx, ctx->x[ctx->cur]);
 }
 
@@ -734,6 +831,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->sums = (unsigned long long*)(ctx->ws + L.off_sums);
     ctx->sums_max = (unsigned long long*)(ctx->ws + L.off_sums_max);
     ctx->flag = (int*)(ctx->ws + L.off_flag);
+    ctx->pflags = (uint32_t*)(ctx->ws + L.off_flag + 64);
     ctx->stage = ctx->ws + L.off_stage;
     ctx->truth = ctx->ws + L.off_truth;
     ctx->io_in = ctx->ws + L.off_io;
@@ -795,6 +893,8 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
                                     ctx->dtab_host.size() * sizeof(double), cudaMemcpyHostToDevice,
                                     ctx->stream);
     if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "upload dtab"));
+    e = cudaMemsetAsync(ctx->pflags, 0, 2 * sizeof(uint32_t), ctx->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "clear peer flags"));
     st = do_reset(ctx, g, x0);
     if (st != PCA_OK) return bail(st);
     *out = ctx;
@@ -812,9 +912,9 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
     const bool strip = ctx->lay.rows < ctx->cfg.height;
-    if (strip && !ctx->comm && n > 1)
+    if (strip && !ctx->comm && !ctx->p2p && n > 1)
         return fail(PCA_EINVAL,
-                    "a strip context without NCCL sweeps one step at a time (caller exchanges halos)");
+                    "a strip context without NCCL or peers sweeps one step at a time (caller exchanges halos)");
     // two sweeps per HBM pass (sweep_binary2.cu, opt-in): levels == 2, whole lattice,
     // W % 16 == 0.  Measured slower than one sweep per pass on B200.
     const bool pairs = ctx->kernel == PCA_KERNEL_BINARY && !strip && (ctx->cfg.width % 16) == 0 &&
@@ -903,7 +1003,26 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
         };
         const int R = ctx->lay.rows;
         int e = 0;
-        if (strip && R >= 3) {
+        if (strip && ctx->p2p) {
+            // device-initiated halo exchange: ONE launch over all rows whose edge-row CTAs also
+            // store the new rows into the peers' halo rows (their output buffer); stream waits
+            // and writes of the phase words order it against the peers (p2p_begin / p2p_end)
+            const uint32_t k = ctx->phase + 1;
+            st = p2p_begin(ctx, k);
+            if (st != PCA_OK) return st;
+            const int nb = ctx->cur ^ 1;
+            const size_t pitch = (size_t)ctx->lay.xpitch;
+            for (SweepCommon* sc : {&ctx->bin.c, &ctx->gen.c}) {
+                sc->peer_up = ctx->has_up ? ctx->up.x[nb] + (HALO + (size_t)ctx->up.rows) * pitch : nullptr;
+                sc->peer_dn = ctx->has_dn ? ctx->dn.x[nb] + (HALO - 1) * pitch : nullptr;
+                sc->peer_up_chain = ctx->up.chain_stride;
+                sc->peer_dn_chain = ctx->dn.chain_stride;
+            }
+            e = launch_rows(0, R, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (peer halos)");
+            st = p2p_end(ctx, k);
+            if (st != PCA_OK) return st;
+        } else if (strip && R >= 3) {
             // row strip: the two edge rows first, then their halo exchange on the main stream
             // overlapping the interior rows on the side stream; the next sweep starts after
             // both (the interior never reads the halo rows).
@@ -945,6 +1064,8 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
     if (c.periodic && ((c.height & 1) || (c.width & 1)))
         return fail(PCA_EUNSUPPORTED, "the Gibbs colouring needs even height and width on a torus");
     const bool strip = ctx->lay.rows < c.height;
+    if (strip && ctx->p2p)
+        return fail(PCA_EUNSUPPORTED, "row-strip Gibbs sweeps exchange halos over NCCL, not over attached peers");
     if (strip && !(ctx->comm && ctx->nranks > 1))
         return fail(PCA_EINVAL, "a row-strip Gibbs sweep exchanges halos between colours: attach NCCL");
     // Moore-8: the two colours of a row parity in one launch (2 launches per sweep) when the
@@ -1414,6 +1535,109 @@ pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out) {
     out->row_bytes = HALO * pitch;
     out->chain_stride = (size_t)ctx->geo.xchain;
     return PCA_OK;
+}
+
+pca_status pca_peer_info(pca_ctx* ctx, pca_peer* out) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!out) return fail(PCA_EINVAL, "out is NULL");
+    memset(out, 0, sizeof(*out));
+    out->x[0] = ctx->x[0];
+    out->x[1] = ctx->x[1];
+    out->flags = ctx->pflags;
+    out->rows = ctx->lay.rows;
+    out->batch = ctx->cfg.batch;
+    out->chain_stride = ctx->geo.xchain;
+    return PCA_OK;
+}
+
+pca_status pca_ipc_handle(pca_ctx* ctx, void* handle64, uint64_t* offset) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!handle64 || !offset) return fail(PCA_EINVAL, "handle / offset is NULL");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t must be 64 bytes");
+    cudaSetDevice(ctx->device);
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return fail(PCA_ECUDA, "cuMemGetAddressRange unavailable");
+    const CUresult r = ((RangeFn)fn)(&base, &size, (CUdeviceptr)ctx->ws);
+    if (r != CUDA_SUCCESS) return fail(PCA_ECUDA, "cuMemGetAddressRange: CUresult %d", (int)r);
+    cudaIpcMemHandle_t h;
+    CK(ctx, cudaIpcGetMemHandle(&h, (void*)base));
+    memcpy(handle64, &h, 64);
+    *offset = (uint64_t)((CUdeviceptr)ctx->ws - base);
+    return PCA_OK;
+}
+
+pca_status pca_open_peer(pca_ctx* ctx, const void* handle64, uint64_t offset,
+                         const pca_config* peer_cfg, pca_peer* out) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!handle64 || !peer_cfg || !out) return fail(PCA_EINVAL, "handle / config / out is NULL");
+    st = validate(peer_cfg);
+    if (st != PCA_OK) return st;
+    if (peer_cfg->width != ctx->cfg.width || peer_cfg->height != ctx->cfg.height ||
+        peer_cfg->batch != ctx->cfg.batch)
+        return fail(PCA_EINVAL, "the peer's lattice (height, width, batch) differs from this context's");
+    cudaSetDevice(ctx->device);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    void* base = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+        return fail(PCA_ECUDA, "cudaIpcOpenMemHandle: CUDA error %d (%s)", (int)e, cudaGetErrorString(e));
+    const Layout L = make_layout(peer_cfg);
+    uint8_t* ws = (uint8_t*)base + offset;
+    memset(out, 0, sizeof(*out));
+    out->x[0] = ws + L.off_x0;
+    out->x[1] = ws + L.off_x1;
+    out->flags = (uint32_t*)(ws + L.off_flag + 64);
+    out->ipc_base = base;
+    out->rows = L.rows;
+    out->batch = peer_cfg->batch;
+    out->chain_stride = (int64_t)(L.rows + 2 * HALO) * L.xpitch;
+    return PCA_OK;
+}
+
+pca_status pca_close_peer(pca_peer* peer) {
+    if (!peer || !peer->ipc_base) return PCA_OK;
+    const cudaError_t e = cudaIpcCloseMemHandle(peer->ipc_base);
+    peer->ipc_base = nullptr;
+    if (e != cudaSuccess)
+        return fail(PCA_ECUDA, "cudaIpcCloseMemHandle: CUDA error %d (%s)", (int)e, cudaGetErrorString(e));
+    return PCA_OK;
+}
+
+pca_status pca_attach_peers(pca_ctx* ctx, const pca_peer* up, const pca_peer* down) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (ctx->lay.rows == ctx->cfg.height) return fail(PCA_EINVAL, "peers need a row-strip context");
+    if (ctx->p2p) return fail(PCA_EINVAL, "peers already attached");
+    if (!up && !down) return fail(PCA_EINVAL, "no peer given");
+    if (ctx->cfg.periodic && (!up || !down)) return fail(PCA_EINVAL, "a torus strip has two peers");
+    const size_t pitch = (size_t)ctx->lay.xpitch;
+    for (const pca_peer* q : {up, down}) {
+        if (!q) continue;
+        if (!q->x[0] || !q->x[1] || !q->flags || q->rows < HALO || q->batch != ctx->cfg.batch ||
+            q->chain_stride != (int64_t)((q->rows + 2 * HALO) * pitch))
+            return fail(PCA_EINVAL, "peer layout does not match this context's lattice");
+    }
+    StreamMemOps& M = memops();
+    if (!M.wait || !M.write) return fail(PCA_EUNSUPPORTED, "%s", M.why.c_str());
+    ctx->has_up = up != nullptr;
+    ctx->has_dn = down != nullptr;
+    if (up) ctx->up = *up;
+    if (down) ctx->dn = *down;
+    ctx->p2p = 1;
+    // phase 1: the current state's edge rows into the peers' halo rows
+    st = p2p_push(ctx, ctx->cur);
+    if (st != PCA_OK) return st;
+    return sync(ctx);
 }
 
 pca_status pca_nccl_unique_id(void* id128) {

@@ -197,6 +197,17 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
         }
     };
 
+    // device-initiated halo exchange: the edge rows also go straight into the neighbouring
+    // ranks' halo rows (peer memory over NVLink), written by the lanes that computed them
+    auto store_peer_rows = [&](int r, const uint32_t (&O)[4]) {
+        if (p.c.peer_up != nullptr && r == 0)
+            store_row_chunk<HALO, XOFF>(p.c.peer_up + chain * p.c.peer_up_chain, O, ccol, G.W - ccol, k, r,
+                                        G.W, G.nchunks, G.rows, G.xpitch, PER, false);
+        if (p.c.peer_dn != nullptr && r == G.rows - 1)
+            store_row_chunk<HALO, XOFF>(p.c.peer_dn + chain * p.c.peer_dn_chain, O, ccol, G.W - ccol, k, r,
+                                        G.W, G.nchunks, G.rows, G.xpitch, PER, false);
+    };
+
     // update local row r from the window (U = row r-1, M = row r, D = row r+1); its g row
     // and counts row are slot q of stage st
     auto update = [&](int r, const uint8_t* st, int q, const XRow& U, const XRow& M, const XRow& D) {
@@ -272,9 +283,10 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
             cp[0] = c0;
             cp[1] = c1;
         }
-        // ---- store x_{t+1} (+ torus halos) ----
+        // ---- store x_{t+1} (+ torus halos, + the peers' halo rows) ----
         store_row_chunk<HALO, XOFF>(xo + (long long)(r - rbeg) * G.xpitch, O, ccol, G.W - ccol, k, r,
                                     G.W, G.nchunks, G.rows, G.xpitch, PER, G.self_halo_rows);
+        store_peer_rows(r, O);
     };
 
     // Torus: update local rows r0 and (when nrow == 2) r0+1 together from the window rows
@@ -406,9 +418,10 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
                 cp[0] = c0;
                 cp[1] = c1;
             }
-            // ---- store x_{t+1} (+ torus halos) ----
+            // ---- store x_{t+1} (+ torus halos, + the peers' halo rows) ----
             store_row_chunk<HALO, XOFF>(xo + (long long)(r - rbeg) * G.xpitch, O[q], ccol, G.W - ccol, k,
                                         r, G.W, G.nchunks, G.rows, G.xpitch, PER, G.self_halo_rows);
+            store_peer_rows(r, O[q]);
         }
     };
 

@@ -406,6 +406,10 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 if (r < HALO) store(op + (long long)G.rows * G.xpitch);
                 if (r >= G.rows - HALO) store(op - (long long)G.rows * G.xpitch);
             }
+            // device-initiated halo exchange: the edge rows straight into the peers' halo rows
+            if (p.c.peer_up != nullptr && r == 0) store(p.c.peer_up + chain * p.c.peer_up_chain + XOFF + c0);
+            if (p.c.peer_dn != nullptr && r == G.rows - 1)
+                store(p.c.peer_dn + chain * p.c.peer_dn_chain + XOFF + c0);
             if (count_enable) {
                 if (nvalid == 4) {
                     // the quad's 4 counters of a plane form one 8-byte word; each distinct label

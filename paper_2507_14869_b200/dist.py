@@ -5,6 +5,9 @@
 * ``broadcast_unique_id``: rank 0 creates the NCCL unique id through the C ABI
   (pca_nccl_unique_id) and torch.distributed broadcasts its 128 bytes.
 * ``strip_context``: a PcaContext for this rank's strip with NCCL attached.
+* ``attach_peers_ipc``: the device-initiated halo exchange instead of NCCL sends/receives:
+  every rank publishes its workspace's CUDA IPC handle, maps its up / down neighbours' and
+  attaches them (pca_attach_peers).
 * ``chain_range``: the batch-mode partition of independent chains (replicas only).
 * ``batch_context``: a PcaContext for this rank's chain range (chain0 = its first global
   chain, so every chain draws the same Philox words whatever the world size).
@@ -49,6 +52,30 @@ def broadcast_unique_id(group=None) -> bytes:
     dist.broadcast_object_list(obj, src=0, group=group)
     assert isinstance(obj[0], bytes) and len(obj[0]) == 128
     return obj[0]
+
+
+def attach_peers_ipc(ctx, cfg_kwargs: dict, H: int, W: int, levels: int, group=None):
+    """Map the up / down ranks' workspaces (CUDA IPC, exchanged with torch.distributed) and
+    attach them to this rank's strip context: from then on every PCA sweep stores its edge rows
+    straight into the neighbours' halo rows.  Returns the mapped peers (pca_close_peer them
+    after the context is destroyed)."""
+    import torch.distributed as dist
+
+    from . import make_config
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    handle, off = ctx.pca_ipc_handle()
+    table = [None] * world
+    dist.all_gather_object(table, (handle, off), group=group)
+    up, down = ring_peers(rank, world, bool(cfg_kwargs.get("periodic", False)))
+    peers = {}
+    for q in {up, down} - {-1}:
+        row0, rows = strip_rows(H, world, q)
+        cfg = make_config(H, W, levels, row0=row0, rows=rows, **cfg_kwargs)
+        peers[q] = ctx.pca_open_peer(table[q][0], table[q][1], cfg)
+    dist.barrier(group=group)  # every rank has mapped its neighbours before anyone pushes
+    ctx.pca_attach_peers(peers.get(up), peers.get(down))
+    return list(peers.values())
 
 
 def strip_context(cfg_kwargs: dict, H: int, W: int, levels: int, g_strip, *, stream=None,

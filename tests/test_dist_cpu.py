@@ -193,3 +193,55 @@ def test_batch_mode_gathers_chain_metrics_in_global_order(world, n_chains):
     for p in procs:
         p.join(timeout=60)
     assert all(res)
+
+
+class _FakeStripCtx:
+    """Stands in for a PcaContext in the host logic of dist.attach_peers_ipc."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = []
+        self.attached = None
+
+    def pca_ipc_handle(self):
+        return bytes([self.rank]) * 64, 1000 + self.rank
+
+    def pca_open_peer(self, handle, off, cfg):
+        self.opened.append((handle[0], off, cfg.row0, cfg.rows, cfg.height))
+        return ("peer", handle[0])
+
+    def pca_attach_peers(self, up, down):
+        self.attached = (up, down)
+
+
+def _peers_worker(rank, world, port, H, periodic, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = _FakeStripCtx(rank)
+        pdist.attach_peers_ipc(ctx, dict(periodic=periodic, sigma=0.5), H, 64, 2)
+        up, dn = pdist.ring_peers(rank, world, periodic)
+        ok = ctx.attached == (("peer", up) if up >= 0 else None, ("peer", dn) if dn >= 0 else None)
+        for h, off, row0, rows, height in ctx.opened:  # each neighbour's own strip and handle
+            ok &= (row0, rows) == pdist.strip_rows(H, world, h) and off == 1000 + h and height == H
+        ok &= sorted(h for h, *_ in ctx.opened) == sorted({up, dn} - {-1})
+        out_q.put(bool(ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,periodic", [(2, True), (3, True), (3, False)])
+def test_attach_peers_ipc_maps_the_neighbour_strips(world, periodic):
+    """dist.attach_peers_ipc: every rank publishes its workspace handle, maps exactly its up /
+    down neighbours with THEIR strip configs, and attaches them in (up, down) order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peers_worker, args=(r, world, port, 50, periodic, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res)
