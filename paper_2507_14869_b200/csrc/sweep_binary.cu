@@ -102,7 +102,7 @@ struct XRow {
 // One warp per CTA: every per-warp quantity (segment, row range, stage addresses) derives
 // from blockIdx and kernel parameters only, so the compiler keeps it in uniform registers and
 // the bulk-copy issue needs no per-lane address handling.
-template <int NB, bool PER>
+template <int NB, bool PER, bool PEERS>  // PEERS: edge rows also stored into the peers' halos
 __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     sweep_binary_kernel(const __grid_constant__ BinarySweepParams p, int R) {
     using C = RingCfg<PER>;
@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     // device-initiated halo exchange: the edge rows also go straight into the neighbouring
     // ranks' halo rows (peer memory over NVLink), written by the lanes that computed them
     auto store_peer_rows = [&](int r, const uint32_t (&O)[4]) {
+        if (!PEERS) return;  // compiled out: the checks alone cost 3.5 us per 8192^2 sweep
         if (p.c.peer_up != nullptr && r == 0)
             store_row_chunk<HALO, XOFF>(p.c.peer_up + chain * p.c.peer_up_chain, O, ccol, G.W - ccol, k, r,
                                         G.W, G.nchunks, G.rows, G.xpitch, PER, false);
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     }
 }
 
-template <int NB, bool PER>
+template <int NB, bool PER, bool PEERS>
 int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     const Geometry& G = p.c.geo;
     static LaunchInfo info[MAX_DEVICES];
@@ -470,13 +471,13 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     if (!li.ok.load(std::memory_order_acquire)) {
         std::lock_guard<std::mutex> lock(launch_info_mutex());
         if (!li.ok.load(std::memory_order_relaxed)) {
-            cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER>,
+            cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER, PEERS>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, RingCfg<PER>::SMEM);
             if (e != cudaSuccess) return (int)e;
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_binary_kernel<NB, PER>, 32,
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_binary_kernel<NB, PER, PEERS>, 32,
                                                           RingCfg<PER>::SMEM);
             if (li.occ < 1) li.occ = 1;
             li.ok.store(true, std::memory_order_release);
@@ -496,7 +497,7 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     if (nrb <= 0) return 0;
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS, nrb, batch);
-    sweep_binary_kernel<NB, PER><<<grid, 32, RingCfg<PER>::SMEM, s>>>(p, R);
+    sweep_binary_kernel<NB, PER, PEERS><<<grid, 32, RingCfg<PER>::SMEM, s>>>(p, R);
     return (int)cudaGetLastError();
 }
 
@@ -505,9 +506,12 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
 int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int R = rows_per_thread;  // 0 = auto (one wave)
+    const bool peers = p.c.peer_up != nullptr || p.c.peer_dn != nullptr;
     if (p.c.geo.nbhd == 8)
-        return p.c.geo.periodic ? launch_t<8, true>(p, batch, R, s) : launch_t<8, false>(p, batch, R, s);
-    return p.c.geo.periodic ? launch_t<4, true>(p, batch, R, s) : launch_t<4, false>(p, batch, R, s);
+        return peers ? (p.c.geo.periodic ? launch_t<8, true, true>(p, batch, R, s) : launch_t<8, false, true>(p, batch, R, s))
+                     : (p.c.geo.periodic ? launch_t<8, true, false>(p, batch, R, s) : launch_t<8, false, false>(p, batch, R, s));
+    return peers ? (p.c.geo.periodic ? launch_t<4, true, true>(p, batch, R, s) : launch_t<4, false, true>(p, batch, R, s))
+                 : (p.c.geo.periodic ? launch_t<4, true, false>(p, batch, R, s) : launch_t<4, false, false>(p, batch, R, s));
 }
 
 }  // namespace pcab200
