@@ -179,7 +179,7 @@ __host__ __device__ inline Decomp make_decomp(int nquads, int nrows, int R) {
 // queue needs uniform trip counts); lanes past their rows idle.  COH: x is read through L2
 // (ld.global.cg) because an earlier sweep of the same launch wrote it; otherwise through the
 // read-only path.
-template <int NB, int LT, bool COH>
+template <int NB, int LT, bool COH, bool PEERS = false>  // PEERS: edge rows also to the peers' halos
 __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT>& sm,
                                          const uint8_t* __restrict__ x_in, uint8_t* __restrict__ x_out,
                                          uint32_t t, int count_enable, int qd, int chain, int rbeg,
@@ -407,9 +407,12 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                 if (r >= G.rows - HALO) store(op - (long long)G.rows * G.xpitch);
             }
             // device-initiated halo exchange: the edge rows straight into the peers' halo rows
-            if (p.c.peer_up != nullptr && r == 0) store(p.c.peer_up + chain * p.c.peer_up_chain + XOFF + c0);
-            if (p.c.peer_dn != nullptr && r == G.rows - 1)
-                store(p.c.peer_dn + chain * p.c.peer_dn_chain + XOFF + c0);
+            // (compiled out otherwise: even never-taken checks cost ~5% of a C5 sweep)
+            if (PEERS) {
+                if (p.c.peer_up != nullptr && r == 0) store(p.c.peer_up + chain * p.c.peer_up_chain + XOFF + c0);
+                if (p.c.peer_dn != nullptr && r == G.rows - 1)
+                    store(p.c.peer_dn + chain * p.c.peer_dn_chain + XOFF + c0);
+            }
             if (count_enable) {
                 if (nvalid == 4) {
                     // the quad's 4 counters of a plane form one 8-byte word; each distinct label
@@ -455,7 +458,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
     }
 }
 
-template <int NB, int LT>  // LT: levels known at compile time, 0 = any
+template <int NB, int LT, bool PEERS>  // LT: levels known at compile time, 0 = any
 __global__ void __launch_bounds__(GEN_THREADS, PCA_GEN_MINB)
     sweep_general_kernel(const __grid_constant__ GeneralSweepParams p, int R) {
     __shared__ GenSmem<LT> sm;
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(GEN_THREADS, PCA_GEN_MINB)
     const int qd = blockIdx.x * d.QW + (threadIdx.x & (d.QW - 1));
     const int rbeg = p.c.rlo + (blockIdx.y * d.RS + threadIdx.x / d.QW) * d.R;
     const int rend = min(rbeg + d.R, p.c.rhi);
-    gen_rows<NB, LT, false>(p, sm, p.c.x_in, p.c.x_out, p.c.t, p.c.count_enable, qd, blockIdx.z,
+    gen_rows<NB, LT, false, PEERS>(p, sm, p.c.x_in, p.c.x_out, p.c.t, p.c.count_enable, qd, blockIdx.z,
                             rbeg, rend, d.R);
 }
 
@@ -519,9 +522,10 @@ struct GenLaunch {
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
                 const int smem = (int)sizeof(GenSmem<LT>);
-                cudaFuncSetAttribute(sweep_general_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                cudaFuncSetAttribute(sweep_general_kernel<NB, LT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                cudaFuncSetAttribute(sweep_general_kernel<NB, LT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
                 cudaFuncSetAttribute(sweep_multi_kernel<NB, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_general_kernel<NB, LT>, GEN_THREADS, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_general_kernel<NB, LT, false>, GEN_THREADS, smem);
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, sweep_multi_kernel<NB, LT>, GEN_THREADS, smem);
                 if (li.occ < 1) li.occ = 1;
                 if (li.mocc < 1) li.mocc = 1;
@@ -563,7 +567,10 @@ int launch_g(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t s
     Decomp d = make_decomp(nquads, nr, (int)R);
     while (d.nrb > 65535) d = make_decomp(nquads, nr, d.R * 2);
     dim3 grid((unsigned)d.nxb, (unsigned)d.nrb, batch);
-    sweep_general_kernel<NB, LT><<<grid, GEN_THREADS, 0, s>>>(p, d.R);
+    if (p.c.peer_up != nullptr || p.c.peer_dn != nullptr)
+        sweep_general_kernel<NB, LT, true><<<grid, GEN_THREADS, 0, s>>>(p, d.R);
+    else
+        sweep_general_kernel<NB, LT, false><<<grid, GEN_THREADS, 0, s>>>(p, d.R);
     return (int)cudaGetLastError();
 }
 
