@@ -186,7 +186,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                                          int rend, int iters) {
     constexpr bool SMEM_U = LT > 0 && LT <= 9;
     const Geometry& G = p.c.geo;
-    const int L = G.levels;
+    const int L = LT > 0 ? LT : G.levels;  // a compile-time constant when LT fixes it
     const int nquads = (G.W + 3) >> 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool active = qd < nquads && rbeg < rend;
@@ -196,7 +196,8 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
     uint32_t* stage = sm.stage[warp];
     uint8_t* queue = sm.queue[warp];
     uint8_t* res = sm.res[warp];
-    const bool use_u = LT == 2 || p.uthr != nullptr;
+    // the uniform table exists for every level count <= 16 (UTHR_MAX_LEVELS)
+    const bool use_u = (LT >= 2 && LT <= 16) || p.uthr != nullptr;
     const uint32_t* U = (SMEM_U || LT == 2) ? sm.U : p.uthr;
     const int c0 = 4 * qd;
     const int nvalid = active ? min(4, G.W - c0) : 0;
