@@ -102,9 +102,18 @@ struct XRow {
 // One warp per CTA: every per-warp quantity (segment, row range, stage addresses) derives
 // from blockIdx and kernel parameters only, so the compiler keeps it in uniform registers and
 // the bulk-copy issue needs no per-lane address handling.
-template <int NB, bool PER, bool PEERS>  // PEERS: edge rows also stored into the peers' halos
+// F: compile-time launch flags.  This kernel's schedule is sensitive to code it never runs:
+// two never-taken peer-pointer tests cost 3.5 us per 8192^2 sweep, and making the counting
+// or the torus self-halo compile-time in the counting variant cost 2 (torus) to 7.5 (free
+// boundary) us through a different register allocation, so only the peer stores and the
+// no-counting variant (76.1 -> 73.9 us) are separate instantiations.
+constexpr int BF_PEERS = 1;    // edge rows also stored into the peers' halo rows
+constexpr int BF_NOCOUNT = 2;  // no MPM counting in this sweep
+template <int NB, bool PER, int F>
 __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     sweep_binary_kernel(const __grid_constant__ BinarySweepParams p, int R) {
+    constexpr bool PEERS = (F & BF_PEERS) != 0;
+    constexpr bool NOCOUNT = (F & BF_NOCOUNT) != 0;
     using C = RingCfg<PER>;
     constexpr int KSTAGES = C::K;
     constexpr int STAGE_BYTES = C::STAGE;
@@ -135,7 +144,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     const bool active = lane < nch;
     const int ccol = col0 + 16 * lane;      // first column of the chunk
     const uint32_t xbytes = 16 * nch + 32, gbytes = 16 * nch;
-    const uint32_t cbytes = p.c.count_enable ? 32 * nch : 0;
+    const uint32_t cbytes = (!NOCOUNT && p.c.count_enable) ? 32 * nch : 0;
     // padded x row j starts at (j+HALO)*xpitch; byte col0 of it is column col0-16; xin points
     // at x row rbeg-1 (item 0)
     const uint8_t* xin = p.c.x_in + chain * G.xchain + col0 + (long long)(rbeg - 1 + HALO) * G.xpitch;
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     // device-initiated halo exchange: the edge rows also go straight into the neighbouring
     // ranks' halo rows (peer memory over NVLink), written by the lanes that computed them
     auto store_peer_rows = [&](int r, const uint32_t (&O)[4]) {
-        if (!PEERS) return;  // compiled out: the checks alone cost 3.5 us per 8192^2 sweep
+        if (!PEERS) return;
         if (p.c.peer_up != nullptr && r == 0)
             store_row_chunk<HALO, XOFF>(p.c.peer_up + chain * p.c.peer_up_chain, O, ccol, G.W - ccol, k, r,
                                         G.W, G.nchunks, G.rows, G.xpitch, PER, false);
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     }
 }
 
-template <int NB, bool PER, bool PEERS>
+template <int NB, bool PER, int F>
 int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     const Geometry& G = p.c.geo;
     static LaunchInfo info[MAX_DEVICES];
@@ -471,13 +480,13 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     if (!li.ok.load(std::memory_order_acquire)) {
         std::lock_guard<std::mutex> lock(launch_info_mutex());
         if (!li.ok.load(std::memory_order_relaxed)) {
-            cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER, PEERS>,
+            cudaError_t e = cudaFuncSetAttribute(sweep_binary_kernel<NB, PER, F>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, RingCfg<PER>::SMEM);
             if (e != cudaSuccess) return (int)e;
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_binary_kernel<NB, PER, PEERS>, 32,
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_binary_kernel<NB, PER, F>, 32,
                                                           RingCfg<PER>::SMEM);
             if (li.occ < 1) li.occ = 1;
             li.ok.store(true, std::memory_order_release);
@@ -497,8 +506,20 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     if (nrb <= 0) return 0;
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS, nrb, batch);
-    sweep_binary_kernel<NB, PER, PEERS><<<grid, 32, RingCfg<PER>::SMEM, s>>>(p, R);
+    sweep_binary_kernel<NB, PER, F><<<grid, 32, RingCfg<PER>::SMEM, s>>>(p, R);
     return (int)cudaGetLastError();
+}
+
+template <int NB, bool PER>
+int launch_f(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
+    const bool peers = p.c.peer_up != nullptr || p.c.peer_dn != nullptr;
+    const int f = (peers ? BF_PEERS : 0) | (p.c.count_enable ? 0 : BF_NOCOUNT);
+    switch (f) {
+        case 0: return launch_t<NB, PER, 0>(p, batch, R, s);
+        case 1: return launch_t<NB, PER, 1>(p, batch, R, s);
+        case 2: return launch_t<NB, PER, 2>(p, batch, R, s);
+        default: return launch_t<NB, PER, 3>(p, batch, R, s);
+    }
 }
 
 }  // namespace
@@ -506,12 +527,9 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
 int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int R = rows_per_thread;  // 0 = auto (one wave)
-    const bool peers = p.c.peer_up != nullptr || p.c.peer_dn != nullptr;
     if (p.c.geo.nbhd == 8)
-        return peers ? (p.c.geo.periodic ? launch_t<8, true, true>(p, batch, R, s) : launch_t<8, false, true>(p, batch, R, s))
-                     : (p.c.geo.periodic ? launch_t<8, true, false>(p, batch, R, s) : launch_t<8, false, false>(p, batch, R, s));
-    return peers ? (p.c.geo.periodic ? launch_t<4, true, true>(p, batch, R, s) : launch_t<4, false, true>(p, batch, R, s))
-                 : (p.c.geo.periodic ? launch_t<4, true, false>(p, batch, R, s) : launch_t<4, false, false>(p, batch, R, s));
+        return p.c.geo.periodic ? launch_f<8, true>(p, batch, R, s) : launch_f<8, false>(p, batch, R, s);
+    return p.c.geo.periodic ? launch_f<4, true>(p, batch, R, s) : launch_f<4, false>(p, batch, R, s);
 }
 
 }  // namespace pcab200
