@@ -288,8 +288,11 @@ pca_status pca_attach_nccl(pca_ctx* ctx, const void* id128, int32_t nranks, int3
  * a wait until both peers completed phase k-1 (cuStreamWaitValue32 on this context's phase
  * words; no kernel spins) and followed by a write of k into the peers' phase words
  * (cuStreamWriteValue32, fenced).  Every rank must issue the same sequence of sweeps and state
- * loads (SPMD).  Row-strip Gibbs sweeps need NCCL (PCA_EUNSUPPORTED with peers attached).  The
- * metric reductions still use NCCL when it is attached, else they cover this strip only.
+ * loads (SPMD), and the contexts must run on different streams (in practice different GPUs):
+ * a call with several phases (pca_sweep(n > 1), a Gibbs sweep) waits on the peers' later
+ * phases, which on a shared stream would be queued behind the wait.  Row-strip Gibbs sweeps
+ * use the peers too: each launch is a phase whose edge rows are copied to the peers after it.
+ * The metric reductions still use NCCL when it is attached, else they cover this strip only.
  * Errors: PCA_EINVAL (not a strip, already attached, layout mismatch), PCA_ECUDA (IPC or
  * stream memory operations unavailable / failed), PCA_EUNSUPPORTED (no stream memory ops). */
 pca_status pca_peer_info(pca_ctx* ctx, pca_peer* out);

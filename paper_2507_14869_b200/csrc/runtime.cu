@@ -670,26 +670,35 @@ pca_status p2p_end(pca_ctx* ctx, uint32_t k) {
     return PCA_OK;
 }
 
-// A phase that rewrote buffer `b` outside a sweep kernel (a state load): copy its first /
-// last HALO owned rows into the peers' halo rows of their buffer b, with the protocol.
+// Copy the first / last `depth` owned rows of buffer `b` into the peers' halo rows of their
+// buffer b (the copies of a phase whose kernel did not store them itself).
+pca_status p2p_copy_edges(pca_ctx* ctx, int b, int depth) {
+    const size_t pitch = (size_t)ctx->lay.xpitch, R = (size_t)ctx->lay.rows;
+    const size_t rb = (size_t)depth * pitch;
+    uint8_t* mine = ctx->x[b];
+    for (int c = 0; c < ctx->cfg.batch; ++c) {
+        uint8_t* base = mine + (size_t)c * ctx->geo.xchain;
+        if (ctx->has_up) {  // our rows 0..depth-1 -> the up peer's rows below its strip
+            uint8_t* dst = ctx->up.x[b] + (size_t)c * ctx->up.chain_stride + (HALO + (size_t)ctx->up.rows) * pitch;
+            CK(ctx, cudaMemcpyAsync(dst, base + HALO * pitch, rb, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        if (ctx->has_dn) {  // our last depth rows -> the down peer's rows above its strip
+            uint8_t* dst = ctx->dn.x[b] + (size_t)c * ctx->dn.chain_stride + (size_t)(HALO - depth) * pitch;
+            CK(ctx, cudaMemcpyAsync(dst, base + (HALO + R - depth) * pitch, rb, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+        }
+    }
+    return PCA_OK;
+}
+
+// A phase that rewrote buffer `b` outside a sweep kernel (a state load): its HALO edge rows
+// to the peers, with the protocol.
 pca_status p2p_push(pca_ctx* ctx, int b) {
     const uint32_t k = ctx->phase + 1;
     pca_status st = p2p_begin(ctx, k);
     if (st != PCA_OK) return st;
-    const size_t pitch = (size_t)ctx->lay.xpitch, R = (size_t)ctx->lay.rows;
-    const size_t rb = HALO * pitch;
-    uint8_t* mine = ctx->x[b];
-    for (int c = 0; c < ctx->cfg.batch; ++c) {
-        uint8_t* base = mine + (size_t)c * ctx->geo.xchain;
-        if (ctx->has_up) {  // our rows 0..HALO-1 -> the up peer's rows below its strip
-            uint8_t* dst = ctx->up.x[b] + (size_t)c * ctx->up.chain_stride + (HALO + (size_t)ctx->up.rows) * pitch;
-            CK(ctx, cudaMemcpyAsync(dst, base + HALO * pitch, rb, cudaMemcpyDeviceToDevice, ctx->stream));
-        }
-        if (ctx->has_dn) {  // our last HALO rows -> the down peer's rows above its strip
-            uint8_t* dst = ctx->dn.x[b] + (size_t)c * ctx->dn.chain_stride;
-            CK(ctx, cudaMemcpyAsync(dst, base + R * pitch, rb, cudaMemcpyDeviceToDevice, ctx->stream));
-        }
-    }
+    st = p2p_copy_edges(ctx, b, HALO);
+    if (st != PCA_OK) return st;
     return p2p_end(ctx, k);
 }
 
@@ -1064,10 +1073,24 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
     if (c.periodic && ((c.height & 1) || (c.width & 1)))
         return fail(PCA_EUNSUPPORTED, "the Gibbs colouring needs even height and width on a torus");
     const bool strip = ctx->lay.rows < c.height;
-    if (strip && ctx->p2p)
-        return fail(PCA_EUNSUPPORTED, "row-strip Gibbs sweeps exchange halos over NCCL, not over attached peers");
-    if (strip && !(ctx->comm && ctx->nranks > 1))
-        return fail(PCA_EINVAL, "a row-strip Gibbs sweep exchanges halos between colours: attach NCCL");
+    if (strip && !ctx->p2p && !(ctx->comm && ctx->nranks > 1))
+        return fail(PCA_EINVAL, "a row-strip Gibbs sweep exchanges halos between colours: attach NCCL or peers");
+    // strips: every Gibbs launch is one exchange phase.  With peers attached the launch is
+    // preceded by the phase wait and followed by copies of its buffer's edge rows into the
+    // peers' halo rows (in place or not, a launch never reads a byte that it or a peer's launch
+    // of the same phase changes, so rewriting unchanged halo bytes is safe), then the signal.
+    auto phase_begin = [&](uint32_t& k) -> pca_status {
+        if (!strip || !ctx->p2p) return PCA_OK;
+        k = ctx->phase + 1;
+        return p2p_begin(ctx, k);
+    };
+    auto phase_end = [&](uint32_t k, int b) -> pca_status {
+        if (!strip) return PCA_OK;
+        if (!ctx->p2p) return exchange(ctx, ctx->x[b], 1);
+        pca_status s2 = p2p_copy_edges(ctx, b, 1);
+        if (s2 != PCA_OK) return s2;
+        return p2p_end(ctx, k);
+    };
     // Moore-8: the two colours of a row parity in one launch (2 launches per sweep) when the
     // right-neighbour recomputation has its columns (free boundary, or 16-column torus pads);
     // with two levels on the binary PCA kernel's data path (sweep_gibbs_binary.cu), X -> Y
@@ -1116,14 +1139,15 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
             for (int par = 0; par < 2; ++par) {
                 ctx->gbin.parity = par;
                 ctx->gbin.x_nb = par == 0 ? ctx->x[ctx->cur] : ctx->x[ctx->cur ^ 1];
+                uint32_t k = 0;
+                st = phase_begin(k);
+                if (st != PCA_OK) return st;
                 ctx->launches++;
                 ctx->sweep_launches++;
                 const int e = launch_gibbs_binary(ctx->gbin, c.batch, ctx->stream);
                 if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep (binary)");
-                if (strip) {
-                    st = exchange(ctx, ctx->x[ctx->cur ^ 1], 1);
-                    if (st != PCA_OK) return st;
-                }
+                st = phase_end(k, ctx->cur ^ 1);
+                if (st != PCA_OK) return st;
             }
             ctx->cur ^= 1;
             ctx->prev_valid = 1;
@@ -1140,15 +1164,16 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
             ctx->gib.colour = k;
             // rows are final after colour 1 / 3, or after their fused launch
             ctx->gib.c.count_enable = count && (fused || (k & 1));
+            uint32_t ph = 0;
+            st = phase_begin(ph);
+            if (st != PCA_OK) return st;
             ctx->launches++;
             ctx->sweep_launches++;
             const int e = launch_sweep_gibbs(ctx->gib, c.batch, 1, ctx->stream);
             if (e) return cuda_fail(ctx, (cudaError_t)e, "gibbs sweep");
             ctx->prev_valid = 0;  // in place
-            if (strip) {
-                st = exchange(ctx, ctx->x[ctx->cur], 1);
-                if (st != PCA_OK) return st;
-            }
+            st = phase_end(ph, ctx->cur);
+            if (st != PCA_OK) return st;
         }
         ctx->t = t + 1;
         ctx->counted += count;
