@@ -313,10 +313,13 @@ def run_ours(args):
             ectx = P.PcaContext(P.make_config(wl["H"], W, wl["levels"], **kw_e), g_h, stream=stream)
 
         def step_e2e():
-            ectx.pca_reset(g_h, None)            # H2D of g inside the step
+            ectx.pca_reset_staged()              # this step's g (its H2D ran during the last step)
+            ectx.pca_stage_input(g_h)            # H2D of the next step's g, overlapping the sweeps
             ectx.pca_stage_truth(t_h)            # H2D of the truth, overlapping the sweeps
             ectx.pca_sweep(S)
             return ectx.pca_finalize(None, mpm_h)  # D2H of the MPM image
+
+        ectx.pca_stage_input(g_h)                # the first step's input
 
         for _ in range(max(1, args.warmup)):
             step_e2e()
@@ -334,7 +337,9 @@ def run_ours(args):
                "d2h_bytes_per_step": int(mpm_h.numel() + 4 * 8),
                "ms_per_step": ems / args.steps,
                "io": ("bit-packed images (packed_io): g and truth in, MPM image out, 1 bit per site"
-                      if packed else "dense uint8 images")}
+                      if packed else "dense uint8 images") +
+                     "; each step copies the next step's g and its own truth on a copy stream "
+                     "overlapping its sweeps (pca_stage_input / pca_stage_truth)"}
         ectx.pca_destroy()
 
     clk = clocks.stop()

@@ -212,6 +212,18 @@ pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, doubl
  * asynchronous).  Asynchronous. */
 pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth);
 
+/* Stage the NEXT reset's observed image g (host or device, the layout of pca_init's g; bit-
+ * packed with packed_io) into the context on the internal copy stream, so the transfer overlaps
+ * the work enqueued after it; pca_reset_staged then resets from it (x0 = g), waiting for the
+ * copy on the device, not the host.  Host memory must stay valid until that reset returns
+ * (pinned memory makes the copy truly asynchronous).  A second pca_stage_input waits for the
+ * first to be consumed.  Asynchronous. */
+pca_status pca_stage_input(pca_ctx* ctx, const uint8_t* g);
+
+/* pca_reset(ctx, g_staged, NULL) with the image of the last pca_stage_input; PCA_EINVAL when
+ * nothing is staged.  Synchronises like pca_reset. */
+pca_status pca_reset_staged(pca_ctx* ctx);
+
 /* The end of a run in ONE fused pass over truth, the current state and the counts
  * (SURVEY 8(a) a8 + a9): the MPM image (written to mpm_out, host or device
  * [batch][rows][width], when non-NULL) and PSNR / global SSIM of both the last sample and

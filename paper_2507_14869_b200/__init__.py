@@ -35,7 +35,7 @@ EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "p
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
            "pca_destroy", "pca_last_error", "pca_peer_info", "pca_ipc_handle", "pca_open_peer",
-           "pca_close_peer", "pca_attach_peers"]
+           "pca_close_peer", "pca_attach_peers", "pca_stage_input", "pca_reset_staged"]
 
 
 class PcaError(RuntimeError):
@@ -114,6 +114,8 @@ def lib():
             "pca_get_stats": (i32, [vp, ctypes.POINTER(pca_stats)]),
             "pca_halo_ptrs": (i32, [vp, ctypes.POINTER(pca_halo)]),
             "pca_peer_info": (i32, [vp, ctypes.POINTER(pca_peer)]),
+            "pca_stage_input": (i32, [vp, vp]),
+            "pca_reset_staged": (i32, [vp]),
             "pca_ipc_handle": (i32, [vp, vp, ctypes.POINTER(ctypes.c_uint64)]),
             "pca_open_peer": (i32, [vp, vp, ctypes.c_uint64, ctypes.POINTER(pca_config), ctypes.POINTER(pca_peer)]),
             "pca_close_peer": (i32, [ctypes.POINTER(pca_peer)]),
@@ -228,6 +230,15 @@ class PcaContext:
     # ---- ABI wrappers (same names) ----
     def pca_reset(self, g=None, x0=None):
         _check(lib().pca_reset(self.handle, _ptr(g), _ptr(x0)), "pca_reset")
+
+    def pca_stage_input(self, g):
+        """Copy the next reset's g on the internal copy stream (overlaps the work after it)."""
+        self._staged_input = g  # keep the host buffer alive until pca_reset_staged
+        _check(lib().pca_stage_input(self.handle, _ptr(g)), "pca_stage_input")
+
+    def pca_reset_staged(self):
+        _check(lib().pca_reset_staged(self.handle), "pca_reset_staged")
+        self._staged_input = None
 
     def pca_sweep(self, n: int):
         _check(lib().pca_sweep(self.handle, int(n)), "pca_sweep")

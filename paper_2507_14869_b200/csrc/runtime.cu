@@ -121,7 +121,7 @@ struct Layout {
     size_t off_bthr = 0;                    // binary PCA thresholds [THR_ENTRIES]
     size_t off_gbthr = 0;                   // binary Gibbs thresholds [GIBBS_THR_PAD]
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
-           off_sums_max = 0, off_flag = 0, off_stage = 0, off_truth = 0, off_io = 0;
+           off_sums_max = 0, off_flag = 0, off_stage = 0, off_truth = 0, off_io = 0, off_in = 0;
     size_t io_bytes = 0;  // one bit-packed image set (packed_io), 0 otherwise
     size_t stage_bytes = 0, counts_bytes = 0, total = 0;
 };
@@ -217,6 +217,7 @@ Layout make_layout(const pca_config* c) {
     L.off_truth = o; o = align256(o + B * R * W);  // staged truth (pca_stage_truth)
     L.io_bytes = c->packed_io ? B * R * (size_t)((c->width + 7) / 8) : 0;
     L.off_io = o; o = align256(o + 3 * align256(L.io_bytes));  // packed in / out / truth
+    L.off_in = o; o = align256(o + (c->packed_io ? L.io_bytes : B * R * W));  // pca_stage_input
     L.total = o;
     return L;
 }
@@ -273,6 +274,10 @@ struct pca_ctx {
     int truth_staged = 0;
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_truth_ready = nullptr, ev_truth_free = nullptr;
+    // pca_stage_input: the next reset's g, copied on the copy stream
+    uint8_t* in_stage = nullptr;
+    int in_staged = 0;
+    cudaEvent_t ev_in_ready = nullptr, ev_in_free = nullptr;
     // device-initiated halo exchange (pca_attach_peers)
     int p2p = 0;
     int has_up = 0, has_dn = 0;
@@ -846,6 +851,7 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->io_in = ctx->ws + L.off_io;
     ctx->io_out = ctx->io_in + align256(L.io_bytes);
     ctx->io_truth = ctx->io_out + align256(L.io_bytes);
+    ctx->in_stage = ctx->ws + L.off_in;
     ctx->uthr = L.uthr_entries ? (uint32_t*)(ctx->ws + L.off_uthr) : nullptr;
     ctx->uthr_host.resize(L.uthr_entries);
     ctx->sparse_host.resize(2 * L.sparse_entries);
@@ -1313,16 +1319,52 @@ pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, doubl
     return PCA_OK;
 }
 
+static pca_status ensure_copy_stream(pca_ctx* ctx) {
+    if (ctx->copy) return PCA_OK;
+    CK(ctx, cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ctx->ev_truth_ready, &ctx->ev_truth_free, &ctx->ev_in_ready, &ctx->ev_in_free})
+        CK(ctx, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    CK(ctx, cudaEventRecord(ctx->ev_truth_free, ctx->stream));
+    CK(ctx, cudaEventRecord(ctx->ev_in_free, ctx->stream));
+    return PCA_OK;
+}
+
+pca_status pca_stage_input(pca_ctx* ctx, const uint8_t* g) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!g) return fail(PCA_EINVAL, "g is NULL");
+    st = check_same_device(ctx, g, "staged input");
+    if (st != PCA_OK) return st;
+    st = ensure_copy_stream(ctx);
+    if (st != PCA_OK) return st;
+    // the previous staged input must have been consumed by its reset
+    CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev_in_free, 0));
+    const size_t bytes = ctx->cfg.packed_io ? ctx->lay.io_bytes : dense_bytes(ctx);
+    CK(ctx, cudaMemcpyAsync(ctx->in_stage, g, bytes, cudaMemcpyDefault, ctx->copy));
+    CK(ctx, cudaEventRecord(ctx->ev_in_ready, ctx->copy));
+    ctx->in_staged = 1;
+    return PCA_OK;
+}
+
+pca_status pca_reset_staged(pca_ctx* ctx) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!ctx->in_staged) return fail(PCA_EINVAL, "no input staged (pca_stage_input)");
+    CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_in_ready, 0));
+    ctx->in_staged = 0;
+    // the staged bytes are a device copy of the caller's argument: the pca_reset path
+    st = do_reset(ctx, ctx->in_stage, nullptr);
+    if (st != PCA_OK) return st;
+    CK(ctx, cudaEventRecord(ctx->ev_in_free, ctx->stream));
+    return PCA_OK;
+}
+
 pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth) {
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!truth) return fail(PCA_EINVAL, "truth is NULL");
-    if (!ctx->copy) {
-        CK(ctx, cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
-        CK(ctx, cudaEventCreateWithFlags(&ctx->ev_truth_ready, cudaEventDisableTiming));
-        CK(ctx, cudaEventCreateWithFlags(&ctx->ev_truth_free, cudaEventDisableTiming));
-        CK(ctx, cudaEventRecord(ctx->ev_truth_free, ctx->stream));
-    }
+    st = ensure_copy_stream(ctx);
+    if (st != PCA_OK) return st;
     // the previous finalize's read of the buffer comes first
     CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev_truth_free, 0));
     if (ctx->cfg.packed_io) {
@@ -1719,6 +1761,8 @@ pca_status pca_destroy(pca_ctx* ctx) {
         cudaStreamDestroy(ctx->copy);
         cudaEventDestroy(ctx->ev_truth_ready);
         cudaEventDestroy(ctx->ev_truth_free);
+        cudaEventDestroy(ctx->ev_in_ready);
+        cudaEventDestroy(ctx->ev_in_free);
     }
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     delete ctx;

@@ -713,3 +713,29 @@ def test_contexts_driven_from_concurrent_host_threads(cuda_device):
         t.join()
     for i in range(len(shapes)):
         assert np.array_equal(alone[i][0], together[i][0]) and np.array_equal(alone[i][1], together[i][1])
+
+
+@pytest.mark.parametrize("packed", [0, 1])
+def test_staged_input_reset_equals_direct_reset(cuda_device, packed):
+    """pca_stage_input + pca_reset_staged (the copy on the copy stream, overlapping the sweeps
+    enqueued after it) is pca_reset with that g: same chain, counts and metrics; host and
+    device sources; an unstaged reset is an error."""
+    import torch
+
+    H, W = 40, 77
+    g1 = synth.degrade(synth.smooth_labels(H, W, 2, 3), 2, 0.4, 4)[None]
+    g2 = synth.degrade(synth.smooth_labels(H, W, 2, 5), 2, 0.4, 6)[None]
+    enc = (lambda a: P.pack_bits(a)) if packed else (lambda a: a)
+    kw = dict(sigma=0.4, seed=5, mpm_burn_in=2, packed_io=packed)
+    a = P.PcaContext(P.make_config(H, W, 2, **kw), np.ascontiguousarray(enc(g1)))
+    b = P.PcaContext(P.make_config(H, W, 2, **kw), np.ascontiguousarray(enc(g1)))
+    with pytest.raises(P.PcaError, match="staged"):
+        b.pca_reset_staged()
+    for src in (np.ascontiguousarray(enc(g2)), torch.from_numpy(np.ascontiguousarray(enc(g1))).cuda()):
+        b.pca_stage_input(src)
+        b.pca_sweep(3)                # the copy overlaps these sweeps
+        b.pca_reset_staged()
+        a.pca_reset(src)
+        a.pca_sweep(6)
+        b.pca_sweep(6)
+        assert np.array_equal(a.state(), b.state()) and np.array_equal(a.counts(), b.counts())
