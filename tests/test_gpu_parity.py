@@ -739,3 +739,32 @@ def test_staged_input_reset_equals_direct_reset(cuda_device, packed):
         a.pca_sweep(6)
         b.pca_sweep(6)
         assert np.array_equal(a.state(), b.state()) and np.array_equal(a.counts(), b.counts())
+
+
+def test_largest_single_lattice_32768_squared(cuda_device):
+    """Config 4's whole 32768 x 32768 torus (1.07e9 sites, the P = 8 lattice) in ONE context on
+    one GPU (~10 GB of workspace of the 180 GB): sampled rows of the last of four sweeps
+    recomputed by the oracle from the GPU's x_t, and the MPM counts equal the sum of the four
+    states at every site."""
+    H = W = 32768
+    g = synth.tiled_labels(H, W, 2, seed=21)  # a smooth two-level field as the observation
+    cfg = P.make_config(H, W, 2, neighborhood=8, periodic=True, sigma=0.5, beta0=1.5,
+                        beta_step=0.0, seed=13, mpm_burn_in=0)
+    ctx = P.PcaContext(cfg, g[None])
+    acc = np.zeros((H, W), np.uint16)
+    for _ in range(3):
+        ctx.pca_sweep(1)
+        acc += ctx.state()[0]
+    x3 = ctx.state()[0]
+    ctx.pca_sweep(1)
+    x4 = ctx.state()[0]
+    acc += x4
+    m = oracle_model(cfg)
+    rows = sorted({0, 1, H - 1, H // 2} | set(np.random.default_rng(3).integers(0, H, 6).tolist()))
+    tally = Tally()
+    for r in rows:
+        ref, mg = orc.pca_sweep(m, x3, g, 1.5, cfg.seed, 0, 3, rows=(r, r + 1))
+        tally.add(x4[r], ref[0], mg[0])
+    tally.check()
+    assert np.array_equal(ctx.counts()[0], acc)
+    ctx.pca_destroy()

@@ -61,6 +61,11 @@ def main():
                         P.make_config(4096, 32768, 2, periodic=True, sigma=0.5, beta0=1.5, beta_step=0,
                                       mpm_burn_in=0), c4, 50))
     if not quick:
+        c4w = synth.tiled_labels(32768, 32768, 2, 21)[None]
+        out.append(time_cfg("c4 whole lattice 32768x32768 l2 moore torus mpm on ONE GPU",
+                            P.make_config(32768, 32768, 2, periodic=True, sigma=0.5, beta0=1.5, beta_step=0,
+                                          mpm_burn_in=0), c4w, 20))
+        del c4w
         big5 = synth.degrade(synth.tiled_labels(8192, 8192, 5, 1), 5, 0.25, 2)[None]
         out.append(time_cfg("c3 l5 moore torus mpm", P.make_config(8192, 8192, 5, periodic=True, sigma=0.25, beta0=1.5, beta_step=0, mpm_burn_in=0), big5, 10))
         B = 128
