@@ -160,6 +160,10 @@ typedef struct pca_peer {
     int64_t chain_stride;
 } pca_peer;
 
+/* Devices: a context lives on the device that was current at pca_init.  Every call that
+ * takes a context runs on that device and restores the caller's current device before it
+ * returns, so one host thread may drive contexts on several GPUs. */
+
 /* Version of this ABI (PCA_ABI_VERSION). */
 int32_t pca_abi_version(void);
 

@@ -306,6 +306,18 @@ pca_status cuda_fail(pca_ctx* ctx, cudaError_t e, const char* where) {
         if (e_ != 0) return cuda_fail((ctx), (cudaError_t)e_, #expr);            \
     } while (0)
 
+// Every ABI call that takes a context runs on the context's device (usable() makes it
+// current) and gives the caller's current device back when it returns.
+struct DeviceScope {
+    int prev = -1;
+    DeviceScope() {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 pca_status usable(pca_ctx* ctx) {
     if (!ctx) return fail(PCA_EINVAL, "context is NULL");
     if (ctx->poisoned)
@@ -917,12 +929,14 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
 }
 
 pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     return do_reset(ctx, g, x0);
 }
 
 pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
@@ -1072,6 +1086,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
 }
 
 pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
@@ -1188,6 +1203,7 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
 }
 
 pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
@@ -1232,6 +1248,7 @@ pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
 }
 
 pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int64_t* sums) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!truth || !sums) return fail(PCA_EINVAL, "truth and sums must be non-NULL");
@@ -1308,6 +1325,7 @@ bool metrics_from_sums(const int64_t* v, int levels, double* psnr, double* ssim)
 
 pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* psnr,
                          double* ssim) {
+    DeviceScope device_scope_;
     if (!psnr || !ssim) return fail(PCA_EINVAL, "psnr and ssim must be non-NULL");
     std::vector<int64_t> s((size_t)(ctx ? ctx->cfg.batch : 1) * 8);
     pca_status st = pca_metric_sums(ctx, truth, kind, s.data());
@@ -1330,6 +1348,7 @@ static pca_status ensure_copy_stream(pca_ctx* ctx) {
 }
 
 pca_status pca_stage_input(pca_ctx* ctx, const uint8_t* g) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!g) return fail(PCA_EINVAL, "g is NULL");
@@ -1347,6 +1366,7 @@ pca_status pca_stage_input(pca_ctx* ctx, const uint8_t* g) {
 }
 
 pca_status pca_reset_staged(pca_ctx* ctx) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!ctx->in_staged) return fail(PCA_EINVAL, "no input staged (pca_stage_input)");
@@ -1360,6 +1380,7 @@ pca_status pca_reset_staged(pca_ctx* ctx) {
 }
 
 pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!truth) return fail(PCA_EINVAL, "truth is NULL");
@@ -1381,6 +1402,7 @@ pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth) {
 
 pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
                         double* ssim) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!psnr || !ssim) return fail(PCA_EINVAL, "psnr and ssim must be non-NULL");
@@ -1457,6 +1479,7 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
 }
 
 pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* ssim) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!truth || !ssim) return fail(PCA_EINVAL, "truth and ssim must be non-NULL");
@@ -1511,6 +1534,7 @@ pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, d
 }
 
 pca_status pca_changed_sites(pca_ctx* ctx, int64_t* changed) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!changed) return fail(PCA_EINVAL, "changed is NULL");
@@ -1531,6 +1555,7 @@ pca_status pca_changed_sites(pca_ctx* ctx, int64_t* changed) {
 pca_status pca_read_state(pca_ctx* ctx, uint8_t* out) { return pca_estimate(ctx, PCA_EST_LAST, out); }
 
 pca_status pca_write_state(pca_ctx* ctx, const uint8_t* x) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!x) return fail(PCA_EINVAL, "x is NULL");
@@ -1541,6 +1566,7 @@ pca_status pca_write_state(pca_ctx* ctx, const uint8_t* x) {
 }
 
 pca_status pca_read_counts(pca_ctx* ctx, uint16_t* out) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
@@ -1553,6 +1579,7 @@ pca_status pca_read_counts(pca_ctx* ctx, uint16_t* out) {
 }
 
 pca_status pca_write_counts(pca_ctx* ctx, const uint16_t* cin, int64_t counted) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!cin || counted < 0 || counted > 65535) return fail(PCA_EINVAL, "bad counts arguments");
@@ -1566,6 +1593,7 @@ pca_status pca_write_counts(pca_ctx* ctx, const uint16_t* cin, int64_t counted) 
 }
 
 pca_status pca_set_step(pca_ctx* ctx, int64_t t) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (t < 0 || t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EINVAL, "t out of range");
@@ -1574,6 +1602,7 @@ pca_status pca_set_step(pca_ctx* ctx, int64_t t) {
 }
 
 pca_status pca_get_stats(pca_ctx* ctx, pca_stats* out) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
@@ -1590,6 +1619,7 @@ pca_status pca_get_stats(pca_ctx* ctx, pca_stats* out) {
 }
 
 pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
@@ -1605,6 +1635,7 @@ pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out) {
 }
 
 pca_status pca_peer_info(pca_ctx* ctx, pca_peer* out) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
@@ -1619,6 +1650,7 @@ pca_status pca_peer_info(pca_ctx* ctx, pca_peer* out) {
 }
 
 pca_status pca_ipc_handle(pca_ctx* ctx, void* handle64, uint64_t* offset) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!handle64 || !offset) return fail(PCA_EINVAL, "handle / offset is NULL");
@@ -1643,6 +1675,7 @@ pca_status pca_ipc_handle(pca_ctx* ctx, void* handle64, uint64_t* offset) {
 
 pca_status pca_open_peer(pca_ctx* ctx, const void* handle64, uint64_t offset,
                          const pca_config* peer_cfg, pca_peer* out) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!handle64 || !peer_cfg || !out) return fail(PCA_EINVAL, "handle / config / out is NULL");
@@ -1681,6 +1714,7 @@ pca_status pca_close_peer(pca_peer* peer) {
 }
 
 pca_status pca_attach_peers(pca_ctx* ctx, const pca_peer* up, const pca_peer* down) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (ctx->lay.rows == ctx->cfg.height) return fail(PCA_EINVAL, "peers need a row-strip context");
@@ -1720,6 +1754,7 @@ pca_status pca_nccl_unique_id(void* id128) {
 }
 
 pca_status pca_attach_nccl(pca_ctx* ctx, const void* id128, int32_t nranks, int32_t rank) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!id128 || nranks < 1 || rank < 0 || rank >= nranks)
@@ -1741,12 +1776,14 @@ pca_status pca_attach_nccl(pca_ctx* ctx, const void* id128, int32_t nranks, int3
 }
 
 pca_status pca_sync(pca_ctx* ctx) {
+    DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     return sync(ctx);
 }
 
 pca_status pca_destroy(pca_ctx* ctx) {
+    DeviceScope device_scope_;
     if (!ctx) return PCA_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
