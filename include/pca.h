@@ -219,13 +219,16 @@ pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth);
 /* Stage the NEXT reset's observed image g (host or device, the layout of pca_init's g; bit-
  * packed with packed_io) into the context on the internal copy stream, so the transfer overlaps
  * the work enqueued after it; pca_reset_staged then resets from it (x0 = g), waiting for the
- * copy on the device, not the host.  Host memory must stay valid until that reset returns
+ * copy on the device, not the host.  Host memory must stay valid until the copy has run:
+ * until that reset returns, or with packed_io until the next synchronising call after it
  * (pinned memory makes the copy truly asynchronous).  A second pca_stage_input waits for the
  * first to be consumed.  Asynchronous. */
 pca_status pca_stage_input(pca_ctx* ctx, const uint8_t* g);
 
 /* pca_reset(ctx, g_staged, NULL) with the image of the last pca_stage_input; PCA_EINVAL when
- * nothing is staged.  Synchronises like pca_reset. */
+ * nothing is staged.  Synchronises like pca_reset, except with packed_io: bit-unpacked labels
+ * are valid by construction, so the level check and its host synchronisation are skipped and
+ * the call is asynchronous. */
 pca_status pca_reset_staged(pca_ctx* ctx);
 
 /* The end of a run in ONE fused pass over truth, the current state and the counts

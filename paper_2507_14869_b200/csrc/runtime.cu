@@ -761,19 +761,23 @@ pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
     return PCA_OK;
 }
 
+// `checked` = src is known to hold labels < levels (the validated g, or bits unpacked by
+// packed_io): the level check and its host synchronisation are skipped
 pca_status load_state(pca_ctx* ctx, const uint8_t* src, int pitch, long long chain_stride,
-                      const char* what) {
+                      const char* what, bool checked = false) {
     ctx->prev_valid = 0;
     CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
     LAUNCH(ctx, launch_pack_state(ctx->geo, src, pitch, chain_stride, ctx->x[ctx->cur],
                                   ctx->cfg.batch, ctx->flag, ctx->stream));
-    pca_status st = check_flag(ctx, what);
-    if (st != PCA_OK) return st;
+    if (!checked) {
+        pca_status st = check_flag(ctx, what);
+        if (st != PCA_OK) return st;
+    }
     if (ctx->p2p) return p2p_push(ctx, ctx->cur);
     return exchange(ctx, ctx->x[ctx->cur]);
 }
 
-pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
+pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool staged = false) {
     const pca_config& c = ctx->cfg;
     const Layout& L = ctx->lay;
     if (g) {
@@ -784,8 +788,13 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
         CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
         LAUNCH(ctx, launch_pack_g(ctx->geo, dg, c.width, (long long)L.rows * c.width, ctx->g,
                                   c.batch, ctx->flag, ctx->stream));
-        st = check_flag(ctx, "g");
-        if (st != PCA_OK) return st;
+        // the check's host synchronisation also ends the caller's buffer lifetime at return;
+        // it is skipped only for the context's own staged copy holding bit-unpacked labels
+        // (packed_io, levels == 2: 0/1 by construction)
+        if (!(staged && c.packed_io)) {
+            st = check_flag(ctx, "g");
+            if (st != PCA_OK) return st;
+        }
     }
     // free boundary: halos and padding hold the sentinel 0xFF; torus: halos are rewritten by
     // every sweep and padding is 0 (a valid label, so SWAR sums need no masking)
@@ -809,7 +818,9 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
         if (st != PCA_OK) return st;
         return load_state(ctx, dx, c.width, (long long)L.rows * c.width, "x0");
     }
-    return load_state(ctx, ctx->g + (size_t)GHALO * L.gpitch + XOFF, L.gpitch, ctx->geo.gchain, "g");
+    // x0 = g: g's labels were checked when it was loaded
+    return load_state(ctx, ctx->g + (size_t)GHALO * L.gpitch + XOFF, L.gpitch, ctx->geo.gchain, "g",
+                      true);
 }
 
 }  // namespace
@@ -1373,7 +1384,7 @@ pca_status pca_reset_staged(pca_ctx* ctx) {
     CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_in_ready, 0));
     ctx->in_staged = 0;
     // the staged bytes are a device copy of the caller's argument: the pca_reset path
-    st = do_reset(ctx, ctx->in_stage, nullptr);
+    st = do_reset(ctx, ctx->in_stage, nullptr, true);
     if (st != PCA_OK) return st;
     CK(ctx, cudaEventRecord(ctx->ev_in_free, ctx->stream));
     return PCA_OK;
