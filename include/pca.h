@@ -241,6 +241,15 @@ pca_status pca_reset_staged(pca_ctx* ctx);
 pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
                         double* ssim);
 
+/* pca_finalize, except that a host mpm_out (or any mpm_out with packed_io) is filled on the
+ * context's copy stream: PSNR / SSIM are returned as by pca_finalize, but the MPM image may
+ * still be in flight at return, so that its device->host copy overlaps the work enqueued next
+ * (the next run's reset and sweeps).  mpm_out must stay valid and unread until pca_sync; later
+ * calls that reuse the context's output staging wait for the copy on the device.  A device
+ * mpm_out without packed_io is written as by pca_finalize.  Same errors as pca_finalize. */
+pca_status pca_finalize_async(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
+                              double* ssim);
+
 /* Windowed SSIM (R16's secondary metric, the form Table 1 of PAPER.md:703 appears to use):
  * the mean over every 7x7 window position inside the image (stride 1, no padding) of
  *   SSIM_w = (2 mx my + c1)(2 sxy + c2) / ((mx^2 + my^2 + c1)(sx^2 + sy^2 + c2)),
@@ -321,7 +330,8 @@ pca_status pca_open_peer(pca_ctx* ctx, const void* handle64, uint64_t offset, co
 pca_status pca_close_peer(pca_peer* peer);
 pca_status pca_attach_peers(pca_ctx* ctx, const pca_peer* up, const pca_peer* down);
 
-/* Synchronise the context's stream and report any pending asynchronous error. */
+/* Synchronise the context's stream and its copy stream (staged inputs, pca_finalize_async's
+ * image) and report any pending asynchronous error. */
 pca_status pca_sync(pca_ctx* ctx);
 
 /* Destroy the context (and its NCCL communicator).  Never frees caller memory. */

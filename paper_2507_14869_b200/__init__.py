@@ -35,7 +35,8 @@ EXPORTS = ["pca_abi_version", "pca_workspace_bytes", "pca_init", "pca_reset", "p
            "pca_write_state", "pca_read_counts", "pca_write_counts", "pca_set_step",
            "pca_get_stats", "pca_halo_ptrs", "pca_nccl_unique_id", "pca_attach_nccl", "pca_sync",
            "pca_destroy", "pca_last_error", "pca_peer_info", "pca_ipc_handle", "pca_open_peer",
-           "pca_close_peer", "pca_attach_peers", "pca_stage_input", "pca_reset_staged"]
+           "pca_close_peer", "pca_attach_peers", "pca_stage_input", "pca_reset_staged",
+           "pca_finalize_async"]
 
 
 class PcaError(RuntimeError):
@@ -104,6 +105,7 @@ def lib():
             "pca_psnr_ssim": (i32, [vp, vp, i32, vp, vp]),
             "pca_ssim_windowed": (i32, [vp, vp, i32, vp]),
             "pca_finalize": (i32, [vp, vp, vp, vp, vp]),
+            "pca_finalize_async": (i32, [vp, vp, vp, vp, vp]),
             "pca_stage_truth": (i32, [vp, vp]),
             "pca_changed_sites": (i32, [vp, vp]),
             "pca_read_state": (i32, [vp, vp]),
@@ -277,6 +279,17 @@ class PcaContext:
         s = np.zeros((self.cfg.batch, 2), np.float64)
         _check(lib().pca_finalize(self.handle, _ptr(truth), _ptr(mpm_out), p.ctypes.data,
                                   s.ctypes.data), "pca_finalize")
+        return p, s
+
+    def pca_finalize_async(self, truth, mpm_out):
+        """pca_finalize with the MPM image's copy into host mpm_out on the copy stream: the
+        image may still be in flight at return (pca_sync waits for it); keep mpm_out alive
+        and unread until then."""
+        self._async_out = mpm_out  # keep the buffer alive until the copy has run
+        p = np.zeros((self.cfg.batch, 2), np.float64)
+        s = np.zeros((self.cfg.batch, 2), np.float64)
+        _check(lib().pca_finalize_async(self.handle, _ptr(truth), _ptr(mpm_out), p.ctypes.data,
+                                        s.ctypes.data), "pca_finalize_async")
         return p, s
 
     def pca_ssim_windowed(self, truth, kind: int):

@@ -278,6 +278,8 @@ struct pca_ctx {
     uint8_t* in_stage = nullptr;
     int in_staged = 0;
     cudaEvent_t ev_in_ready = nullptr, ev_in_free = nullptr;
+    // pca_finalize_async: the MPM image's device->host copy on the copy stream
+    cudaEvent_t ev_out_ready = nullptr, ev_out_free = nullptr;
     // device-initiated halo exchange (pca_attach_peers)
     int p2p = 0;
     int has_up = 0, has_dn = 0;
@@ -1213,6 +1215,13 @@ pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
     return PCA_OK;
 }
 
+// the output staging (stage past the input image, io_out, the stage's float planes) may still
+// be read by an asynchronous MPM image copy (pca_finalize_async): writers wait on the device
+static pca_status wait_out_free(pca_ctx* ctx) {
+    if (ctx->copy) CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_out_free, 0));
+    return PCA_OK;
+}
+
 pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
     DeviceScope device_scope_;
     pca_status st = usable(ctx);
@@ -1226,6 +1235,8 @@ pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
     if (st != PCA_OK) return st;
     const bool dev = is_device_ptr(out);
     const size_t plane = (size_t)ctx->lay.rows * c.width;
+    st = wait_out_free(ctx);
+    if (st != PCA_OK) return st;
     if (kind == PCA_EST_LAST || kind == PCA_EST_MPM) {
         uint8_t* dst = (dev && !c.packed_io) ? (uint8_t*)out : ctx->stage;
         if (kind == PCA_EST_LAST)
@@ -1351,10 +1362,12 @@ pca_status pca_psnr_ssim(pca_ctx* ctx, const uint8_t* truth, int32_t kind, doubl
 static pca_status ensure_copy_stream(pca_ctx* ctx) {
     if (ctx->copy) return PCA_OK;
     CK(ctx, cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ctx->ev_truth_ready, &ctx->ev_truth_free, &ctx->ev_in_ready, &ctx->ev_in_free})
+    for (cudaEvent_t* e : {&ctx->ev_truth_ready, &ctx->ev_truth_free, &ctx->ev_in_ready,
+                           &ctx->ev_in_free, &ctx->ev_out_ready, &ctx->ev_out_free})
         CK(ctx, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CK(ctx, cudaEventRecord(ctx->ev_truth_free, ctx->stream));
     CK(ctx, cudaEventRecord(ctx->ev_in_free, ctx->stream));
+    CK(ctx, cudaEventRecord(ctx->ev_out_free, ctx->stream));
     return PCA_OK;
 }
 
@@ -1411,9 +1424,8 @@ pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth) {
     return PCA_OK;
 }
 
-pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
-                        double* ssim) {
-    DeviceScope device_scope_;
+static pca_status finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
+                           double* ssim, bool async_image) {
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
     if (!psnr || !ssim) return fail(PCA_EINVAL, "psnr and ssim must be non-NULL");
@@ -1435,6 +1447,15 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
     }
     const bool dev_out = mpm_out && is_device_ptr(mpm_out) && !c.packed_io;
     uint8_t* mo = mpm_out ? (dev_out ? mpm_out : ctx->stage + align256(dense_bytes(ctx))) : nullptr;
+    const bool async_copy = async_image && mpm_out && !dev_out;
+    if (async_copy) {
+        st = ensure_copy_stream(ctx);
+        if (st != PCA_OK) return st;
+    }
+    if (mpm_out && !dev_out) {
+        st = wait_out_free(ctx);  // the previous asynchronous image copy has read the staging
+        if (st != PCA_OK) return st;
+    }
     const size_t nb = (size_t)c.batch * 16 * sizeof(unsigned long long);
     CK(ctx, cudaMemsetAsync(ctx->sums, 0, nb, ctx->stream));
     MetricParams mp;
@@ -1465,12 +1486,23 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
     CK(ctx, cudaMemcpyAsync(h.data(), ctx->sums, nb, cudaMemcpyDeviceToHost, ctx->stream));
     if (ctx->comm && ctx->nranks > 1)
         CK(ctx, cudaMemcpyAsync(hm.data(), ctx->sums_max, nb, cudaMemcpyDeviceToHost, ctx->stream));
-    if (mpm_out && c.packed_io) {  // bit-packed MPM image
-        LAUNCH(ctx, launch_pack_bits(mo, ctx->io_out, c.width, (long long)c.batch * ctx->lay.rows,
-                                     ctx->stream));
-        CK(ctx, cudaMemcpyAsync(mpm_out, ctx->io_out, ctx->lay.io_bytes, cudaMemcpyDefault, ctx->stream));
-    } else if (mpm_out && !dev_out) {
-        CK(ctx, cudaMemcpyAsync(mpm_out, mo, dense_bytes(ctx), cudaMemcpyDeviceToHost, ctx->stream));
+    if (mpm_out && !dev_out) {
+        const uint8_t* src = mo;
+        size_t bytes = dense_bytes(ctx);
+        if (c.packed_io) {  // bit-packed MPM image
+            LAUNCH(ctx, launch_pack_bits(mo, ctx->io_out, c.width, (long long)c.batch * ctx->lay.rows,
+                                         ctx->stream));
+            src = ctx->io_out;
+            bytes = ctx->lay.io_bytes;
+        }
+        if (async_copy) {  // on the copy stream: overlaps whatever is enqueued after this call
+            CK(ctx, cudaEventRecord(ctx->ev_out_ready, ctx->stream));
+            CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev_out_ready, 0));
+            CK(ctx, cudaMemcpyAsync(mpm_out, src, bytes, cudaMemcpyDefault, ctx->copy));
+            CK(ctx, cudaEventRecord(ctx->ev_out_free, ctx->copy));
+        } else {
+            CK(ctx, cudaMemcpyAsync(mpm_out, src, bytes, cudaMemcpyDefault, ctx->stream));
+        }
     }
     st = sync(ctx);
     if (st != PCA_OK) return st;
@@ -1489,6 +1521,18 @@ pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, do
     return PCA_OK;
 }
 
+pca_status pca_finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
+                        double* ssim) {
+    DeviceScope device_scope_;
+    return finalize(ctx, truth, mpm_out, psnr, ssim, false);
+}
+
+pca_status pca_finalize_async(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
+                              double* ssim) {
+    DeviceScope device_scope_;
+    return finalize(ctx, truth, mpm_out, psnr, ssim, true);
+}
+
 pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* ssim) {
     DeviceScope device_scope_;
     pca_status st = usable(ctx);
@@ -1503,6 +1547,8 @@ pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, d
         return fail(PCA_EUNSUPPORTED, "windowed SSIM needs the whole lattice (not a row strip)");
     if (c.height < SSIM_WIN || c.width < SSIM_WIN)
         return fail(PCA_EINVAL, "windowed SSIM needs height, width >= %d", SSIM_WIN);
+    st = wait_out_free(ctx);
+    if (st != PCA_OK) return st;
     const uint8_t* dt = nullptr;
     st = device_input(ctx, truth, &dt);  // host truth -> stage[0, BRW)
     if (st != PCA_OK) return st;
@@ -1790,6 +1836,7 @@ pca_status pca_sync(pca_ctx* ctx) {
     DeviceScope device_scope_;
     pca_status st = usable(ctx);
     if (st != PCA_OK) return st;
+    if (ctx->copy) CK(ctx, cudaStreamSynchronize(ctx->copy));  // staged copies, async images
     return sync(ctx);
 }
 
@@ -1811,6 +1858,8 @@ pca_status pca_destroy(pca_ctx* ctx) {
         cudaEventDestroy(ctx->ev_truth_free);
         cudaEventDestroy(ctx->ev_in_ready);
         cudaEventDestroy(ctx->ev_in_free);
+        cudaEventDestroy(ctx->ev_out_ready);
+        cudaEventDestroy(ctx->ev_out_free);
     }
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     delete ctx;

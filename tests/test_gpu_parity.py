@@ -741,6 +741,39 @@ def test_staged_input_reset_equals_direct_reset(cuda_device, packed):
         assert np.array_equal(a.state(), b.state()) and np.array_equal(a.counts(), b.counts())
 
 
+@pytest.mark.parametrize("packed", [0, 1])
+def test_finalize_async_equals_finalize(cuda_device, packed):
+    """pca_finalize_async (the MPM image's device->host copy on the copy stream, overlapping
+    the next run's reset and sweeps) gives pca_finalize's metrics and, after pca_sync, its
+    image, run after run into the same pinned buffer; an estimate issued while a copy is in
+    flight waits for it and is itself correct."""
+    import torch
+
+    H, W = 48, 83
+    truth = synth.smooth_labels(H, W, 2, 7)[None]
+    gs = [synth.degrade(truth[0], 2, 0.45, s)[None] for s in (8, 9, 10)]
+    enc = (lambda a: P.pack_bits(a)) if packed else (lambda a: a)
+    kw = dict(sigma=0.45, seed=11, mpm_burn_in=1, packed_io=packed)
+    a = P.PcaContext(P.make_config(H, W, 2, **kw), np.ascontiguousarray(enc(gs[0])))
+    b = P.PcaContext(P.make_config(H, W, 2, **kw), np.ascontiguousarray(enc(gs[0])))
+    t_h = torch.from_numpy(np.ascontiguousarray(enc(truth))).pin_memory()
+    out_a = np.zeros(t_h.shape, np.uint8)
+    out_b = torch.zeros(tuple(t_h.shape), dtype=torch.uint8).pin_memory()
+    for i, g in enumerate(gs):
+        a.pca_reset(np.ascontiguousarray(enc(g)))
+        a.pca_sweep(5 + i)
+        pa, sa = a.pca_finalize(t_h.numpy(), out_a)
+        if i:  # the previous run's image copy may still be in flight: reset/sweep overlap it
+            b.pca_reset(np.ascontiguousarray(enc(g)))
+        b.pca_sweep(5 + i)
+        pb, sb = b.pca_finalize_async(t_h, out_b)
+        assert np.array_equal(pa, pb) and np.array_equal(sa, sb)
+        est = np.zeros(t_h.shape, np.uint8)
+        b.pca_estimate(P.EST_MPM, est)  # reuses the output staging: waits for the copy
+        b.pca_sync()
+        assert np.array_equal(out_b.numpy(), out_a) and np.array_equal(est, out_a)
+
+
 def test_largest_single_lattice_32768_squared(cuda_device):
     """Config 4's whole 32768 x 32768 torus (1.07e9 sites, the P = 8 lattice) in ONE context on
     one GPU (~10 GB of workspace of the 180 GB): sampled rows of the last of four sweeps
