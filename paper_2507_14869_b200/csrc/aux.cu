@@ -236,6 +236,17 @@ __global__ void __launch_bounds__(TPB) metric_sums_kernel(const MetricParams p) 
                 }
             }
             const uint32_t tw[4] = {tv.x & msk[0], tv.y & msk[1], tv.z & msk[2], tv.w & msk[3]};
+            if (BOTH && p.mpm_bits) {  // 16 labels 0/1 -> 16 bits, site c0 + j at bit j
+                const uint32_t yw[4] = {yv[1].x & msk[0], yv[1].y & msk[1], yv[1].z & msk[2],
+                                        yv[1].w & msk[3]};
+                uint32_t bits = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)  // byte k's bit 0 lands on bit 24 + k, no carries
+                    bits |= (((yw[i] & 0x01010101u) * 0x01020408u) >> 24) << (4 * i);
+                uint8_t* bp = p.mpm_bits + ((long long)chain * G.rows + r) * ((G.W + 7) >> 3) + (c0 >> 3);
+                bp[0] = (uint8_t)bits;
+                if (n > 8) bp[1] = (uint8_t)(bits >> 8);
+            }
             uint32_t sx = 0, sxx = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {

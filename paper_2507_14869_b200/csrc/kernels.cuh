@@ -150,6 +150,8 @@ struct MetricParams {
     int kind;              // 0 LAST, 1 MPM, 2 both in one pass (finalize)
     int nsamp;             // counted sweeps (MPM ties for levels == 2)
     uint8_t* mpm_out;      // kind 2: dense MPM image [batch][rows][W], or nullptr
+    uint8_t* mpm_bits = nullptr;  // kind 2, levels == 2: bit-packed MPM image
+                                  // [batch][rows][(W+7)/8], site c at bit c%8 of byte c/8
 };
 
 // Per-device launch facts (occupancy, SM count) cached on first use on each device:

@@ -1446,7 +1446,10 @@ static pca_status finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out,
         if (st != PCA_OK) return st;
     }
     const bool dev_out = mpm_out && is_device_ptr(mpm_out) && !c.packed_io;
-    uint8_t* mo = mpm_out ? (dev_out ? mpm_out : ctx->stage + align256(dense_bytes(ctx))) : nullptr;
+    // packed_io: the finalisation pass writes the bit-packed image itself (into io_out)
+    const bool packed_out = mpm_out && c.packed_io;
+    uint8_t* mo = (mpm_out && !packed_out)
+                      ? (dev_out ? mpm_out : ctx->stage + align256(dense_bytes(ctx))) : nullptr;
     const bool async_copy = async_image && mpm_out && !dev_out;
     if (async_copy) {
         st = ensure_copy_stream(ctx);
@@ -1467,6 +1470,7 @@ static pca_status finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out,
     mp.kind = 2;
     mp.nsamp = (int)ctx->counted;
     mp.mpm_out = mo;
+    mp.mpm_bits = packed_out ? ctx->io_out : nullptr;
     LAUNCH(ctx, launch_metric_sums(mp, c.batch, ctx->stream));
     if (!truth) CK(ctx, cudaEventRecord(ctx->ev_truth_free, ctx->stream));
     if (ctx->comm && ctx->nranks > 1) {
@@ -1487,14 +1491,8 @@ static pca_status finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out,
     if (ctx->comm && ctx->nranks > 1)
         CK(ctx, cudaMemcpyAsync(hm.data(), ctx->sums_max, nb, cudaMemcpyDeviceToHost, ctx->stream));
     if (mpm_out && !dev_out) {
-        const uint8_t* src = mo;
-        size_t bytes = dense_bytes(ctx);
-        if (c.packed_io) {  // bit-packed MPM image
-            LAUNCH(ctx, launch_pack_bits(mo, ctx->io_out, c.width, (long long)c.batch * ctx->lay.rows,
-                                         ctx->stream));
-            src = ctx->io_out;
-            bytes = ctx->lay.io_bytes;
-        }
+        const uint8_t* src = packed_out ? ctx->io_out : mo;
+        const size_t bytes = packed_out ? ctx->lay.io_bytes : dense_bytes(ctx);
         if (async_copy) {  // on the copy stream: overlaps whatever is enqueued after this call
             CK(ctx, cudaEventRecord(ctx->ev_out_ready, ctx->stream));
             CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->ev_out_ready, 0));

@@ -621,7 +621,7 @@ def test_changed_sites_counts_the_last_sweep(cuda_device, shape, L, n):
         ctx.pca_changed_sites()
 
 
-@pytest.mark.parametrize("W", [64, 77])
+@pytest.mark.parametrize("W", [64, 77, 200])
 def test_packed_io_matches_dense_io(cuda_device, W):
     """packed_io (two levels): bit-packed g / x0 / truth in, bit-packed LAST / MPM / state out,
     host and device buffers, staged truth -- the same chain and metrics as dense I/O."""
