@@ -774,6 +774,41 @@ def test_finalize_async_equals_finalize(cuda_device, packed):
         assert np.array_equal(out_b.numpy(), out_a) and np.array_equal(est, out_a)
 
 
+def test_finalize_async_device_output_none_and_destroy_in_flight(cuda_device):
+    """pca_finalize_async with a device mpm_out (written as by pca_finalize), with no image
+    (metrics only), with a batch of ragged chains into pageable host memory, and a context
+    destroyed while its image copy may still be in flight."""
+    import torch
+
+    H, W, B = 33, 70, 3
+    truth = np.stack([synth.smooth_labels(H, W, 5, seed=30 + b) for b in range(B)])
+    g = np.stack([synth.degrade(truth[b], 5, 0.25, seed=40 + b) for b in range(B)])
+    kw = dict(batch=B, neighborhood=8, periodic=False, sigma=0.25, seed=23, mpm_burn_in=2)
+    a = make_ctx(P.make_config(H, W, 5, **kw), g)
+    b = make_ctx(P.make_config(H, W, 5, **kw), g)
+    for c in (a, b):
+        c.pca_sweep(6)
+    ref = np.zeros((B, H, W), np.uint8)
+    pa, sa = a.pca_finalize(truth, ref)
+    dev = torch.zeros((B, H, W), dtype=torch.uint8, device="cuda")
+    pb, sb = b.pca_finalize_async(truth, dev)
+    assert np.array_equal(pa, pb) and np.array_equal(sa, sb)
+    assert np.array_equal(dev.cpu().numpy(), ref)
+    pn, sn = b.pca_finalize_async(truth, None)
+    assert np.array_equal(pn, pa) and np.array_equal(sn, sa)
+    host = np.zeros((B, H, W), np.uint8)  # pageable
+    b.pca_finalize_async(truth, host)
+    b.pca_sync()
+    assert np.array_equal(host, ref)
+    pinned = torch.zeros((B, H, W), dtype=torch.uint8).pin_memory()
+    b.pca_sweep(1)
+    b.pca_finalize_async(truth, pinned)
+    b.pca_destroy()  # waits for the copy stream before releasing the context
+    a.pca_sweep(1)
+    a.pca_finalize(truth, ref)
+    assert np.array_equal(pinned.numpy(), ref)
+
+
 def test_largest_single_lattice_32768_squared(cuda_device):
     """Config 4's whole 32768 x 32768 torus (1.07e9 sites, the P = 8 lattice) in ONE context on
     one GPU (~10 GB of workspace of the 180 GB): sampled rows of the last of four sweeps
