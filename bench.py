@@ -335,6 +335,9 @@ def run_ours(args):
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
         assert abs(pe[0, 1] - psnr[0, 1]) < 1e-9 and abs(se[0, 1] - ssim[0, 1]) < 1e-12  # same chain
+        # the MPM image that came back asynchronously is the device-timed run's
+        assert np.array_equal(mpm_h.numpy().reshape(-1),
+                              np.asarray(pk(mpm_dev.cpu().numpy())).reshape(-1)), "e2e MPM image differs"
         e2e = {"value": sites_all * S * args.steps / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(g_h.numel() + t_h.numel()),
                "d2h_bytes_per_step": int(mpm_h.numel() + 4 * 8),
