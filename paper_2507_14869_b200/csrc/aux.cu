@@ -52,7 +52,10 @@ __device__ __forceinline__ void store16(uint8_t* row, int c0, int n, bool vec, c
 __global__ void __launch_bounds__(TPB) pack_padded_kernel(Geometry G, const uint8_t* __restrict__ src,
                                                           int src_pitch, long long src_chain,
                                                           uint8_t* __restrict__ dst, long long dpitch,
-                                                          long long dchain, int halo, int* bad) {
+                                                          long long dchain, int halo, int* bad,
+                                                          uint8_t* __restrict__ dst2,
+                                                          long long dpitch2, long long dchain2,
+                                                          int halo2) {
     const int chain = blockIdx.z;
     const int k = blockIdx.x * TPB + threadIdx.x;  // chunk
     const int c0 = 16 * k;
@@ -68,7 +71,6 @@ __global__ void __launch_bounds__(TPB) pack_padded_kernel(Geometry G, const uint
         for (int j = 0; j < n; ++j) m[j >> 2] |= 0xFFu << (8 * (j & 3));
         found |= any_ge(v.x & m[0], lv4) | any_ge(v.y & m[1], lv4) | any_ge(v.z & m[2], lv4) |
                  any_ge(v.w & m[3], lv4);
-        uint8_t* rowp = dst + chain * dchain + (long long)(r + halo) * dpitch;
         auto put = [&](uint8_t* rp) {
             store16(rp + XOFF, c0, n, true, v);
             if (G.periodic) {
@@ -81,11 +83,16 @@ __global__ void __launch_bounds__(TPB) pack_padded_kernel(Geometry G, const uint
                 }
             }
         };
-        put(rowp);
-        if (G.periodic && G.self_halo_rows) {
-            if (r < halo) put(rowp + (long long)G.rows * dpitch);
-            if (r >= G.rows - halo) put(rowp - (long long)G.rows * dpitch);
-        }
+        auto emit = [&](uint8_t* base, long long pitch, long long cstride, int h) {
+            uint8_t* rowp = base + chain * cstride + (long long)(r + h) * pitch;
+            put(rowp);
+            if (G.periodic && G.self_halo_rows) {
+                if (r < h) put(rowp + (long long)G.rows * pitch);
+                if (r >= G.rows - h) put(rowp - (long long)G.rows * pitch);
+            }
+        };
+        emit(dst, dpitch, dchain, halo);
+        if (dst2) emit(dst2, dpitch2, dchain2, halo2);
     }
     if (found) atomicOr(bad, 1);
 }
@@ -470,14 +477,15 @@ int launch_pack_bits(const uint8_t* dense, uint8_t* bits, int W, long long nrows
 int launch_pack_state(const Geometry& G, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad, void* stream) {
     pack_padded_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(
-        G, src, src_pitch, src_chain, xbuf, G.xpitch, G.xchain, HALO, bad);
+        G, src, src_pitch, src_chain, xbuf, G.xpitch, G.xchain, HALO, bad, nullptr, 0, 0, 0);
     return (int)cudaGetLastError();
 }
 
 int launch_pack_g(const Geometry& G, const uint8_t* src, int src_pitch, long long src_chain,
-                  uint8_t* gbuf, int batch, int* bad, void* stream) {
+                  uint8_t* gbuf, int batch, int* bad, void* stream, uint8_t* xbuf) {
     pack_padded_kernel<<<chunk_grid(G, batch), TPB, 0, (cudaStream_t)stream>>>(
-        G, src, src_pitch, src_chain, gbuf, G.gpitch, G.gchain, GHALO, bad);
+        G, src, src_pitch, src_chain, gbuf, G.gpitch, G.gchain, GHALO, bad, xbuf, G.xpitch,
+        G.xchain, HALO);
     return (int)cudaGetLastError();
 }
 

@@ -194,8 +194,9 @@ int launch_param_table(const ParamTable& t, int n, uint32_t* dst, void* stream);
 int launch_sweep_binary2(const Binary2SweepParams& p, int batch, int rows_per_thread, void* stream);
 int launch_pack_state(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad_flag, void* stream);
+// xbuf non-null: the same pass also writes the state buffer (x0 = g, one read of the input)
 int launch_pack_g(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
-                  uint8_t* gbuf, int batch, int* bad_flag, void* stream);
+                  uint8_t* gbuf, int batch, int* bad_flag, void* stream, uint8_t* xbuf = nullptr);
 int launch_unpack_state(const Geometry& geo, const uint8_t* xbuf, uint8_t* dense, int batch,
                         void* stream);
 int launch_check_levels(const uint8_t* dense, size_t n, int levels, int* bad_flag,

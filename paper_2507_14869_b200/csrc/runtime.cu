@@ -782,6 +782,10 @@ pca_status load_state(pca_ctx* ctx, const uint8_t* src, int pitch, long long cha
 pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool staged = false) {
     const pca_config& c = ctx->cfg;
     const Layout& L = ctx->lay;
+    // x0 = g on an initialised context: the g pass also writes x[0], the state the reset
+    // starts from, so the input is read once (a failed level check leaves x[0] overwritten,
+    // like g: the context needs a valid reset either way)
+    const bool fused_x = g && !x0 && ctx->x_initialized;
     if (g) {
         const uint8_t* dg = nullptr;
         pca_status st = device_input(ctx, g, &dg);
@@ -789,7 +793,7 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool stag
         CK(ctx, cudaMemsetAsync(ctx->g, 0, L.gbuf, ctx->stream));
         CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
         LAUNCH(ctx, launch_pack_g(ctx->geo, dg, c.width, (long long)L.rows * c.width, ctx->g,
-                                  c.batch, ctx->flag, ctx->stream));
+                                  c.batch, ctx->flag, ctx->stream, fused_x ? ctx->x[0] : nullptr));
         // the check's host synchronisation also ends the caller's buffer lifetime at return;
         // it is skipped only for the context's own staged copy holding bit-unpacked labels
         // (packed_io, levels == 2: 0/1 by construction)
@@ -819,6 +823,10 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool stag
         pca_status st = device_input(ctx, x0, &dx);
         if (st != PCA_OK) return st;
         return load_state(ctx, dx, c.width, (long long)L.rows * c.width, "x0");
+    }
+    if (fused_x) {  // x[0] was written by the g pass: only the halo exchange is left
+        if (ctx->p2p) return p2p_push(ctx, ctx->cur);
+        return exchange(ctx, ctx->x[ctx->cur]);
     }
     // x0 = g: g's labels were checked when it was loaded
     return load_state(ctx, ctx->g + (size_t)GHALO * L.gpitch + XOFF, L.gpitch, ctx->geo.gchain, "g",
