@@ -414,6 +414,51 @@ def test_coloured_sweep_law_is_the_product_of_site_kernels(lat, g):
     assert np.abs(gs @ K - gs).max() < 1e-15  # the coloured sweep leaves pi_GS invariant
 
 
+def _site_kernel_product(lat, g, a, b, order):
+    K = np.eye(lat.levels ** lat.n)
+    for i in order:
+        K = K @ en.gibbs_site_kernel(lat, g.reshape(-1), a, b, i)
+    return K
+
+
+@pytest.mark.parametrize("lat,g", [(en.Lattice(2, 3, 2, nbhd=8), np.array([[0, 1, 1], [1, 0, 1]])),
+                                   (en.Lattice(3, 2, 2, nbhd=8), np.array([[0, 1], [1, 1], [0, 0]])),
+                                   (en.Lattice(2, 2, 3, nbhd=8), np.array([[0, 2], [1, 2]]))])
+def test_column_major_sweep_law_is_the_product_of_site_kernels(lat, g):
+    """The paper's systematic scan (section 5.1: pixels visited column by
+    column, R13): the C sweep's one-step law from a fixed x equals the row of
+    K_{i1} ... K_{in} with the sites in COLUMN-MAJOR order (c outer, r inner), built from the
+    enumeration's single-site Gibbs kernels (independent code).  The same frequencies must
+    reject the row-major product, so a scan in the wrong order fails this pin.  Moore-8 only:
+    on the 4-neighbour grid both scans orient every edge from (r, c) towards larger r or c,
+    so they are linear extensions of the same order and have the SAME law (checked below);
+    the anti-diagonal Moore edges (r, c+1)-(r+1, c) are oriented oppositely by the two."""
+    m = orc.model(lat.H, lat.W, lat.levels, nbhd=lat.nbhd, periodic=False, J=1 / 3, q=0.0,
+                  sigma=0.5)
+    g = g.astype(np.uint8)
+    beta = 1.25
+    a, b, _ = en.coefficients(beta, 1 / 3, 0.0, 0.5)
+    col_major = sorted(range(lat.n), key=lambda i: (i % lat.W, i // lat.W))
+    row_major = list(range(lat.n))
+    x = (np.arange(lat.n).reshape(lat.H, lat.W) % 2).astype(np.uint8)
+    k_col = _site_kernel_product(lat, g, a, b, col_major)[en.state_index(lat, x.reshape(-1))]
+    k_row = _site_kernel_product(lat, g, a, b, row_major)[en.state_index(lat, x.reshape(-1))]
+    assert 0.5 * np.abs(k_col - k_row).sum() > 0.02  # the two scan orders have different laws
+    lat4 = en.Lattice(lat.H, lat.W, lat.levels, nbhd=4)
+    k4 = [_site_kernel_product(lat4, g, a, b, o)[en.state_index(lat4, x.reshape(-1))]
+          for o in (col_major, row_major)]
+    assert np.abs(k4[0] - k4[1]).max() < 1e-15  # 4-neighbour: indistinguishable orders
+    n = 30000
+    counts = np.zeros(len(k_col))
+    for k in range(n):
+        w = orc.gibbs_sweep(m, x, g, beta, seed=6, chain=k, t=4)
+        counts[en.state_index(lat, w.reshape(-1))] += 1
+    ok, stat, crit = _chi2_ok(counts, k_col, n)
+    assert ok, (stat, crit)
+    bad, stat_row, _ = _chi2_ok(counts, k_row, n)
+    assert not bad, stat_row
+
+
 def test_coloured_gibbs_run_counts():
     """orc_gibbs_run(order = colour) == repeated coloured sweeps, with counts of x after
     every sweep t >= burn_in."""
