@@ -228,6 +228,19 @@ class PcaContext:
                                   _ptr(g), _ptr(x0), self.stream.cuda_stream), "pca_init")
         self.handle = h
         self._keep = None
+        # host buffers a copy-stream transfer may still read or write: staged
+        # inputs (pca_stage_input) and asynchronous MPM images (pca_finalize_async).  They are
+        # released only once a call has provably waited for the copy on the host, never at the
+        # return of the call that enqueued or consumed it.
+        self._staged_inputs = []   # [buffer, consumed by a reset_staged?]
+        self._async_outputs = []
+
+    def _synced_main(self):
+        """The library host-synchronised the main stream after waiting on the copy events:
+        inputs already consumed by a staged reset, and earlier asynchronous images (every
+        synchronising call waits for the previous image copy first), are complete."""
+        self._staged_inputs = [e for e in self._staged_inputs if not e[1]]
+        self._async_outputs = []
 
     # ---- ABI wrappers (same names) ----
     def pca_reset(self, g=None, x0=None):
@@ -235,12 +248,13 @@ class PcaContext:
 
     def pca_stage_input(self, g):
         """Copy the next reset's g on the internal copy stream (overlaps the work after it)."""
-        self._staged_input = g  # keep the host buffer alive until pca_reset_staged
+        self._staged_inputs.append([g, False])  # alive until a host sync covers the copy
         _check(lib().pca_stage_input(self.handle, _ptr(g)), "pca_stage_input")
 
     def pca_reset_staged(self):
         _check(lib().pca_reset_staged(self.handle), "pca_reset_staged")
-        self._staged_input = None
+        for e in self._staged_inputs:  # the main stream now waits for these copies
+            e[1] = True
 
     def pca_sweep(self, n: int):
         _check(lib().pca_sweep(self.handle, int(n)), "pca_sweep")
@@ -250,6 +264,7 @@ class PcaContext:
 
     def pca_estimate(self, kind: int, out):
         _check(lib().pca_estimate(self.handle, int(kind), _ptr(out)), "pca_estimate")
+        self._synced_main()
         return out
 
     def pca_metric_sums(self, truth, kind: int) -> np.ndarray:
@@ -263,6 +278,7 @@ class PcaContext:
         s = np.zeros(self.cfg.batch, np.float64)
         _check(lib().pca_psnr_ssim(self.handle, _ptr(truth), int(kind), p.ctypes.data,
                                    s.ctypes.data), "pca_psnr_ssim")
+        self._synced_main()
         return p, s
 
     def pca_stage_truth(self, truth):
@@ -279,17 +295,21 @@ class PcaContext:
         s = np.zeros((self.cfg.batch, 2), np.float64)
         _check(lib().pca_finalize(self.handle, _ptr(truth), _ptr(mpm_out), p.ctypes.data,
                                   s.ctypes.data), "pca_finalize")
+        self._synced_main()
         return p, s
 
     def pca_finalize_async(self, truth, mpm_out):
         """pca_finalize with the MPM image's copy into host mpm_out on the copy stream: the
         image may still be in flight at return (pca_sync waits for it); keep mpm_out alive
         and unread until then."""
-        self._async_out = mpm_out  # keep the buffer alive until the copy has run
         p = np.zeros((self.cfg.batch, 2), np.float64)
         s = np.zeros((self.cfg.batch, 2), np.float64)
+        # the previous image stays referenced until this call has waited for its copy
+        self._async_outputs.append(mpm_out)
         _check(lib().pca_finalize_async(self.handle, _ptr(truth), _ptr(mpm_out), p.ctypes.data,
                                         s.ctypes.data), "pca_finalize_async")
+        self._synced_main()
+        self._async_outputs = [mpm_out]  # in flight until the next synchronising call
         return p, s
 
     def pca_ssim_windowed(self, truth, kind: int):
@@ -362,11 +382,15 @@ class PcaContext:
 
     def pca_sync(self):
         _check(lib().pca_sync(self.handle), "pca_sync")
+        self._staged_inputs = []
+        self._async_outputs = []
 
     def pca_destroy(self):
         if getattr(self, "handle", None):
-            lib().pca_destroy(self.handle)
+            lib().pca_destroy(self.handle)  # waits for every stream, copies included
             self.handle = None
+            self._staged_inputs = []
+            self._async_outputs = []
 
     # ---- conveniences (host NumPy results) ----
     def state(self) -> np.ndarray:

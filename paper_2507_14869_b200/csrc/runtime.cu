@@ -58,11 +58,11 @@ struct NcclApi {
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
-NcclApi& nccl() {
-    static NcclApi api;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+// loaded once, thread-safely (a function-local static's initialiser runs exactly once, and
+// concurrent first callers wait for it: one host thread per GPU may attach at the same time)
+NcclApi load_nccl() {
+    NcclApi api;
+    {
         void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
@@ -88,6 +88,11 @@ NcclApi& nccl() {
 #undef LOAD
         api.loaded = true;
     }
+    return api;
+}
+
+NcclApi& nccl() {
+    static NcclApi api = load_nccl();
     return api;
 }
 
@@ -248,6 +253,10 @@ struct pca_ctx {
     int rows_per_thread = 8;
     int poisoned = 0;
     int x_initialized = 0;
+    // g / the state passed their level checks: a failed reset or state load leaves labels >=
+    // levels in the buffers (the fused reset writes x[0] before the check), which would index
+    // the tables out of range, so every call that reads them refuses until a good load
+    int g_ok = 0, x_ok = 0;
     int prev_valid = 0;  // x[cur ^ 1] holds x_{t-1} (after a PCA or double-buffered Gibbs sweep)
     int64_t tab_stage = -1;
     int64_t gtab_stage = -1;
@@ -326,6 +335,16 @@ pca_status usable(pca_ctx* ctx) {
         return fail(PCA_ESTATE, "context poisoned by an earlier CUDA/NCCL error; destroy it");
     cudaError_t e = cudaSetDevice(ctx->device);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+    return PCA_OK;
+}
+
+// usable, and the observed image and the state hold valid labels (calls that read them)
+pca_status ready(pca_ctx* ctx) {
+    pca_status st = usable(ctx);
+    if (st != PCA_OK) return st;
+    if (!ctx->g_ok || !ctx->x_ok)
+        return fail(PCA_ESTATE, "the last reset or state load failed its level check: "
+                                "reset with a valid g (and x0) first");
     return PCA_OK;
 }
 
@@ -768,6 +787,7 @@ pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
 pca_status load_state(pca_ctx* ctx, const uint8_t* src, int pitch, long long chain_stride,
                       const char* what, bool checked = false) {
     ctx->prev_valid = 0;
+    ctx->x_ok = 0;
     CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
     LAUNCH(ctx, launch_pack_state(ctx->geo, src, pitch, chain_stride, ctx->x[ctx->cur],
                                   ctx->cfg.batch, ctx->flag, ctx->stream));
@@ -775,6 +795,7 @@ pca_status load_state(pca_ctx* ctx, const uint8_t* src, int pitch, long long cha
         pca_status st = check_flag(ctx, what);
         if (st != PCA_OK) return st;
     }
+    ctx->x_ok = 1;
     if (ctx->p2p) return p2p_push(ctx, ctx->cur);
     return exchange(ctx, ctx->x[ctx->cur]);
 }
@@ -786,7 +807,9 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool stag
     // starts from, so the input is read once (a failed level check leaves x[0] overwritten,
     // like g: the context needs a valid reset either way)
     const bool fused_x = g && !x0 && ctx->x_initialized;
+    if (fused_x) ctx->x_ok = 0;  // the g pass writes x[0] before its check
     if (g) {
+        ctx->g_ok = 0;
         const uint8_t* dg = nullptr;
         pca_status st = device_input(ctx, g, &dg);
         if (st != PCA_OK) return st;
@@ -801,6 +824,7 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool stag
             st = check_flag(ctx, "g");
             if (st != PCA_OK) return st;
         }
+        ctx->g_ok = 1;
     }
     // free boundary: halos and padding hold the sentinel 0xFF; torus: halos are rewritten by
     // every sweep and padding is 0 (a valid label, so SWAR sums need no masking)
@@ -825,6 +849,7 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool stag
         return load_state(ctx, dx, c.width, (long long)L.rows * c.width, "x0");
     }
     if (fused_x) {  // x[0] was written by the g pass: only the halo exchange is left
+        ctx->x_ok = 1;
         if (ctx->p2p) return p2p_push(ctx, ctx->cur);
         return exchange(ctx, ctx->x[ctx->cur]);
     }
@@ -958,7 +983,7 @@ pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
 
 pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     DeviceScope device_scope_;
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
     const bool strip = ctx->lay.rows < ctx->cfg.height;
@@ -1108,7 +1133,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
 
 pca_status pca_gibbs_sweep(pca_ctx* ctx, int32_t n) {
     DeviceScope device_scope_;
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
     const pca_config& c = ctx->cfg;
@@ -1232,7 +1257,7 @@ static pca_status wait_out_free(pca_ctx* ctx) {
 
 pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
     DeviceScope device_scope_;
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
     if (kind < PCA_EST_LAST || kind > PCA_EST_CM) return fail(PCA_EINVAL, "unknown estimate kind");
@@ -1279,7 +1304,7 @@ pca_status pca_estimate(pca_ctx* ctx, int32_t kind, void* out) {
 
 pca_status pca_metric_sums(pca_ctx* ctx, const uint8_t* truth, int32_t kind, int64_t* sums) {
     DeviceScope device_scope_;
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (!truth || !sums) return fail(PCA_EINVAL, "truth and sums must be non-NULL");
     if (kind != PCA_EST_LAST && kind != PCA_EST_MPM)
@@ -1434,7 +1459,7 @@ pca_status pca_stage_truth(pca_ctx* ctx, const uint8_t* truth) {
 
 static pca_status finalize(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_out, double* psnr,
                            double* ssim, bool async_image) {
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (!psnr || !ssim) return fail(PCA_EINVAL, "psnr and ssim must be non-NULL");
     if (!truth && !ctx->truth_staged)
@@ -1541,7 +1566,7 @@ pca_status pca_finalize_async(pca_ctx* ctx, const uint8_t* truth, uint8_t* mpm_o
 
 pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, double* ssim) {
     DeviceScope device_scope_;
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (!truth || !ssim) return fail(PCA_EINVAL, "truth and ssim must be non-NULL");
     if (kind != PCA_EST_LAST && kind != PCA_EST_MPM)
@@ -1598,7 +1623,7 @@ pca_status pca_ssim_windowed(pca_ctx* ctx, const uint8_t* truth, int32_t kind, d
 
 pca_status pca_changed_sites(pca_ctx* ctx, int64_t* changed) {
     DeviceScope device_scope_;
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (!changed) return fail(PCA_EINVAL, "changed is NULL");
     if (!ctx->prev_valid)
@@ -1630,7 +1655,7 @@ pca_status pca_write_state(pca_ctx* ctx, const uint8_t* x) {
 
 pca_status pca_read_counts(pca_ctx* ctx, uint16_t* out) {
     DeviceScope device_scope_;
-    pca_status st = usable(ctx);
+    pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (!out) return fail(PCA_EINVAL, "out is NULL");
     const pca_config& c = ctx->cfg;

@@ -28,3 +28,29 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.fail("-m gpu test run without a CUDA device")
     return torch.device("cuda:0")
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Parity report: per test, the site updates compared with the oracle in lockstep, the
+    near-tie mismatches and the largest oracle margin of a mismatch (north star / R19)."""
+    import json
+
+    helpers = sys.modules.get("parity_helpers") or sys.modules.get("tests.parity_helpers")
+    if helpers is None or not helpers.REGISTRY:
+        return
+    rep = {}
+    for t in helpers.REGISTRY:
+        e = rep.setdefault(t.name, {"updates": 0, "mismatches": 0, "max_margin": 0.0})
+        e["updates"] += t.updates
+        e["mismatches"] += t.mismatches
+        e["max_margin"] = max(e["max_margin"], t.max_margin)
+    tot_u = sum(e["updates"] for e in rep.values())
+    tot_m = sum(e["mismatches"] for e in rep.values())
+    out = {"tolerance": {"margin": 1e-6, "rate": 1e-6},
+           "total": {"updates": tot_u, "mismatches": tot_m,
+                     "rate": tot_m / tot_u if tot_u else 0.0,
+                     "max_margin": max(e["max_margin"] for e in rep.values())},
+           "tests": rep}
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "parity_report.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)

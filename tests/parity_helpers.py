@@ -2,6 +2,8 @@
 the oracle on the same seeded inputs, and classify every disagreement (R19)."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 import oracle as orc
@@ -21,11 +23,18 @@ def beta_of(cfg: P.pca_config, t: int) -> float:
     return orc.beta_at(cfg.beta0, cfg.beta_step, cfg.beta_period, t)
 
 
+# every Tally of the session, written to gpurun_out/parity_report.json by conftest.py
+REGISTRY: list = []
+
+
 class Tally:
-    def __init__(self):
+    def __init__(self, name: str = None):
         self.updates = 0
         self.mismatches = 0
         self.max_margin = 0.0
+        self.name = name or os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
+        self.counts = None  # lockstep(count_from=...): oracle-side MPM counts of the GPU states
+        REGISTRY.append(self)
 
     def add(self, gpu_next, ora_next, margins):
         bad = gpu_next != ora_next
@@ -44,19 +53,28 @@ class Tally:
             f"{self.mismatches} near-tie mismatches in {self.updates} updates (> 1e-6)")
 
 
-def lockstep(ctx: P.PcaContext, cfg: P.pca_config, n: int, t0: int = 0, tally: Tally = None):
+def lockstep(ctx: P.PcaContext, cfg: P.pca_config, n: int, t0: int = 0, tally: Tally = None,
+             count_from: int = None):
     """n sweeps in lockstep: at every sweep the oracle recomputes one sweep from the GPU's
-    own x_t (state injection) and every site of the GPU's x_{t+1} is compared."""
+    own x_t (state injection) and every site of the GPU's x_{t+1} is compared.
+    count_from = the MPM burn-in: tally.counts[b][k] = #{t >= count_from: GPU x_{t+1} == k},
+    the oracle's count rule (R15) applied to the lockstep states, so MPM and the metrics stay
+    comparable when a near-tie mismatch makes the free-running chains part."""
     tally = tally or Tally()
     m = oracle_model(cfg)
     g = ctx._g_host
     x = ctx.state()
+    if count_from is not None and tally.counts is None:
+        tally.counts = np.zeros((cfg.batch, cfg.levels) + x.shape[1:], np.int64)
     for t in range(t0, t0 + n):
         ctx.pca_sweep(1)
         xn = ctx.state()
         for b in range(cfg.batch):
             ref, mg = orc.pca_sweep(m, x[b], g[b], beta_of(cfg, t), cfg.seed, cfg.chain0 + b, t)
             tally.add(xn[b], ref, mg)
+            if count_from is not None and t >= count_from:
+                for k in range(cfg.levels):
+                    tally.counts[b, k] += xn[b] == k
         x = xn
     return tally
 

@@ -155,21 +155,40 @@ def test_config2_paper_protocol_lockstep(cuda_device, levels, sigma, ramp, n):
     cfg = P.make_config(256, 256, levels, neighborhood=8, periodic=False, sigma=sigma,
                         seed=2025 + levels, mpm_burn_in=burn)
     ctx = make_ctx(cfg, g)
-    tally = lockstep(ctx, cfg, n)
+    tally = lockstep(ctx, cfg, n, count_from=burn)
     tally.check()
+    # Estimates are compared in every case, never skipped: against the oracle's count rule
+    # and metrics applied to the lockstep states (the GPU chain, each sweep of which the
+    # oracle confirmed up to allowed near-ties), and -- when no near-tie occurred -- also
+    # against the free-running oracle chain, which is then the same chain.
+    x_g = ctx.state()[0]
+    cnt_l = tally.counts[0]
+    assert np.array_equal(ctx.counts()[0], cnt_l.astype(np.uint16))
     x_o, cnt_o = orc.pca_run(oracle_model(cfg), g, g, n, 1.25, 0.25, 250, cfg.seed, burn_in=burn)
+    refs = [(x_g, cnt_l)]
     if tally.mismatches == 0:
-        assert np.array_equal(ctx.state()[0], x_o)
-        assert np.array_equal(ctx.counts()[0], cnt_o.astype(np.uint16))
-        for kind, est in [(P.EST_LAST, x_o), (P.EST_MPM, orc.mpm(cnt_o))]:
+        assert np.array_equal(x_g, x_o)
+        assert np.array_equal(cnt_l, cnt_o)
+        refs.append((x_o, cnt_o))
+    for last, cnt in refs:
+        for kind, est in [(P.EST_LAST, last), (P.EST_MPM, orc.mpm(cnt))]:
             psnr, ssim = ctx.pca_psnr_ssim(truth[None], kind)
             _, p_o, s_o, _ = orc.metrics(truth, est, levels)
             assert abs(psnr[0] - p_o) < 1e-9 and abs(ssim[0] - s_o) < 1e-9
             sw = ctx.pca_ssim_windowed(truth[None], kind)
             assert abs(sw[0] - orc.ssim_windowed(truth, est, levels)) < 1e-12
+        assert np.array_equal(ctx.estimate(P.EST_MPM)[0], orc.mpm(cnt))
         cm = ctx.estimate(P.EST_CM)[0]
-        ref = (np.arange(levels)[:, None, None] / (levels - 1) * cnt_o).sum(0) / (n - burn)
+        ref = (np.arange(levels)[:, None, None] / (levels - 1) * cnt).sum(0) / (n - burn)
         assert np.allclose(cm, ref, atol=1e-6)
+    # the north star's end-to-end tolerances against the FREE-RUNNING oracle chain hold in
+    # every case: MPM marginals within 1e-3, PSNR within 0.01 dB
+    marg = ctx.estimate(P.EST_MARGINALS)[0]
+    if tally.mismatches == 0:
+        assert np.abs(marg - cnt_o / (n - burn)).max() < 1e-3
+    for kind, est in [(P.EST_LAST, x_o), (P.EST_MPM, orc.mpm(cnt_o))]:
+        psnr, _ = ctx.pca_psnr_ssim(truth[None], kind)
+        assert abs(psnr[0] - orc.metrics(truth, est, levels)[1]) < 0.01
 
 
 @pytest.mark.parametrize("H,W,L", [(7, 7, 2), (8, 300, 5), (130, 9, 9), (71, 133, 255), (64, 64, 33)])
@@ -278,6 +297,10 @@ def test_row_strips_with_loopback_halo_exchange(cuda_device, periodic, levels):
     assert np.array_equal(got, full.state()[0])
     gc = np.concatenate([s.counts()[0] for s in strips], axis=-2)
     assert np.array_equal(gc, full.counts()[0])
+    # and against the oracle's unsharded chain (not only the GPU's own)
+    x_o, cnt_o = orc.pca_run(oracle_model(full.cfg), g, g, 10, 1.25, 0.25, 250, 99, burn_in=4)
+    assert np.array_equal(got, x_o)
+    assert np.array_equal(gc, (cnt_o[1] if levels == 2 else cnt_o).astype(np.uint16))
     truth = synth.smooth_labels(H, W, levels, 5)
     tot = sum(s.pca_metric_sums(truth[bounds[i]:bounds[i + 1]][None], P.EST_LAST)
               for i, s in enumerate(strips))
@@ -336,6 +359,24 @@ def test_error_paths(cuda_device):
     with pytest.raises(P.PcaError) as e:
         ctx.pca_write_state(bad)
     assert e.value.status == P.PCA_EINVAL
+    # a failed load leaves labels >= levels in the buffer: calls that read the state refuse
+    # until a valid load, and a valid one makes the context usable again
+    for call in (lambda: ctx.pca_sweep(1), ctx.state, lambda: ctx.pca_gibbs_sweep(1)):
+        with pytest.raises(P.PcaError) as e:
+            call()
+        assert e.value.status == P.PCA_ESTATE
+    ctx.pca_write_state(g)
+    # the same for a failed reset with a new g on a context that has swept (the fused reset
+    # writes x[0] in the pass that checks g)
+    ctx.pca_sweep(2)
+    with pytest.raises(P.PcaError) as e:
+        ctx.pca_reset(bad, None)
+    assert e.value.status == P.PCA_EINVAL
+    with pytest.raises(P.PcaError) as e:
+        ctx.pca_sweep(1)
+    assert e.value.status == P.PCA_ESTATE
+    ctx.pca_reset(g, None)
+    assert np.array_equal(ctx.state()[0], g)
     black = np.zeros((1, H, W), np.uint8)
     with pytest.raises(P.PcaError):
         ctx.pca_psnr_ssim(black, P.EST_LAST)
@@ -404,28 +445,32 @@ def test_distribution_matches_exact_transition_powers(cuda_device):
                          ids=["c3", "c4-strip-shape", "c3-free", "c3-vn4"])
 def test_full_size_sampled_rows(cuda_device, H, W, nb, per):
     """Bench-size lattices (config 3, 8192^2, and config 4's per-GPU 4096 x 32768 shape, l = 2,
-    MPM on): rows sampled across the lattice (edges, middle, random) are recomputed by the
-    oracle from the GPU's x_t for the last sweep; the MPM counts must equal the sum of the
-    four states exactly at every site."""
+    MPM on, one launch per sweep as in the bench): for EVERY one of four sweeps, rows sampled
+    across the lattice (edges, middle, random) are recomputed by the oracle from the GPU's
+    x_t; for config 3 the oracle recomputes the whole last sweep (67 M sites, ~5 s).  The MPM
+    counts equal the sum of the four oracle-confirmed states at every site."""
     truth = synth.tiled_labels(H, W, 2, seed=1)
     g = synth.degrade(truth, 2, 0.5, seed=2)
     cfg = P.make_config(H, W, 2, neighborhood=nb, periodic=per, sigma=0.5, beta0=1.5,
                         beta_step=0.0, seed=11, mpm_burn_in=0)
     ctx = make_ctx(cfg, g)
-    acc = np.zeros((H, W), np.uint16)
-    for _ in range(3):
-        ctx.pca_sweep(1)
-        acc += ctx.state()[0]
-    x3 = ctx.state()[0]
-    ctx.pca_sweep(1)
-    x4 = ctx.state()[0]
-    acc += x4
     m = oracle_model(cfg)
-    rows = sorted({0, 1, H - 1, H // 2} | set(np.random.default_rng(0).integers(0, H, 16).tolist()))
+    acc = np.zeros((H, W), np.uint16)
     tally = Tally()
-    for r in rows:
-        ref, mg = orc.pca_sweep(m, x3, g, 1.5, cfg.seed, 0, 3, rows=(r, r + 1))
-        tally.add(x4[r], ref[0], mg[0])
+    x = g
+    rng = np.random.default_rng(0)
+    for t in range(4):
+        ctx.pca_sweep(1)
+        xn = ctx.state()[0]
+        rows = sorted({0, 1, H - 2, H - 1, H // 2} | set(rng.integers(0, H, 40).tolist()))
+        for r in rows:
+            ref, mg = orc.pca_sweep(m, x, g, 1.5, cfg.seed, 0, t, rows=(r, r + 1))
+            tally.add(xn[r], ref[0], mg[0])
+        acc += xn
+        if t == 3 and H == W == 8192 and nb == 8 and per:
+            ref, mg = orc.pca_sweep(m, x, g, 1.5, cfg.seed, 0, t)
+            tally.add(xn, ref, mg)
+        x = xn
     tally.check()
     assert np.array_equal(ctx.counts()[0], acc)
 
@@ -739,6 +784,63 @@ def test_staged_input_reset_equals_direct_reset(cuda_device, packed):
         a.pca_sweep(6)
         b.pca_sweep(6)
         assert np.array_equal(a.state(), b.state()) and np.array_equal(a.counts(), b.counts())
+
+
+@pytest.mark.parametrize("packed", [0, 1])
+def test_staged_temporary_pinned_input_survives_host_reuse(cuda_device, packed):
+    """A temporary pinned tensor handed to pca_stage_input and dropped by the caller right
+    away stays referenced by the binding until a host synchronisation covers its copy
+    (ADVICE r1): new pinned tensors allocated and overwritten before pca_sync cannot reuse
+    its block under the in-flight copy, so the chain starts from the staged g."""
+    import torch
+
+    H, W = 64, 400
+    g1 = synth.degrade(synth.smooth_labels(H, W, 2, 3), 2, 0.4, 4)[None]
+    g2 = synth.degrade(synth.smooth_labels(H, W, 2, 7), 2, 0.4, 8)[None]
+    enc = (lambda a: P.pack_bits(a)) if packed else (lambda a: a)
+    kw = dict(sigma=0.4, seed=5, mpm_burn_in=2, packed_io=packed)
+    a = P.PcaContext(P.make_config(H, W, 2, **kw), np.ascontiguousarray(enc(g2)))
+    b = P.PcaContext(P.make_config(H, W, 2, **kw), np.ascontiguousarray(enc(g1)))
+    b.pca_sweep(20)
+    tmp = torch.from_numpy(np.ascontiguousarray(enc(g2))).pin_memory()
+    b.pca_stage_input(tmp)
+    del tmp
+    b.pca_reset_staged()
+    junk = [torch.full(enc(g2).shape, 1 if packed else 0xAB, dtype=torch.uint8).pin_memory()
+            for _ in range(8)]
+    for j in junk:
+        j.fill_(0xFF)
+    b.pca_sweep(5)
+    b.pca_sync()
+    a.pca_sweep(5)
+    assert np.array_equal(a.state(), b.state()) and np.array_equal(a.counts(), b.counts())
+
+
+@pytest.mark.parametrize("packed", [0, 1])
+def test_reset_with_new_g_equals_a_fresh_context(cuda_device, packed):
+    """the fused reset (pca_reset(g_new, NULL) on a context that has swept) equals
+    a fresh PcaContext(cfg, g_new): torus and free boundary, W in {64, 77}, 2 and 5 levels."""
+    for periodic in (True, False):
+        for W in (64, 77):
+            for L in ((2,) if packed else (2, 5)):
+                H = 40
+                g1 = synth.degrade(synth.smooth_labels(H, W, L, 3), L, 0.3, 4)[None]
+                g2 = synth.degrade(synth.smooth_labels(H, W, L, 5), L, 0.3, 6)[None]
+                enc = (lambda a: P.pack_bits(a)) if packed else (lambda a: a)
+                cfg = P.make_config(H, W, L, periodic=periodic, sigma=0.3, seed=9, mpm_burn_in=1,
+                                    packed_io=packed)
+                old = P.PcaContext(cfg, np.ascontiguousarray(enc(g1)))
+                old.pca_sweep(7)
+                old.pca_reset(np.ascontiguousarray(enc(g2)), None)
+                new = P.PcaContext(cfg, np.ascontiguousarray(enc(g2)))
+                for c in (old, new):
+                    c.pca_sweep(6)
+                assert np.array_equal(old.state(), new.state())
+                assert np.array_equal(old.counts(), new.counts())
+                truth = np.ascontiguousarray(enc(synth.smooth_labels(H, W, L, 5)[None]))
+                assert np.array_equal(old.pca_finalize(truth), new.pca_finalize(truth))
+                old.pca_destroy()
+                new.pca_destroy()
 
 
 @pytest.mark.parametrize("packed", [0, 1])

@@ -9,9 +9,10 @@ cross-process mapping (CUDA IPC) is checked separately without any waiting."""
 import numpy as np
 import pytest
 
+import oracle as orc
 import paper_2507_14869_b200 as P
 import synth
-from parity_helpers import make_ctx
+from parity_helpers import make_ctx, oracle_model
 
 pytestmark = pytest.mark.gpu
 
@@ -61,6 +62,12 @@ def test_device_initiated_halos_reproduce_unsharded_chain(cuda_device, periodic,
     assert np.array_equal(got, full.state())
     gc = np.concatenate([s.counts() for s in strips], axis=-2)
     assert np.array_equal(gc, full.counts())
+    # and against the oracle's unsharded chains (chain id b per batch entry)
+    for b in range(batch):
+        x_o, cnt_o = orc.pca_run(oracle_model(full.cfg), g[b], g[b], 12, 1.25, 0.25, 5, 99, chain=b,
+                                 burn_in=4)
+        assert np.array_equal(got[b], x_o)
+        assert np.array_equal(gc[b], (cnt_o[1] if levels == 2 else cnt_o).astype(np.uint16))
     # a state load (reset from a new x0) is a phase too: its edge rows are pushed
     x0 = np.stack([synth.random_labels((H, W), levels, 40 + b) for b in range(batch)])
     for i, s in enumerate(strips):
@@ -186,5 +193,18 @@ def test_gibbs_strips_over_peers_reproduce_unsharded_chain(cuda_device, periodic
     assert np.array_equal(got, full.state())
     gc = np.concatenate([s.counts() for s in strips], axis=-2)
     assert np.array_equal(gc, full.counts())
+    # and against the oracle's sequence (colour-order Gibbs, R21, and PCA sweeps)
+    m = oracle_model(full.cfg)
+    x = g[0].copy()
+    cnt = np.zeros((levels, H, W), np.int64)
+    for t in range(8):
+        beta = orc.beta_at(1.25, 0.25, 4, t)
+        x = orc.gibbs_sweep_coloured(m, x, g[0], beta, 17, 0, t) if t % 3 else \
+            orc.pca_sweep(m, x, g[0], beta, 17, 0, t)[0]
+        if t >= 3:
+            for k in range(levels):
+                cnt[k] += x == k
+    assert np.array_equal(got[0], x)
+    assert np.array_equal(gc[0], (cnt[1] if levels == 2 else cnt).astype(np.uint16))
     for s in strips:
         s.pca_destroy()
