@@ -48,11 +48,38 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the multi-level variants (C5 per GPU, C3 at l = 5) of the N = 1 line")
     ap.add_argument("--rows-per-thread", type=int, default=0)
     ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1: halo rows by NCCL send/recv (default) or stored by the sweep "
                          "kernel straight into the neighbours' memory (pca_attach_peers, CUDA IPC)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only (gloo, stub context): exercise the multi-rank orchestration "
+                         "(self-launch, strip partition, unique-id broadcast, max-over-ranks "
+                         "timing, rank-0 line) without a GPU; the line is marked dry_run")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` outside torchrun (WORLD_SIZE unset) with N > 1: re-launch this
+    script as N ranks (one process per GPU) with torch.distributed.run on 127.0.0.1, exactly as
+    the driver's torchrun launch would, and pass rank 0's JSON line through.  None when this
+    process already is a rank (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
 
 
 def workload(n_gpus: int):
@@ -131,10 +158,14 @@ class ClockSampler:
 
 
 def load_traffic():
-    """dram bytes per sweep launch from the committed ncu --set full summary, if any."""
+    """DRAM bytes per sweep launch of the 8192^2 headline kernel from the committed ncu
+    summary: preferably a multi-launch capture without cache control (the steady state: each
+    launch's dirty lines are written back during the next, so writes are counted), else the
+    --set full capture."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary*.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary*.json"))) + \
+        sorted(glob.glob(os.path.join(ROOT, "profiles", "*dram_multilaunch*.json")))
     for f in reversed(files):
         try:
             d = json.load(open(f))
@@ -143,6 +174,89 @@ def load_traffic():
         except Exception:
             pass
     return None, None
+
+
+# Issue peak for ALU-bound kernels: 4 SM sub-partitions per SM, each issuing
+# at most one warp instruction per clock (B300_MICROARCH.md "Per-warp issue scheduler"), i.e.
+# 148 SMs x 4 x 32 thread-instructions per clock at the max SM clock of MEASURED_PEAKS.json.
+def issue_peak():
+    try:
+        mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    return 148 * 4 * 32 * mhz * 1e6
+
+
+def load_instr_per_su(tag):
+    """thread-instructions per site-update of a variant's sweep kernel from its committed ncu
+    summary (profiles/*<tag>*summary*.json: smsp__inst_executed.sum x 32 / sites)."""
+    import glob
+
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*{tag}*summary*.json")), reverse=True):
+        try:
+            d = json.load(open(f))
+            return float(d["thread_instr_per_su"]), os.path.relpath(f, ROOT)
+        except Exception:
+            pass
+    return None, None
+
+
+def run_variants(P, torch, dev, stream):
+    """The paper's multi-level workloads on one GPU: C5 per GPU (one 512^2 truth,
+    l = 5, sigma = 0.25, x 128 noise seeds = 128 chains, Moore-8, free boundary, the paper's
+    protocol: 1000 sweeps, beta 1.25 + 0.25 / 250, MPM burn-in 750) and C3 at l = 5 (8192^2
+    torus, beta = 1.5, MPM every sweep, 200 sweeps from x0 = g).  Each: device time of one
+    timed run (reset + sweeps + fused finalisation) after a warm-up run, SU/s, and the ALU
+    roofline of its sweep kernel (instructions per SU from the committed ncu summary x SU/s
+    against the issue peak)."""
+    import synth
+
+    out = {}
+    peak = issue_peak()
+    cases = [
+        ("c5", "C5 per GPU: 128 chains x 512x512, l=5, sigma=0.25, Moore-8 free, paper protocol "
+               "(1000 sweeps, beta 1.25+0.25/250, MPM burn-in 750)", 512, 512, 128, 1000,
+         dict(sigma=0.25, mpm_burn_in=750)),
+        ("c3_l5", "C3 at l=5: 8192x8192 torus, sigma=0.25, beta=1.5, MPM every sweep, 200 sweeps "
+                  "from x0 = g", 8192, 8192, 1, 200,
+         dict(sigma=0.25, periodic=True, beta0=1.5, beta_step=0.0, mpm_burn_in=0)),
+    ]
+    for tag, name, H, W, B, S, kw in cases:
+        if B > 1:
+            truth1 = synth.smooth_labels(H, W, 5, seed=7)
+            truth = np.repeat(truth1[None], B, 0)
+            g = np.stack([synth.degrade(truth1, 5, 0.25, seed=100 + b) for b in range(B)])
+        else:
+            truth = synth.tiled_labels(H, W, 5, seed=1)[None]
+            g = synth.degrade(truth[0], 5, 0.25, seed=2)[None]
+        gd = torch.from_numpy(np.ascontiguousarray(g)).to(dev)
+        td = torch.from_numpy(np.ascontiguousarray(truth)).to(dev)
+        mpm = torch.empty_like(gd)
+        ctx = P.PcaContext(P.make_config(H, W, 5, batch=B, seed=11, **kw), gd, stream=stream)
+        ms = []
+        for _ in range(2):
+            ctx.pca_reset(None, None)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.pca_sweep(S)
+            psnr, ssim = ctx.pca_finalize(td, mpm)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ms.append(a.elapsed_time(b))
+        su_s = B * H * W * S / (ms[-1] * 1e-3)
+        ipsu, src = load_instr_per_su(tag)
+        roof = None
+        if ipsu:
+            roof = {"bound": "alu", "achieved": ipsu * su_s, "peak": peak, "unit": "thread-instr/s",
+                    "frac": ipsu * su_s / peak, "instr_per_su": ipsu, "instr_source": src,
+                    "peak_source": "148 SMs x 4 schedulers x 32 lanes x sm_max_mhz (1 warp-instr/clk/SMSP)"}
+        out[tag] = {"workload": name, "value": su_s, "unit": UNIT, "ms_per_run": ms[-1],
+                    "us_per_sweep": 1e3 * ms[-1] / S, "sweeps": S,
+                    "psnr_ssim_mpm_chain0": [float(psnr[0, 1]), float(ssim[0, 1])],
+                    "roofline": roof}
+        ctx.pca_destroy()
+        del gd, td, mpm
+    return out
 
 
 def measured_peak():
@@ -154,25 +268,48 @@ def measured_peak():
 
 
 # ---------------------------------------------------------------------------
+def host_cpu():
+    """The host CPU model and the number of online cores (nproc)."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
 def cpu_baseline_oracle(wl, truth, g, rows=None, sweeps=2):
     """The oracle, as it stands (single-threaded C, fp64), on a bounded sample of the
-    workload: `sweeps` sweeps of the first `rows` rows treated as their own torus."""
+    workload: `sweeps` sweeps of the first `rows` rows treated as their own torus.  The
+    process is pinned to ONE core (sched_setaffinity) for the timed call."""
     import oracle as orc
 
     rows = rows or wl["rows"]
     m = orc.model(rows, wl["W"], wl["levels"], nbhd=wl["nbhd"], periodic=wl["periodic"],
                   sigma=wl["sigma"], q=0.51)
     gs = np.ascontiguousarray(g[:rows])
-    t0 = time.perf_counter()
-    x, cnt = orc.pca_run(m, gs, gs, sweeps, wl["beta"], 0.0, 1 << 30, 11, burn_in=0)
     ts = np.ascontiguousarray(truth[:rows])
-    orc.metrics(ts, x, wl["levels"])                # LAST
-    orc.metrics(ts, orc.mpm(cnt), wl["levels"])     # MPM (argmax of the counts)
-    dt = time.perf_counter() - t0
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        t0 = time.perf_counter()
+        x, cnt = orc.pca_run(m, gs, gs, sweeps, wl["beta"], 0.0, 1 << 30, 11, burn_in=0)
+        orc.metrics(ts, x, wl["levels"])                # LAST
+        orc.metrics(ts, orc.mpm(cnt), wl["levels"])     # MPM (argmax of the counts)
+        dt = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old)
     su = rows * wl["W"] * sweeps
+    model, nproc = host_cpu()
     return {"value": su / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_model": model, "nproc": nproc, "pinned_core": core,
             "sample": f"{sweeps} oracle sweeps (+MPM counts, MPM image, metrics of LAST and MPM) of a {rows}x{wl['W']} "
-                      f"torus cut from the same input, 1 thread, {dt:.1f} s"}
+                      f"torus cut from the same input, 1 thread pinned to core {core} of {nproc} "
+                      f"({model}), {dt:.1f} s"}
 
 
 def run_reference(args):
@@ -196,8 +333,10 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": wl["name"], "H": wl["H"], "W": wl["W"],
                                         "reference_sample_rows": rows, "sweeps_per_step": 1},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "cpu_model": times[0]["cpu_model"], "nproc": times[0]["nproc"],
                          "sample": f"each step: 1 oracle sweep (+MPM, +metrics) of a {rows}x"
-                                   f"{wl['W']} torus cut from the workload, 1 thread"},
+                                   f"{wl['W']} torus cut from the workload, 1 thread pinned to "
+                                   f"one core"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -220,6 +359,10 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        # the strips' halo send/recv kernels must fit beside the resident interior sweep (one
+        # wave of 14 one-warp CTAs per SM leaves ~17 K registers per SM): small NCCL blocks
+        #
+        os.environ.setdefault("NCCL_NTHREADS", "128")
         dist.init_process_group("nccl", device_id=dev)
     from paper_2507_14869_b200 import dist as pdist
 
@@ -378,6 +521,10 @@ def run_ours(args):
                            "waits/writes of phase words)") +
                           " minus S sweeps of the same strip as an isolated torus (no exchange)"}
 
+    variants = None
+    if rank == 0 and n == 1 and not args.no_variants:
+        variants = run_variants(P, torch, dev, stream)
+
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_oracle(wl, truth, g, rows=wl["rows"], sweeps=3)  # ~14 s of CPU work
@@ -397,6 +544,7 @@ def run_ours(args):
                        "psnr_ssim_mpm": [float(psnr[0, 1]), float(ssim[0, 1])]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "frac_dram": (traffic / sweep_s / 1e9 / peak) if traffic else None,
                          "kernel": "sweep_binary_kernel (fused PCA sweep + MPM counts)",
                          "bytes_per_launch_alg": alg_bytes,
                          "alg_bytes_per_site_update": BYTES_PER_SU,
@@ -407,6 +555,7 @@ def run_ours(args):
             "halo": halo,
             "clocks": clk,
             "cpu_baseline": cpu,
+            "variants": variants,
         }
         print(json.dumps(line), flush=True)
     ctx.pca_destroy()
@@ -418,8 +567,76 @@ def run_ours(args):
     return 0
 
 
+def run_dry(args):
+    """--dry-run: the multi-rank orchestration of run_ours on CPU (gloo), with a stub in place
+    of the CUDA context: ranks from the launcher's environment, the workload for N ranks, this
+    rank's strip from dist.strip_rows, the NCCL unique id broadcast (created through the C ABI,
+    which needs no GPU), timed stub steps, max over ranks, one line from rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_14869_b200 import dist as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    n = max(args.gpus, world)
+    if world > 1:
+        dist.init_process_group("gloo")
+    wl = workload(n)
+    row0, rows = pdist.strip_rows(wl["H"], world, rank)
+    assert rows == wl["rows"], (rows, wl["rows"])
+    uid = pdist.broadcast_unique_id() if world > 1 else b""
+    up, down = pdist.ring_peers(rank, world, wl["periodic"])
+
+    class StubStrip:  # what the step calls on a PcaContext, without device work
+        def __init__(self):
+            self.sweeps = 0
+
+        def pca_reset(self, g=None, x0=None):
+            self.sweeps = 0
+
+        def pca_sweep(self, k):
+            self.sweeps += k
+
+        def pca_finalize(self, truth, out):
+            return np.zeros((1, 2)), np.zeros((1, 2))
+
+    ctx = StubStrip()
+    t0 = time.perf_counter()
+    for _ in range(args.warmup + args.steps):
+        ctx.pca_reset()
+        ctx.pca_sweep(args.sweeps)
+        ctx.pca_finalize(None, None)
+    ms = 1e3 * (time.perf_counter() - t0)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        got = [None] * world
+        dist.all_gather_object(got, (rank, row0, rows, up, down, len(uid)))
+    else:
+        got = [(0, row0, rows, up, down, 0)]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": UNIT,
+                          "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms / max(1, args.warmup + args.steps),
+                          "config": {"workload": wl["name"], "H": wl["H"], "W": wl["W"],
+                                     "rows_per_gpu": rows, "parallelism": wl["parallelism"]},
+                          "ranks": [{"rank": r, "row0": a, "rows": b, "up": u, "down": d,
+                                     "unique_id_bytes": k} for r, a, b, u, d, k in got],
+                          "stub_sweeps_per_step": ctx.sweeps}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

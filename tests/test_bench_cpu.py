@@ -36,3 +36,27 @@ def test_workloads():
     w8 = bench.workload(8)
     assert (w8["H"], w8["W"], w8["rows"]) == (32768, 32768, 4096)  # config 4 at P = 8
     assert bench.BYTES_PER_SU == 7
+
+
+@pytest.mark.timeout(300)
+def test_multi_gpu_self_launch_reaches_the_strip_path_dry_run():
+    """`python bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (the driver's
+    scaling run); --dry-run does the ranks' orchestration on CPU (gloo, stub context): the
+    config-4 workload for N = 2, each rank's 4096-row strip, the ring neighbours, the NCCL
+    unique id broadcast, and one line from rank 0."""
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=280,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["dry_run"] is True and d["n_gpus"] == 2
+    assert d["config"]["H"] == 8192 and d["config"]["W"] == 32768
+    ranks = sorted(d["ranks"], key=lambda e: e["rank"])
+    assert [(e["row0"], e["rows"]) for e in ranks] == [(0, 4096), (4096, 4096)]
+    assert [(e["up"], e["down"]) for e in ranks] == [(1, 1), (0, 0)]  # a 2-rank ring (torus)
+    assert all(e["unique_id_bytes"] == 128 for e in ranks)
