@@ -111,7 +111,26 @@ struct GeneralSweepParams {
     // (per beta stage); nullptr otherwise
     const double* w0;
     const double* pfx;
+    // 3 <= levels <= 5: the histogram-table kernel (sweep_table.cu) when tab != nullptr.
+    // tab = one 16-byte-aligned blob, refreshed per beta stage, copied whole into each block's
+    // shared memory by one bulk copy:
+    //   [0, TAB_OFF_W0)           A[0..8] (fp64)
+    //   [TAB_OFF_W0, tab_slots)   W0[g][x][s] = D[g][s] I[x][s] (fp64, the fp64 rare path)
+    //   [tab_slots, tab_thr)      uint2 slot[1 << tab_hbits] = {histogram tag, byte offset of
+    //                             the key's threshold rows in the thr block}; tag 0xFFFFFFFF =
+    //                             empty
+    //   [tab_thr, tab_bytes)      uint32 thr[key][g][x][TP]: T_k = ceil(F_k 2^32) - 1 of the
+    //                             site law for the key's neighbour histogram (TP = 2 for
+    //                             levels == 3, else 4)
+    // A key is a neighbour histogram h (nibble s = number of neighbours carrying s) of an
+    // interior site with at most two distinct neighbour labels; its slot is
+    // (h * tab_magic) >> (32 - tab_hbits).  Other sites (three or more labels, or fewer than
+    // nbhd neighbours at a free boundary) take the fp64 path.
+    const uint8_t* tab;
+    uint32_t tab_bytes, tab_slots, tab_thr, tab_magic;
+    int tab_hbits;
 };
+constexpr int TAB_OFF_W0 = 80;
 
 // Gibbs sampler, one colour class per launch, in place (x_in == x_out): sites of colour k
 // (4-neighbour: (r + c) mod 2; Moore-8: 2 (r mod 2) + (c mod 2), global r) draw from the
@@ -179,6 +198,8 @@ int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thre
 // nsweeps > 1: consecutive sweeps t .. t+nsweeps-1 (same tables and counting) in one
 // cooperative launch, x_in / x_out alternating; the result is in x_in when nsweeps is even.
 int launch_sweep_general(const GeneralSweepParams& p, int batch, int nsweeps, void* stream);
+// 3 <= levels <= 5 with p.tab set: the histogram-table kernel (sweep_table.cu), same contract
+int launch_sweep_table(const GeneralSweepParams& p, int batch, int nsweeps, void* stream);
 // nsweeps > 1: that many Gibbs sweeps (one beta stage, c.count_enable = counting for the run,
 // c.t = first sweep) in one cooperative launch, in place (small lattices)
 int launch_sweep_gibbs(const GibbsSweepParams& p, int batch, int nsweeps, void* stream);

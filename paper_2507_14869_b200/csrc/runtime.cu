@@ -115,6 +115,90 @@ size_t multi_max_sites() {
     return v;
 }
 
+// ---- histogram tables of the 3..5-level kernel (sweep_table.cu) ----
+// Keys: the neighbour histograms of interior sites with at most two distinct neighbour labels
+// (all NB neighbours present): n[s_lo] = NB - n_hi, n[s_hi] = n_hi (n_hi = 0: uniform), packed
+// as nibbles h = sum_s n_s << 4s.  A multiplicative hash (h * magic) >> (32 - hbits) must be
+// collision-free on the keys; the smallest hbits in 8..10 for which a magic is found (a fixed
+// splitmix64 sequence of odd multipliers, so every process finds the same one) is used.
+constexpr int TAB_MAX_LEVELS = 5;
+struct TabKeys {
+    std::vector<uint32_t> h;              // key -> histogram word
+    std::vector<std::vector<int>> n;      // key -> histogram
+    uint32_t magic = 0;
+    int hbits = 0;
+    bool ok = false;
+};
+
+bool table_eligible(const pca_config* c) {
+    const int rows = c->rows == 0 ? c->height : c->rows;
+    return c->levels >= 3 && c->levels <= TAB_MAX_LEVELS && c->width <= 65535 && rows <= 65535;
+}
+
+int tab_tp_host(int L) { return L == 3 ? 2 : 4; }
+
+size_t tab_nkeys(int L, int NB) { return (size_t)L + (size_t)L * (L - 1) / 2 * (NB - 1); }
+
+size_t tab_slots_off(int L) { return (TAB_OFF_W0 + 8 * (size_t)L * L * L + 15) & ~size_t(15); }
+
+size_t tab_blob_bytes(int L, int NB, int hbits) {
+    const size_t thr = tab_nkeys(L, NB) * L * L * tab_tp_host(L) * 4;
+    return (tab_slots_off(L) + (size_t(8) << hbits) + thr + 15) & ~size_t(15);
+}
+
+const TabKeys& tab_keys(int L, int NB) {
+    static std::mutex m;
+    static TabKeys cache[TAB_MAX_LEVELS + 1][9];
+    std::lock_guard<std::mutex> lock(m);
+    TabKeys& K = cache[L][NB];
+    if (K.ok || K.hbits < 0) return K;
+    for (int s = 0; s < L; ++s) {
+        std::vector<int> n(L, 0);
+        n[s] = NB;
+        K.n.push_back(n);
+    }
+    for (int lo = 0; lo < L; ++lo)
+        for (int hi = lo + 1; hi < L; ++hi)
+            for (int nh = 1; nh < NB; ++nh) {
+                std::vector<int> n(L, 0);
+                n[lo] = NB - nh;
+                n[hi] = nh;
+                K.n.push_back(n);
+            }
+    for (const auto& n : K.n) {
+        uint32_t h = 0;
+        for (int s = 0; s < L; ++s) h |= (uint32_t)n[s] << (4 * s);
+        K.h.push_back(h);
+    }
+    uint64_t sm = 0x9E3779B97F4A7C15ull;
+    for (int hb = 8; hb <= 10 && !K.ok; ++hb) {
+        std::vector<uint8_t> used(size_t(1) << hb);
+        for (int trial = 0; trial < (1 << 20) && !K.ok; ++trial) {
+            uint64_t z = (sm += 0x9E3779B97F4A7C15ull);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            const uint32_t mg = (uint32_t)(z ^ (z >> 31)) | 1u;
+            std::fill(used.begin(), used.end(), 0);
+            bool clash = false;
+            for (uint32_t h : K.h) {
+                const uint32_t sl = (h * mg) >> (32 - hb);
+                if (used[sl]) {
+                    clash = true;
+                    break;
+                }
+                used[sl] = 1;
+            }
+            if (!clash) {
+                K.magic = mg;
+                K.hbits = hb;
+                K.ok = true;
+            }
+        }
+    }
+    if (!K.ok) K.hbits = -1;  // no collision-free hash: the general kernel is used
+    return K;
+}
+
 // Workspace layout: byte offsets of every region.
 struct Layout {
     int rows = 0, nchunks = 0, xpitch = 0, gpitch = 0, cpitch = 0, cplanes = 0;
@@ -125,6 +209,7 @@ struct Layout {
     size_t off_gthr = 0, gthr_entries = 0;  // Gibbs uniform-neighbourhood thresholds
     size_t off_bthr = 0;                    // binary PCA thresholds [THR_ENTRIES]
     size_t off_gbthr = 0;                   // binary Gibbs thresholds [GIBBS_THR_PAD]
+    size_t off_tab = 0, tab_max = 0;        // histogram-table blob (3..5 levels, sweep_table.cu)
     size_t off_x0 = 0, off_x1 = 0, off_g = 0, off_counts = 0, off_dtab = 0, off_itab = 0, off_sums = 0,
            off_sums_max = 0, off_flag = 0, off_stage = 0, off_truth = 0, off_io = 0, off_in = 0;
     size_t io_bytes = 0;  // one bit-packed image set (packed_io), 0 otherwise
@@ -162,7 +247,10 @@ pca_status validate(const pca_config* c) {
     } else if (c->rows < c->height && c->rows < HALO) {
         return fail(PCA_EINVAL, "a row strip must own at least %d rows (halo depth)", HALO);
     }
-    if (c->kernel < 0 || c->kernel > 2) return fail(PCA_EINVAL, "kernel must be 0, 1 or 2");
+    if (c->kernel < 0 || c->kernel > 3) return fail(PCA_EINVAL, "kernel must be 0, 1, 2 or 3");
+    if (c->kernel == PCA_KERNEL_TABLE && !table_eligible(c))
+        return fail(PCA_EUNSUPPORTED, "the table kernel needs 3..%d levels, width and rows <= 65535",
+                    TAB_MAX_LEVELS);
     if (c->kernel == PCA_KERNEL_BINARY && c->levels != 2)
         return fail(PCA_EUNSUPPORTED, "the binary kernel needs levels == 2");
     const int R = c->rows_per_thread;
@@ -215,6 +303,8 @@ Layout make_layout(const pca_config* c) {
     L.off_gthr = o; o = align256(o + L.gthr_entries * sizeof(uint32_t));
     L.off_bthr = o; o = align256(o + THR_ENTRIES * sizeof(uint32_t));
     L.off_gbthr = o; o = align256(o + GIBBS_THR_PAD * sizeof(uint32_t));
+    L.tab_max = (c->levels >= 3 && c->levels <= TAB_MAX_LEVELS) ? tab_blob_bytes(c->levels, c->neighborhood, 10) : 0;
+    L.off_tab = o; o = align256(o + L.tab_max);
     L.off_sums = o; o = align256(o + B * 16 * sizeof(unsigned long long));
     L.off_sums_max = o; o = align256(o + B * 16 * sizeof(unsigned long long));
     L.off_flag = o; o = align256(o + 256);
@@ -271,6 +361,7 @@ struct pca_ctx {
     std::vector<double> dtab_host, itab_host, sparse_host;
     std::vector<uint32_t> uthr_host;
     uint32_t* uthr = nullptr;
+    std::vector<uint8_t> tab_host;  // the histogram-table blob of the current stage (TABLE kernel)
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
     cudaStream_t side = nullptr;  // interior rows of a strip, overlapping the halo exchange
@@ -552,6 +643,67 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
                                     ctx->uthr_host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                     ctx->stream));
         }
+    }
+    // the TABLE kernel runs a stage only when its fp64 path needs no log-domain fallback:
+    // Z >= A[n_x] D[g][x] >= exp(-b) and Z <= L A[NB] (weights <= 1 but A); otherwise the
+    // general kernel (which has the oracle's log-domain form) sweeps this stage
+    if (ctx->kernel == PCA_KERNEL_TABLE) {
+        const bool safe = exp(-b) >= 1e-290 && (double)c.levels * ctx->gen.A[c.neighborhood] <= 1e290;
+        ctx->gen.tab = safe ? ctx->ws + ctx->lay.off_tab : nullptr;
+    }
+    if (ctx->gen.tab) {
+        // the TABLE kernel's blob (kernels.cuh): A, W0 = D I, the slot table, and for every
+        // key histogram and (g, x) the oracle's per-site law (max-subtracted softmax,
+        // ascending cumulative sum, fp64, the uthr arithmetic) as thresholds T_k
+        const int L = c.levels, NB = c.neighborhood, TP = tab_tp_host(L);
+        const TabKeys& K = tab_keys(L, NB);
+        GeneralSweepParams& m = ctx->gen;
+        uint8_t* blob = ctx->tab_host.data();
+        std::fill(ctx->tab_host.begin(), ctx->tab_host.end(), 0);
+        memcpy(blob, m.A, 9 * sizeof(double));
+        double* w0 = reinterpret_cast<double*>(blob + TAB_OFF_W0);
+        for (int gl = 0; gl < L; ++gl)
+            for (int xl = 0; xl < L; ++xl)
+                for (int s = 0; s < L; ++s)
+                    w0[(gl * L + xl) * L + s] =
+                        ctx->dtab_host[(size_t)gl * L + s] * exp(-cq * inertia_pen(c.inertia_p, xl, s, L));
+        uint32_t* slot = reinterpret_cast<uint32_t*>(blob + m.tab_slots);
+        for (int i = 0; i < (1 << K.hbits); ++i) {
+            slot[2 * i] = 0xFFFFFFFFu;
+            slot[2 * i + 1] = 0u;
+        }
+        uint32_t* thr = reinterpret_cast<uint32_t*>(blob + m.tab_thr);
+        std::vector<double> E(L), pr(L);
+        for (size_t key = 0; key < K.h.size(); ++key) {
+            const uint32_t sl = (K.h[key] * K.magic) >> (32 - K.hbits);
+            slot[2 * sl] = K.h[key];
+            slot[2 * sl + 1] = (uint32_t)(key * L * L * TP * 4);
+            for (int gl = 0; gl < L; ++gl)
+                for (int xl = 0; xl < L; ++xl) {
+                    double Emax = -INFINITY;
+                    for (int s = 0; s < L; ++s) {
+                        const double d = lum(gl, L) - lum(s, L);
+                        const double inert = inertia_pen(c.inertia_p, xl, s, L);
+                        E[s] = a * (double)K.n[key][s] - b * d * d - cq * inert;
+                        if (E[s] > Emax) Emax = E[s];
+                    }
+                    double Z = 0.0;
+                    for (int s = 0; s < L; ++s) {
+                        pr[s] = exp(E[s] - Emax);
+                        Z += pr[s];
+                    }
+                    for (int s = 0; s < L; ++s) pr[s] = pr[s] / Z;
+                    uint32_t* out = thr + ((key * L + gl) * L + xl) * TP;
+                    double F = 0.0;
+                    for (int k = 0; k < L - 1; ++k) {
+                        F += pr[k];
+                        const double T = ceil(F * 4294967296.0);
+                        out[k] = T < 1.0 ? 0u : (T > 4294967296.0 ? 0xFFFFFFFFu : (uint32_t)(T - 1.0));
+                    }
+                }
+        }
+        CK(ctx, cudaMemcpyAsync(const_cast<uint8_t*>(m.tab), blob, m.tab_bytes, cudaMemcpyHostToDevice,
+                                ctx->stream));
     }
     ctx->tab_stage = stage;
     ctx->beta_last = beta;
@@ -917,9 +1069,25 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     ctx->gen.pfx = L.sparse_entries ? ctx->gen.w0 + L.sparse_entries : nullptr;
     ctx->gthr = L.gthr_entries ? (uint32_t*)(ctx->ws + L.off_gthr) : nullptr;
     ctx->gthr_host.resize(L.gthr_entries);
-    ctx->kernel = (cfg->kernel == PCA_KERNEL_AUTO) ? (cfg->levels == 2 ? PCA_KERNEL_BINARY
-                                                                       : PCA_KERNEL_GENERAL)
-                                                   : cfg->kernel;
+    ctx->kernel = (cfg->kernel == PCA_KERNEL_AUTO)
+                      ? (cfg->levels == 2 ? PCA_KERNEL_BINARY
+                                          : (table_eligible(cfg) ? PCA_KERNEL_TABLE : PCA_KERNEL_GENERAL))
+                      : cfg->kernel;
+    ctx->gen.tab = nullptr;
+    if (ctx->kernel == PCA_KERNEL_TABLE) {
+        const TabKeys& K = tab_keys(cfg->levels, cfg->neighborhood);
+        if (K.ok) {
+            ctx->gen.tab = ctx->ws + L.off_tab;
+            ctx->gen.tab_magic = K.magic;
+            ctx->gen.tab_hbits = K.hbits;
+            ctx->gen.tab_slots = (uint32_t)tab_slots_off(cfg->levels);
+            ctx->gen.tab_thr = ctx->gen.tab_slots + (8u << K.hbits);
+            ctx->gen.tab_bytes = (uint32_t)tab_blob_bytes(cfg->levels, cfg->neighborhood, K.hbits);
+            ctx->tab_host.assign(ctx->gen.tab_bytes, 0);
+        } else {
+            ctx->kernel = PCA_KERNEL_GENERAL;  // no collision-free hash (not expected)
+        }
+    }
     ctx->rows_per_thread = cfg->rows_per_thread;
 
     Geometry& G = ctx->geo;

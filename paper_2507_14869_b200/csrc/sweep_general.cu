@@ -582,6 +582,7 @@ int launch_g(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t s
 }  // namespace
 
 int launch_sweep_general(const GeneralSweepParams& p, int batch, int nsweeps, void* stream) {
+    if (p.tab != nullptr) return launch_sweep_table(p, batch, nsweeps, stream);
     const Geometry& G = p.c.geo;
     cudaStream_t s = (cudaStream_t)stream;
 #define PCA_GEN_LAUNCH(LTV) \

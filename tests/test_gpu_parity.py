@@ -30,6 +30,8 @@ SHAPES = [
     # the compile-time level counts with 4 neighbours (shared-memory W0 weights, SWAR table
     # rows) and 16 levels (the largest fixed path)
     (26, 70, 5, 4, False), (20, 36, 3, 4, True), (23, 50, 16, 8, True), (18, 41, 16, 4, False),
+    # 4 levels (the table kernel's middle instantiation; the general kernel's run-time path)
+    (27, 61, 4, 8, True), (19, 130, 4, 4, False),
 ]
 
 
@@ -44,6 +46,37 @@ def test_lockstep_random_states(cuda_device, shape, kernel):
     ctx = make_ctx(cfg, g, x0)
     tally = lockstep(ctx, cfg, 6)
     tally.check(allow_rate=False)
+
+
+@pytest.mark.parametrize("levels", [3, 4, 5])
+@pytest.mark.parametrize("nb,periodic,W", [(8, False, 257), (8, True, 96), (4, True, 130), (4, False, 64)])
+def test_table_kernel_lockstep_and_agreement(cuda_device, levels, nb, periodic, W):
+    """The histogram-table kernel (3..5 levels, AUTO's choice): smooth states with sprinkled
+    random labels exercise both the table rows (<= 2 neighbour labels) and the queued fp64
+    sites; lockstep against the oracle with zero mismatches, then 40 free-running sweeps with
+    MPM counts equal to the general kernel's (PCA_KERNEL_GENERAL), including the multi-sweep
+    launches of small contexts."""
+    H = 70
+    truth = synth.smooth_labels(H, W, levels, seed=levels * 10 + nb)
+    g = synth.degrade(truth, levels, 0.3, seed=5)
+    x0 = synth.smooth_labels(H, W, levels, seed=77)
+    x0[::5, ::3] = synth.random_labels(x0[::5, ::3].shape, levels, seed=78)
+    kw = dict(neighborhood=nb, periodic=periodic, sigma=0.3, beta0=1.1, beta_step=0.3,
+              beta_period=3, seed=314 + levels, mpm_burn_in=5)
+    cfg = P.make_config(H, W, levels, **kw)
+    ctx = make_ctx(cfg, g, x0)
+    assert ctx.pca_get_stats().kernel == P.KERNEL_TABLE
+    lockstep(ctx, cfg, 6).check(allow_rate=False)
+    a = make_ctx(cfg, g, x0)
+    b = make_ctx(P.make_config(H, W, levels, kernel=P.KERNEL_GENERAL, **kw), g, x0)
+    assert b.pca_get_stats().kernel == P.KERNEL_GENERAL
+    for c in (a, b):
+        c.pca_sweep(40)
+    assert np.array_equal(a.state(), b.state())
+    assert np.array_equal(a.counts(), b.counts())
+    x_o, cnt_o = orc.pca_run(oracle_model(cfg), x0, g, 40, 1.1, 0.3, 3, cfg.seed, burn_in=5)
+    assert np.array_equal(a.state()[0], x_o)
+    assert np.array_equal(a.counts()[0], cnt_o.astype(np.uint16))
 
 
 @pytest.mark.parametrize("q", [0.0, 0.51, 3.0, 1e6])

@@ -22,20 +22,26 @@ import paper_2507_14869_b200 as P  # noqa: E402
 import synth  # noqa: E402
 
 
+KERNEL = 0
+
+
 def workload(name):
     if name == "c5":
         B = 128
         g = np.stack([synth.degrade(synth.smooth_labels(512, 512, 5, 7), 5, 0.25, s) for s in range(B)])
-        return P.make_config(512, 512, 5, batch=B, sigma=0.25, mpm_burn_in=750), g
+        return P.make_config(512, 512, 5, batch=B, sigma=0.25, mpm_burn_in=750, kernel=KERNEL), g
     if name == "l5big":
         g = synth.degrade(synth.tiled_labels(8192, 8192, 5, 1), 5, 0.25, 2)[None]
         return P.make_config(8192, 8192, 5, periodic=True, sigma=0.25, beta0=1.5, beta_step=0,
-                             mpm_burn_in=0), g
+                             mpm_burn_in=0, kernel=KERNEL), g
     raise SystemExit(f"unknown workload {name}")
 
 
 def main():
+    global KERNEL
     name, t = sys.argv[1], int(sys.argv[2])
+    if "--kernel" in sys.argv:
+        KERNEL = int(sys.argv[sys.argv.index("--kernel") + 1])
     cfg, g = workload(name)
     ctx = P.PcaContext(cfg, torch.from_numpy(np.ascontiguousarray(g)).cuda())
     # one launch per sweep (the runtime splits pca_sweep(n) into per-sweep launches here)
@@ -48,7 +54,8 @@ def main():
         ctx.pca_sweep(n)
         b.record(ctx.stream)
         torch.cuda.synchronize()
-        print(f"{name} t={t}: {1e3 * a.elapsed_time(b) / n:.1f} us per sweep", flush=True)
+        print(f"{name} t={t} kernel={ctx.pca_get_stats().kernel}: {1e3 * a.elapsed_time(b) / n:.1f} us "
+              f"per sweep", flush=True)
         return
     torch.cuda.profiler.start()
     ctx.pca_sweep(1)
