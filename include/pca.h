@@ -80,16 +80,20 @@ enum {
  * sweeps on small contexts (rows x width x batch <= 2^18) execute in one cooperative launch
  * of the general code whatever the selection (exact integer thresholds for levels == 2). */
 enum {
-    PCA_KERNEL_AUTO = 0,    /* BINARY when levels == 2, TABLE for 3..5 levels, else GENERAL  */
+    PCA_KERNEL_AUTO = 0,    /* levels == 2: PACKED when eligible, else BINARY; TABLE for 3..5 */
+                            /* levels; else GENERAL                                          */
     PCA_KERNEL_GENERAL = 1, /* levels == 2: integer thresholds for every site; more levels:  */
                             /* integer thresholds where all neighbours agree (levels <= 16), */
                             /* else fp64 per-site weights (log-domain when they overflow)    */
     PCA_KERNEL_BINARY = 2,  /* levels == 2: TMA-staged rows, SWAR neighbour counts, integer  */
                             /* thresholds                                                    */
-    PCA_KERNEL_TABLE = 3    /* 3..5 levels (AUTO's choice there when width and rows <= 65535): */
+    PCA_KERNEL_TABLE = 3,   /* 3..5 levels (AUTO's choice there when width and rows <= 65535): */
                             /* per-site neighbour histograms; integer thresholds for every     */
                             /* interior site with <= 2 distinct neighbour labels (one table    */
                             /* row per histogram, g, x), fp64 weights for the others           */
+    PCA_KERNEL_PACKED = 4   /* levels == 2, whole lattice, width % 512 == 0: the state and g   */
+                            /* bit-packed in HBM (1 bit per site) during runs of sweeps; the   */
+                            /* binary kernel's decisions (same chain)                          */
 };
 
 typedef struct pca_config {
@@ -132,7 +136,7 @@ typedef struct pca_stats {
     int64_t kernel_launches; /* library kernels launched since init (all kinds)             */
     int64_t sweep_launches;  /* sweep kernels launched since init                           */
     double beta;             /* beta of the most recent sweep (beta0 before the first)       */
-    int32_t kernel;          /* PCA_KERNEL_BINARY, _GENERAL or _TABLE actually used          */
+    int32_t kernel;          /* PCA_KERNEL_BINARY, _GENERAL, _TABLE or _PACKED actually used */
     int32_t nranks;          /* NCCL ranks attached (1 if none)                              */
 } pca_stats;
 

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("PCA_B200_LIB_OVERRIDE") or os.path.join(_PKG, "libpca
 PCA_OK, PCA_EINVAL, PCA_ESTATE, PCA_ECUDA, PCA_ENCCL, PCA_ENOSPACE, PCA_EUNSUPPORTED = (
     0, -1, -2, -3, -4, -5, -6)
 EST_LAST, EST_MPM, EST_MARGINALS, EST_CM = 0, 1, 2, 3
-KERNEL_AUTO, KERNEL_GENERAL, KERNEL_BINARY, KERNEL_TABLE = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_GENERAL, KERNEL_BINARY, KERNEL_TABLE, KERNEL_PACKED = 0, 1, 2, 3, 4
 STATUS_NAMES = {0: "PCA_OK", -1: "PCA_EINVAL", -2: "PCA_ESTATE", -3: "PCA_ECUDA",
                 -4: "PCA_ENCCL", -5: "PCA_ENOSPACE", -6: "PCA_EUNSUPPORTED"}
 

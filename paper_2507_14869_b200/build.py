@@ -56,25 +56,52 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
     """Compile every csrc/*.cu into one shared library (default: the in-tree LIB).
-    `out`/`defines` build tuning variants (e.g. defines=("PCA_KSTAGES=2",))."""
+    `out`/`defines` build tuning variants (e.g. defines=("PCA_KSTAGES=2",)).  The translation
+    units compile in parallel (one nvcc per .cu, -c), then one link."""
+    import concurrent.futures as cf
+    import tempfile
+
     target = out or LIB
     if out is None and not force and not _stale():
         return LIB
     tmp = target + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
-           *[f"-D{d}" for d in defines],
-           "-Xcompiler", "-fPIC,-ffp-contract=off",
-           "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(),
-           "-o", tmp, *sources(), "-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(PKG, "build.log")
+    common = [*ARCH, "-O3", "-lineinfo", "-std=c++17", *[f"-D{d}" for d in defines],
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC,
+              "-I", _nccl_include()]
+    objdir = tempfile.mkdtemp(prefix="pca_b200_obj_")
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [_nvcc(), *common, "-c", "-o", obj, src]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, r
+
+    srcs = sources()
+    with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    log_text = []
+    failed = False
+    for src, obj, cmd, r in results:
+        log_text.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        failed |= r.returncode != 0
+    link = [_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp,
+            *[obj for _, obj, _, _ in results], "-ldl"]
+    if not failed:
+        r = subprocess.run(link, capture_output=True, text=True)
+        log_text.append(" ".join(link) + "\n" + r.stdout + r.stderr)
+        failed = r.returncode != 0
+    log = os.path.join(PKG, "build.log") if out is None else out + ".log"
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+        f.write("\n".join(log_text))
+    for _, obj, _, _ in results:
+        if os.path.exists(obj):
+            os.remove(obj)
+    os.rmdir(objdir)
+    if failed:
+        sys.stderr.write("\n".join(log_text)[-20000:])
+        raise RuntimeError(f"nvcc failed; see {log}")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("\n".join(log_text))
     os.replace(tmp, target)
     return target
 

@@ -132,6 +132,20 @@ struct GeneralSweepParams {
 };
 constexpr int TAB_OFF_W0 = 80;
 
+// two levels on bit-packed state (sweep_packed.cu): x_in / x_out packed [batch][rows+2*HALO][pp]
+// (column c at bit c%8 of byte 16 + c/8), g packed [batch][rows][gpp] (gpp = W/8); c.geo,
+// c.keys, c.t, c.chain0, c.counts, c.count_enable as for the byte kernels (c.x_* unused).
+struct PackedSweepParams {
+    SweepCommon c;
+    const uint8_t* x_in;
+    uint8_t* x_out;
+    const uint8_t* g;
+    const uint32_t* thr;  // the binary thresholds [THR_ENTRIES] of the stage
+    uint8_t* dcounts;     // uint8 count deltas of label 1 [batch][rows][cpitch] (folded by the runtime)
+    int pp, gpp;
+    long long xchain, gchain, dchain;
+};
+
 // Gibbs sampler, one colour class per launch, in place (x_in == x_out): sites of colour k
 // (4-neighbour: (r + c) mod 2; Moore-8: 2 (r mod 2) + (c mod 2), global r) draw from the
 // Gibbs conditional exp(a n_i(s) - b (lum g_i - lum s)^2) given the current state.
@@ -213,6 +227,16 @@ struct ParamTable {
 };
 int launch_param_table(const ParamTable& t, int n, uint32_t* dst, void* stream);
 int launch_sweep_binary2(const Binary2SweepParams& p, int batch, int rows_per_thread, void* stream);
+// bit-packed two-level sweep (whole lattice, W % 512 == 0) and the byte <-> packed converters
+int launch_sweep_packed(const PackedSweepParams& p, int batch, void* stream);
+int launch_state_to_packed(const Geometry& G, const uint8_t* xb, uint8_t* xp, int pp, long long pchain,
+                           int batch, void* stream);
+int launch_state_from_packed(const Geometry& G, const uint8_t* xp, int pp, long long pchain, uint8_t* xb,
+                             int batch, void* stream);
+int launch_fold_counts(const Geometry& G, uint16_t* counts, uint8_t* delta, long long dchain, int batch,
+                       void* stream);
+int launch_g_to_packed(const Geometry& G, const uint8_t* gb, uint8_t* gp, int gpp, long long gpchain, int batch,
+                       void* stream);
 int launch_pack_state(const Geometry& geo, const uint8_t* src, int src_pitch, long long src_chain,
                       uint8_t* xbuf, int batch, int* bad_flag, void* stream);
 // xbuf non-null: the same pass also writes the state buffer (x0 = g, one read of the input)
