@@ -36,7 +36,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "PCA site-updates/sec"
 UNIT = "site-updates/s"
-BYTES_PER_SU = 7  # x_t read (1) + g read (1) + x_{t+1} write (1) + uint16 count RMW (2+2)
+BYTES_PER_SU = 7  # byte kernel: x_t read (1) + g read (1) + x_{t+1} write (1) + uint16 count RMW (2+2)
+# bit-packed kernel (PCA_KERNEL_PACKED, the N = 1 default): x_t, g, x_{t+1} at 1 bit each (3/8) +
+# uint8 count-delta RMW (1+1)
+BYTES_PER_SU_PACKED = 3 / 8 + 2
+KERNEL_BINARY, KERNEL_PACKED = 2, 4
 
 
 def parse():
@@ -157,15 +161,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def load_traffic():
-    """DRAM bytes per sweep launch of the 8192^2 headline kernel from the committed ncu
-    summary: preferably a multi-launch capture without cache control (the steady state: each
-    launch's dirty lines are written back during the next, so writes are counted), else the
-    --set full capture."""
+def load_traffic(tag):
+    """DRAM bytes per sweep launch of the 8192^2 headline kernel (`tag`: the kernel's name in the
+    summary file names) from the committed ncu summaries: preferably a multi-launch capture
+    without cache control (the steady state: each launch's dirty lines are written back during
+    the next, so writes are counted), else the --set full capture."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary*.json"))) + \
-        sorted(glob.glob(os.path.join(ROOT, "profiles", "*dram_multilaunch*.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*ncu_full*{tag}*summary*.json"))) + \
+        sorted(glob.glob(os.path.join(ROOT, "profiles", f"*dram_multilaunch*{tag}*.json")))
     for f in reversed(files):
         try:
             d = json.load(open(f))
@@ -192,7 +196,8 @@ def load_instr_per_su(tag):
     summary (profiles/*<tag>*summary*.json: smsp__inst_executed.sum x 32 / sites)."""
     import glob
 
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*{tag}*summary*.json")), reverse=True):
+    pat = f"*ncu_full_{tag}_summary.json" if tag.startswith("sweep_") else f"*ncu_full_variant_{tag}_summary.json"
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", pat)), reverse=True):
         try:
             d = json.load(open(f))
             return float(d["thread_instr_per_su"]), os.path.relpath(f, ROOT)
@@ -431,12 +436,39 @@ def run_ours(args):
     value = sites_all * S * args.steps / (ms * 1e-3)
     launches = int(st1.kernel_launches - st0.kernel_launches)
 
-    # roofline of the dominant kernel (the fused sweep): algorithmic bytes / mean duration
+    # roofline of the dominant kernel (the fused sweep).  sweep_s = the mean time per sweep of
+    # the pca_sweep(S) calls (CUDA events on the library's stream; for the packed kernel it
+    # includes the pack / unpack / count-fold passes of each call)
     sweep_s = sw_ms * 1e-3 / (S * args.steps)
-    alg_bytes = BYTES_PER_SU * rows * W
+    kernel_used = int(st1.kernel)
+    packed_k = kernel_used == KERNEL_PACKED
+    bpsu = BYTES_PER_SU_PACKED if packed_k else BYTES_PER_SU
+    tag = "sweep_packed" if packed_k else "sweep_binary"
+    alg_bytes = bpsu * rows * W
     peak, peak_src = measured_peak()
     achieved = alg_bytes / sweep_s / 1e9
-    traffic, traffic_src = load_traffic()
+    traffic, traffic_src = load_traffic(tag)
+    hbm_roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "frac_dram": (traffic / sweep_s / 1e9 / peak) if traffic else None,
+                "bytes_per_launch_alg": alg_bytes, "alg_bytes_per_site_update": bpsu,
+                "mean_launch_us": sweep_s * 1e6, "peak_source": peak_src,
+                "traffic_source": traffic_src}
+    if packed_k:
+        # the packed kernel moves 2.375 B/SU and is bound by instruction issue: its roofline is
+        # thread-instructions per SU (committed ncu summary) x SU/s against the issue peak
+        ipsu, isrc = load_instr_per_su(tag)
+        ipk = issue_peak()
+        roofline = {"bound": "alu", "kernel": "sweep_packed_kernel (bit-packed PCA sweep + uint8 MPM "
+                                              "count deltas)",
+                    "achieved": (ipsu * rows * W / sweep_s) if ipsu else None, "peak": ipk,
+                    "unit": "thread-instr/s", "frac": (ipsu * rows * W / sweep_s / ipk) if ipsu else None,
+                    "traffic": traffic, "instr_per_su": ipsu, "instr_source": isrc,
+                    "mean_launch_us": sweep_s * 1e6,
+                    "peak_source": "148 SMs x 4 schedulers x 32 lanes x sm_max_mhz (1 warp-instr/clk/SMSP)",
+                    "hbm": hbm_roof}
+    else:
+        roofline = dict(hbm_roof, kernel="sweep_binary_kernel (fused PCA sweep + MPM counts)")
 
     # ---- end-to-end through the C ABI with pinned host buffers.  Two-level images travel
     # bit-packed (pca_config.packed_io): 1 bit per site in each direction ----
@@ -538,18 +570,17 @@ def run_ours(args):
                        "levels": wl["levels"], "sweeps_per_step": S,
                        "step": "reset + S fused sweeps (MPM on) + fused finalisation (MPM image, "
                                "PSNR/SSIM of LAST and MPM in one pass)",
-                       "l2": "working set ~320 MiB/GPU > 126 MB L2: inputs larger than L2, no flush",
+                       "l2": ("no flush: every step starts by rewriting the byte state and the counts "
+                              "(192 MiB > 126 MB L2) and ends with the finalisation pass (~320 MiB); "
+                              "inside a step the packed kernel's per-sweep working set (2 x 8.4 MiB "
+                              "packed state, 8 MiB packed g, 64 MiB count deltas) is L2-sized, which "
+                              "is the method's own reuse" if packed_k else
+                              "working set ~320 MiB/GPU > 126 MB L2: inputs larger than L2, no flush"),
+                       "kernel": {KERNEL_PACKED: "PACKED", KERNEL_BINARY: "BINARY"}.get(kernel_used, kernel_used),
                        "parallelism": wl["parallelism"] + (f", halo {args.halo}" if world > 1 else ""),
                        "psnr_ssim_last": [float(psnr[0, 0]), float(ssim[0, 0])],
                        "psnr_ssim_mpm": [float(psnr[0, 1]), float(ssim[0, 1])]},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "frac_dram": (traffic / sweep_s / 1e9 / peak) if traffic else None,
-                         "kernel": "sweep_binary_kernel (fused PCA sweep + MPM counts)",
-                         "bytes_per_launch_alg": alg_bytes,
-                         "alg_bytes_per_site_update": BYTES_PER_SU,
-                         "mean_launch_us": sweep_s * 1e6, "peak_source": peak_src,
-                         "traffic_source": traffic_src},
+            "roofline": roofline,
             "gpu_launches": launches,
             "e2e": e2e,
             "halo": halo,

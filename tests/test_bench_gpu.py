@@ -26,8 +26,14 @@ def test_bench_contract_line(cuda_device):
     H, W, S = d["config"]["H"], d["config"]["W"], d["config"]["sweeps_per_step"]
     assert abs(d["value"] - H * W * S / (d["ms_per_step"] * 1e-3)) < 1e-6 * d["value"]
     rf = d["roofline"]
-    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] < 1.2
-    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    if d["config"]["kernel"] == "PACKED":  # issue-bound: instructions per SU x SU/s vs the issue peak
+        assert rf["bound"] == "alu" and rf["unit"] == "thread-instr/s" and 0 < rf["frac"] < 1.0
+        assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+        hb = rf["hbm"]
+        assert hb["bound"] == "hbm" and hb["alg_bytes_per_site_update"] == 2.375 and 0 < hb["frac"] < 1.2
+    else:
+        assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] < 1.2
+        assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     assert d["gpu_launches"] >= 2 * (S + 2)
     e2e = d["e2e"]
     # two levels: images cross PCIe bit-packed (packed_io), rows of ceil(W/8) bytes

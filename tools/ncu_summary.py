@@ -41,6 +41,7 @@ def main():
     print("  stalls (warps per issue):", ", ".join(f"{n}={v:.2f}" for v, n in sorted(stalls, reverse=True)[:8]))
     if "--json" in sys.argv:
         H = int(sys.argv[sys.argv.index("--H") + 1]) if "--H" in sys.argv else None
+        sites = int(sys.argv[sys.argv.index("--sites") + 1]) if "--sites" in sys.argv else None
         scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
         rb = float(d["dram__bytes_read.sum"][0]) * scale[d["dram__bytes_read.sum"][1]]
         wb = float(d["dram__bytes_write.sum"][0]) * scale[d["dram__bytes_write.sum"][1]]
@@ -49,6 +50,10 @@ def main():
                "duration_us_ncu": float(d["gpu__time_duration.sum"][0]),
                "metrics": {k: d[k][0] + " " + d[k][1] for k in KEYS if k in d},
                "stalls": {n: v for v, n in stalls}}
+        if sites:
+            inst = float(d["smsp__inst_executed.sum"][0])
+            res["sites_per_launch"] = sites
+            res["thread_instr_per_su"] = 32.0 * inst / sites
         json.dump(res, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
 
 

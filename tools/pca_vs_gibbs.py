@@ -4,10 +4,9 @@
 
 For each config: device time per sweep of the synchronous PCA (pca_sweep, one launch per
 sweep) and of the checkerboard Gibbs sampler (pca_gibbs_sweep, one launch per colour), and,
-for the config-2 images (256x256, Moore-8, free, paper protocol: 1000 sweeps, beta 1.25 +
-0.25 every 250, MPM over the last 250), the restoration quality of both: PSNR, global SSIM
-and 7x7 windowed SSIM of the last sample and of the MPM estimate.  Writes
-gpurun_out/pca_vs_gibbs.json.
+Writes gpurun_out/pca_vs_gibbs.json.  The restoration-quality comparison on config 2's
+MRF recipe is tests/test_gpu_quality.py (it draws the truths with the oracle's sampler, which
+only tests may call).
 """
 import json
 import os
@@ -64,32 +63,6 @@ def main():
         out.append(row)
         ctx.pca_destroy()
 
-    # restoration quality on config-2-sized images (synthetic smooth label fields)
-    for L, sg in [(5, 0.25), (9, 0.2), (33, 0.1)]:
-        truth = synth.smooth_labels(256, 256, L, seed=L)
-        g = synth.degrade(truth, L, sg, seed=L + 50)
-        row = {"config": f"c2 quality l{L} sigma {sg}", "noisy_psnr": None}
-        for method in ("pca", "gibbs"):
-            cfg = P.make_config(256, 256, L, sigma=sg, seed=2025 + L, mpm_burn_in=750)
-            ctx = P.PcaContext(cfg, torch.from_numpy(g[None].copy()).cuda())
-            if row["noisy_psnr"] is None:
-                p0, s0 = ctx.pca_psnr_ssim(truth[None], P.EST_LAST)
-                row["noisy_psnr"], row["noisy_ssim"] = float(p0[0]), float(s0[0])
-                row["noisy_ssim_windowed"] = float(ctx.pca_ssim_windowed(truth[None], P.EST_LAST)[0])
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(ctx.stream)
-            (ctx.pca_sweep if method == "pca" else ctx.pca_gibbs_sweep)(1000)
-            b.record(ctx.stream)
-            torch.cuda.synchronize()
-            res = {"ms_1000_sweeps": a.elapsed_time(b)}
-            for kind, kn in [(P.EST_LAST, "last"), (P.EST_MPM, "mpm")]:
-                p, s = ctx.pca_psnr_ssim(truth[None], kind)
-                res[f"{kn}_psnr"], res[f"{kn}_ssim"] = float(p[0]), float(s[0])
-                res[f"{kn}_ssim_windowed"] = float(ctx.pca_ssim_windowed(truth[None], kind)[0])
-            row[method] = res
-            ctx.pca_destroy()
-        print(json.dumps(row), flush=True)
-        out.append(row)
     os.makedirs("gpurun_out", exist_ok=True)
     json.dump(out, open(os.path.join("gpurun_out", "pca_vs_gibbs.json"), "w"), indent=1)
 
