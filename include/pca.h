@@ -119,7 +119,8 @@ typedef struct pca_config {
     int32_t rows_per_thread; /* binary kernel: rows per warp task; 0 = auto (one wave)       */
     int32_t sweeps_per_pass; /* 0 = auto (1); 1 = one sweep per kernel launch; 2 = two      */
                            /* sweeps per HBM pass (temporal blocking; same chain) when       */
-                           /* levels == 2, W % 16 == 0 and the context owns the whole lattice */
+                           /* levels == 2 and W % 16 == 0 (kernel BINARY); on a row strip the */
+                           /* halos are 2 rows deep and exchanged once per pass              */
     int32_t inertia_p;     /* inertia norm p: 0 = L0 1{s != x_i} (paper), 1 = |lum x_i - lum s|,*/
                            /* 2 = (lum x_i - lum s)^2; identical for   */
                            /* levels == 2                                                      */
@@ -152,6 +153,16 @@ typedef struct pca_halo {
     uint8_t* recv_bottom;
     size_t row_bytes;
     size_t chain_stride;
+    /* the observed image's first / last owned row and its halo row above / below (one padded
+     * row each): with sweeps_per_pass == 2 a strip recomputes one row beyond its edges, so the
+     * caller copies a neighbour's g send row onto the matching g recv row once after
+     * pca_init / a pca_reset with a new g (NCCL or attached peers do this themselves) */
+    uint8_t* g_send_top;
+    uint8_t* g_send_bottom;
+    uint8_t* g_recv_top;
+    uint8_t* g_recv_bottom;
+    size_t g_row_bytes;
+    size_t g_chain_stride;
 } pca_halo;
 
 /* Device-initiated halo exchange: what a strip context needs to know
@@ -195,8 +206,8 @@ pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0);
 
 /* Enqueue n >= 0 synchronous PCA sweeps t, t+1, ..., t+n-1 (asynchronous).  When the
  * context owns a strip (rows < height) and NCCL is attached, each sweep is followed by
- * the halo exchange with the neighbouring ranks; without NCCL, n must be <= 1 and the
- * caller exchanges halos (pca_halo_ptrs).  Returns PCA_EUNSUPPORTED if the uint16 MPM
+ * the halo exchange with the neighbouring ranks; without NCCL or peers, n must be <= 1 (<= 2
+ * with sweeps_per_pass == 2: one pass) and the caller exchanges halos (pca_halo_ptrs).  Returns PCA_EUNSUPPORTED if the uint16 MPM
  * counters would overflow (> 65535 counted sweeps) or the sweep index would pass 2^32-1. */
 pca_status pca_sweep(pca_ctx* ctx, int32_t n);
 

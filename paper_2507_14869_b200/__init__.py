@@ -77,7 +77,10 @@ class pca_peer(ctypes.Structure):
 class pca_halo(ctypes.Structure):
     _fields_ = [("send_top", ctypes.c_void_p), ("send_bottom", ctypes.c_void_p),
                 ("recv_top", ctypes.c_void_p), ("recv_bottom", ctypes.c_void_p),
-                ("row_bytes", ctypes.c_size_t), ("chain_stride", ctypes.c_size_t)]
+                ("row_bytes", ctypes.c_size_t), ("chain_stride", ctypes.c_size_t),
+                ("g_send_top", ctypes.c_void_p), ("g_send_bottom", ctypes.c_void_p),
+                ("g_recv_top", ctypes.c_void_p), ("g_recv_bottom", ctypes.c_void_p),
+                ("g_row_bytes", ctypes.c_size_t), ("g_chain_stride", ctypes.c_size_t)]
 
 
 _lib = None

@@ -421,6 +421,8 @@ struct pca_ctx {
     int p2p = 0;
     int has_up = 0, has_dn = 0;
     pca_peer up{}, dn{};
+    uint8_t* peer_g[2] = {nullptr, nullptr};  // the up / down peers' g buffers (padded row -GHALO)
+    int g_halo_valid = 0;  // strips, two sweeps per pass: g's halo rows hold the neighbours' rows
     uint32_t* pflags = nullptr;  // [0]: phase completed by the up peer, [1]: by the down peer
     uint32_t phase = 0;          // phases (state loads, sweeps) this context has completed
 };
@@ -933,7 +935,10 @@ pca_status p2p_push(pca_ctx* ctx, int b) {
 // `depth` owned rows up and the last `depth` down, receive the halo rows.  Order per chain:
 // send(top->up), recv(bottom halo<-down), send(bottom->down), recv(top halo<-up); with
 // 2 ranks on a torus both neighbours are the same peer and NCCL matches in issue order.
-pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
+// (any padded per-chain buffer: `halo` halo rows above the owned rows, `pitch` bytes per row,
+// `chain_stride` bytes per chain)
+pca_status exchange_rows(pca_ctx* ctx, uint8_t* buf, size_t pitch, size_t chain_stride, int halo,
+                         int depth) {
     if (!ctx->comm || ctx->nranks <= 1) return PCA_OK;
     NvtxRange nvtx_("halo exchange (NCCL)");
     NcclApi& N = nccl();
@@ -947,15 +952,15 @@ pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
         if (down >= P) down = -1;
     }
     // `depth` consecutive padded rows per message (rows are contiguous in the buffer)
-    const size_t pitch = (size_t)ctx->lay.xpitch, rb = (size_t)depth * pitch;
+    const size_t rb = (size_t)depth * pitch;
     const size_t R = (size_t)ctx->lay.rows;
     ncclResult_t e = N.GroupStart();
     for (int b = 0; b < ctx->cfg.batch && e == ncclSuccess; ++b) {
-        uint8_t* base = buf + (size_t)b * ctx->geo.xchain;                       // row -HALO
-        uint8_t* top = base + HALO * pitch;                                       // rows 0..
-        uint8_t* bottom = base + (HALO + R - depth) * pitch;                      // rows R-depth..
-        uint8_t* halo_top = base + (HALO - depth) * pitch;                        // rows -depth..
-        uint8_t* halo_bottom = base + (HALO + R) * pitch;                         // rows R..
+        uint8_t* base = buf + (size_t)b * chain_stride;                           // row -halo
+        uint8_t* top = base + halo * pitch;                                       // rows 0..
+        uint8_t* bottom = base + (halo + R - depth) * pitch;                      // rows R-depth..
+        uint8_t* halo_top = base + (halo - depth) * pitch;                        // rows -depth..
+        uint8_t* halo_bottom = base + (halo + R) * pitch;                         // rows R..
         if (up >= 0 && e == ncclSuccess) e = N.Send(top, rb, ncclUint8, up, ctx->comm, ctx->stream);
         if (down >= 0 && e == ncclSuccess)
             e = N.Recv(halo_bottom, rb, ncclUint8, down, ctx->comm, ctx->stream);
@@ -970,6 +975,37 @@ pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
         return fail(PCA_ENCCL, "halo exchange: %s", N.GetErrorString(e));
     }
     return PCA_OK;
+}
+
+pca_status exchange(pca_ctx* ctx, uint8_t* buf, int depth = HALO) {
+    return exchange_rows(ctx, buf, (size_t)ctx->lay.xpitch, (size_t)ctx->geo.xchain, HALO, depth);
+}
+
+// the observed image's edge rows into the neighbours' g halo rows (strips sweeping two
+// sweeps per pass recompute one row beyond their strip, which needs its g; g changes only on
+// a reset): NCCL, or one peer phase of copies
+pca_status exchange_g(pca_ctx* ctx) {
+    const size_t gp = (size_t)ctx->lay.gpitch, R = (size_t)ctx->lay.rows;
+    if (ctx->p2p) {
+        const uint32_t k = ctx->phase + 1;
+        pca_status st = p2p_begin(ctx, k);
+        if (st != PCA_OK) return st;
+        for (int c = 0; c < ctx->cfg.batch; ++c) {
+            const uint8_t* base = ctx->g + (size_t)c * ctx->geo.gchain;
+            if (ctx->has_up) {  // our row 0 -> the up peer's row below its strip
+                uint8_t* dst = ctx->peer_g[0] + (size_t)c * (GHALO * 2 + (size_t)ctx->up.rows) * gp +
+                               (GHALO + (size_t)ctx->up.rows) * gp;
+                CK(ctx, cudaMemcpyAsync(dst, base + GHALO * gp, gp, cudaMemcpyDeviceToDevice, ctx->stream));
+            }
+            if (ctx->has_dn) {  // our last row -> the down peer's row above its strip
+                uint8_t* dst = ctx->peer_g[1] + (size_t)c * (GHALO * 2 + (size_t)ctx->dn.rows) * gp;
+                CK(ctx, cudaMemcpyAsync(dst, base + (GHALO + R - 1) * gp, gp, cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+            }
+        }
+        return p2p_end(ctx, k);
+    }
+    return exchange_rows(ctx, ctx->g, gp, (size_t)ctx->geo.gchain, GHALO, GHALO);
 }
 
 // `checked` = src is known to hold labels < levels (the validated g, or bits unpacked by
@@ -1001,6 +1037,7 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool stag
     if (g) {
         ctx->g_ok = 0;
         ctx->gpk_valid = 0;
+        ctx->g_halo_valid = 0;
         const uint8_t* dg = nullptr;
         pca_status st = device_input(ctx, g, &dg);
         if (st != PCA_OK) return st;
@@ -1279,13 +1316,17 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
     const bool strip = ctx->lay.rows < ctx->cfg.height;
-    if (strip && !ctx->comm && !ctx->p2p && n > 1)
-        return fail(PCA_EINVAL,
-                    "a strip context without NCCL or peers sweeps one step at a time (caller exchanges halos)");
-    // two sweeps per HBM pass (sweep_binary2.cu, opt-in): levels == 2, whole lattice,
-    // W % 16 == 0.  Measured slower than one sweep per pass on B200.
-    const bool pairs = ctx->kernel == PCA_KERNEL_BINARY && !strip && (ctx->cfg.width % 16) == 0 &&
+    // two sweeps per HBM pass (sweep_binary2.cu, opt-in): levels == 2, W % 16 == 0; on a row
+    // strip the halo is 2 rows deep and exchanged once per pass (half the messages per sweep,
+    // SURVEY 8(f) rank 1).  Measured slower than one sweep per pass on one B200.
+    const bool pairs = ctx->kernel == PCA_KERNEL_BINARY && (ctx->cfg.width % 16) == 0 &&
                        ctx->cfg.sweeps_per_pass == 2;
+    const bool caller_x = strip && !ctx->comm && !ctx->p2p;  // the caller exchanges the halos
+    if (caller_x && n > (pairs ? 2 : 1))
+        return fail(PCA_EINVAL, pairs ? "a strip context without NCCL or peers sweeps one pass (<= 2 "
+                                        "sweeps) at a time (caller exchanges halos)"
+                                      : "a strip context without NCCL or peers sweeps one step at a "
+                                        "time (caller exchanges halos)");
     auto counts_at = [&](int64_t t) {
         return (ctx->cfg.mpm_burn_in >= 0 && t >= ctx->cfg.mpm_burn_in) ? 1 : 0;
     };
@@ -1328,6 +1369,19 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             const int c0 = counts_at(t), c1 = counts_at(t + 1);
             if (ctx->counted + c0 + c1 > 65535)
                 return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+            // a strip recomputes sweep t one row beyond its edges: that row's g must be in the g
+            // halo (exchanged once per g; the caller copies it without NCCL or peers)
+            if (strip && !caller_x && !ctx->g_halo_valid) {
+                st = exchange_g(ctx);
+                if (st != PCA_OK) return st;
+                ctx->g_halo_valid = 1;
+            }
+            uint32_t k2 = 0;
+            if (strip && ctx->p2p) {  // one phase: the pass reads our 2-deep halos, then pushes
+                k2 = ctx->phase + 1;
+                st = p2p_begin(ctx, k2);
+                if (st != PCA_OK) return st;
+            }
             st = build_tables(ctx, t);
             if (st != PCA_OK) return st;
             memcpy(ctx->bin2.thr[0], ctx->bthr_host, sizeof(ctx->bthr_host));
@@ -1342,6 +1396,14 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             ctx->sweep_launches++;
             const int e = launch_sweep_binary2(ctx->bin2, ctx->cfg.batch, 0, ctx->stream);
             if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (two per pass)");
+            if (strip && ctx->p2p) {  // our 2 edge rows of x_{t+2} into the peers' halos
+                st = p2p_copy_edges(ctx, ctx->cur ^ 1, HALO);
+                if (st == PCA_OK) st = p2p_end(ctx, k2);
+                if (st != PCA_OK) return st;
+            } else if (strip) {
+                st = exchange(ctx, ctx->x[ctx->cur ^ 1], HALO);  // NCCL (caller: nothing)
+                if (st != PCA_OK) return st;
+            }
             ctx->cur ^= 1;
             ctx->prev_valid = 1;
             ctx->t = t + 2;
@@ -1371,7 +1433,17 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
         };
         const int R = ctx->lay.rows;
         int e = 0;
-        if (strip && ctx->p2p) {
+        if (strip && ctx->p2p && pairs) {
+            // two sweeps per pass: a single sweep (odd n) leaves 2-deep halos for the next pass
+            const uint32_t k = ctx->phase + 1;
+            st = p2p_begin(ctx, k);
+            if (st != PCA_OK) return st;
+            e = launch_rows(0, R, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (peer halos, depth 2)");
+            st = p2p_copy_edges(ctx, ctx->cur ^ 1, HALO);
+            if (st == PCA_OK) st = p2p_end(ctx, k);
+            if (st != PCA_OK) return st;
+        } else if (strip && ctx->p2p) {
             // device-initiated halo exchange: ONE launch over all rows whose edge-row CTAs also
             // store the new rows into the peers' halo rows (their output buffer); stream waits
             // and writes of the phase words order it against the peers (p2p_begin / p2p_end)
@@ -1390,7 +1462,7 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
             if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (peer halos)");
             st = p2p_end(ctx, k);
             if (st != PCA_OK) return st;
-        } else if (strip && R >= 3) {
+        } else if (strip && R >= 3 && !pairs) {
             // row strip: the two edge rows first, then their halo exchange on the main stream
             // overlapping the interior rows on the side stream; the next sweep starts after
             // both (the interior never reads the halo rows).
@@ -2016,6 +2088,13 @@ pca_status pca_halo_ptrs(pca_ctx* ctx, pca_halo* out) {
     out->recv_bottom = base + (size_t)(ctx->lay.rows + HALO) * pitch;
     out->row_bytes = HALO * pitch;
     out->chain_stride = (size_t)ctx->geo.xchain;
+    const size_t gp = (size_t)ctx->lay.gpitch;
+    out->g_send_top = ctx->g + GHALO * gp;
+    out->g_send_bottom = ctx->g + (size_t)(ctx->lay.rows + GHALO - 1) * gp;
+    out->g_recv_top = ctx->g;
+    out->g_recv_bottom = ctx->g + (size_t)(ctx->lay.rows + GHALO) * gp;
+    out->g_row_bytes = gp;
+    out->g_chain_stride = (size_t)ctx->geo.gchain;
     return PCA_OK;
 }
 
@@ -2119,7 +2198,16 @@ pca_status pca_attach_peers(pca_ctx* ctx, const pca_peer* up, const pca_peer* do
     ctx->has_dn = down != nullptr;
     if (up) ctx->up = *up;
     if (down) ctx->dn = *down;
+    // the peers' g buffers: same lattice, their row count (x[0] is the workspace base)
+    for (int i = 0; i < 2; ++i) {
+        const pca_peer* q = i == 0 ? up : down;
+        if (!q) continue;
+        pca_config pc = ctx->cfg;
+        pc.rows = q->rows;
+        ctx->peer_g[i] = q->x[0] + make_layout(&pc).off_g;
+    }
     ctx->p2p = 1;
+    ctx->g_halo_valid = 0;
     // phase 1: the current state's edge rows into the peers' halo rows
     st = p2p_push(ctx, ctx->cur);
     if (st != PCA_OK) return st;
@@ -2155,6 +2243,7 @@ pca_status pca_attach_nccl(pca_ctx* ctx, const void* id128, int32_t nranks, int3
     ctx->comm = comm;
     ctx->nranks = nranks;
     ctx->rank = rank;
+    ctx->g_halo_valid = 0;
     st = exchange(ctx, ctx->x[ctx->cur]);
     if (st != PCA_OK) return st;
     return sync(ctx);

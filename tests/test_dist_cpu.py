@@ -46,14 +46,14 @@ def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q, method="p
         x = rng.integers(0, levels, (H, W), dtype=np.uint8)  # poison: rows not owned
         x[row0:row0 + rows] = g[row0:row0 + rows]            # x0 = g on the strip
 
-        def exchange(x):
+        def exchange(x, depth=1):
             # library order: send(top -> up), recv(bottom halo <- down),
-            #                send(bottom -> down), recv(top halo <- up)
+            #                send(bottom -> down), recv(top halo <- up); `depth` rows each
             reqs = []
-            top = torch.from_numpy(x[row0].copy())
-            bot = torch.from_numpy(x[row0 + rows - 1].copy())
-            halo_bot = torch.empty(W, dtype=torch.uint8)
-            halo_top = torch.empty(W, dtype=torch.uint8)
+            top = torch.from_numpy(x[row0:row0 + depth].copy())
+            bot = torch.from_numpy(x[row0 + rows - depth:row0 + rows].copy())
+            halo_bot = torch.empty((depth, W), dtype=torch.uint8)
+            halo_top = torch.empty((depth, W), dtype=torch.uint8)
             if up >= 0:
                 reqs.append(dist.isend(top, up, tag=0))
             if down >= 0:
@@ -63,13 +63,35 @@ def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q, method="p
                 reqs.append(dist.irecv(halo_top, up, tag=1))
             for r in reqs:
                 r.wait()
-            if up >= 0:
-                x[(row0 - 1) % H] = halo_top.numpy()
-            if down >= 0:
-                x[(row0 + rows) % H] = halo_bot.numpy()
+            for d in range(depth):
+                if up >= 0:
+                    x[(row0 - depth + d) % H] = halo_top.numpy()[d]
+                if down >= 0:
+                    x[(row0 + rows + d) % H] = halo_bot.numpy()[d]
 
-        exchange(x)
-        for t in range(nsweeps):
+        if method == "pca2":
+            # two sweeps per pass (sweeps_per_pass == 2): g is known on the strip only, its halo
+            # rows come from the neighbours once; x halos are 2 rows deep, once per pass
+            g_full = g
+            g = np.random.default_rng(500 + rank).integers(0, levels, (H, W), dtype=np.uint8)
+            g[row0:row0 + rows] = g_full[row0:row0 + rows]
+            exchange(g)
+            exchange(x, 2)
+        else:
+            exchange(x)
+        for t in range(0, nsweeps, 2) if method == "pca2" else []:
+            # sweep t on the strip and one row beyond each edge (from the 2-deep halo and the
+            # g halo row), then sweep t+1 on the strip; one exchange per pass
+            raw = [row0 - 1] + list(range(row0, row0 + rows)) + [row0 + rows]
+            rows_t = [r % H for r in raw] if periodic else [r for r in raw if 0 <= r < H]
+            y = rng.integers(0, levels, (H, W), dtype=np.uint8)
+            for r in rows_t:
+                y[r] = orc.pca_sweep(m, x, g, 1.25, 99, 0, t, rows=(r, r + 1))[0][0]
+            new, _ = orc.pca_sweep(m, y, g, 1.25, 99, 0, t + 1, rows=(row0, row0 + rows))
+            x = rng.integers(0, levels, (H, W), dtype=np.uint8)
+            x[row0:row0 + rows] = new
+            exchange(x, 2)
+        for t in range(nsweeps) if method != "pca2" else []:
             if method == "pca":
                 new, _ = orc.pca_sweep(m, x, g, 1.25, 99, 0, t, rows=(row0, row0 + rows))
                 x = rng.integers(0, levels, (H, W), dtype=np.uint8)  # fresh poison every sweep
@@ -91,9 +113,10 @@ def _worker(rank, world, port, H, W, levels, periodic, nsweeps, out_q, method="p
             full = np.zeros((H, W), np.uint8)
             for r0, s in strips:
                 full[r0:r0 + len(s)] = s
+            g = np.random.default_rng(7).integers(0, levels, (H, W), dtype=np.uint8)
             ref = g.copy()
             for t in range(nsweeps):
-                if method == "pca":
+                if method in ("pca", "pca2"):
                     ref, _ = orc.pca_sweep(m, ref, g, 1.25, 99, 0, t)
                 else:
                     ref = orc.gibbs_sweep_coloured(m, ref, g, 1.25, 99, 0, t)
@@ -108,6 +131,25 @@ def test_two_rank_strip_exchange_reproduces_unsharded_chain(periodic):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, 13, 11, 3, periodic, 6, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_two_rank_strips_two_sweeps_per_pass(periodic):
+    """The temporally blocked strip protocol (sweeps_per_pass == 2): g halo
+    rows exchanged once, x halos 2 rows deep exchanged once per pass, each pass recomputing
+    sweep t one row beyond the strip: the unsharded chain, with half the exchanges."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 13, 11, 3, periodic, 6, q, "pca2"))
              for r in range(2)]
     for p in procs:
         p.start()

@@ -94,3 +94,105 @@ def test_two_per_pass_full_size_sampled_rows(cuda_device):
         tally.add(x4[r], ref[0], mg[0])
     tally.check()
     assert ctx.counts()[0].max() <= 4
+
+
+def _cudart_copy():
+    from test_gpu_parity import _cudart_memcpy
+    return _cudart_memcpy()
+
+
+def _strip_bounds(H):
+    return [0, H // 3, (2 * H) // 3 + 1, H]
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+@pytest.mark.parametrize("nbhd", [8, 4])
+def test_row_strips_two_sweeps_per_pass_loopback(cuda_device, periodic, nbhd):
+    """SURVEY 8(f) rank 1 on row strips: each strip context advances two sweeps per pass
+    (recomputing sweep t one row beyond its edges from the 2-deep x halo and the g halo row),
+    and the caller exchanges the 2-row halos once per pass -- half the messages of one sweep
+    per pass.  The strips reproduce the oracle's unsharded chain and MPM counts bit for bit,
+    across beta stages, the burn-in and an odd trailing sweep."""
+    import torch
+
+    copy = _cudart_copy()
+    H, W, Pn = 45, 1040, 3
+    g = synth.degrade(synth.smooth_labels(H, W, 2, 7), 2, 0.45, 8)
+    base = dict(neighborhood=nbhd, periodic=periodic, sigma=0.45, beta0=1.0, beta_step=0.3,
+                beta_period=3, seed=31, mpm_burn_in=3, sweeps_per_pass=2, kernel=P.KERNEL_BINARY)
+    b = _strip_bounds(H)
+    strips = [make_ctx(P.make_config(H, W, 2, row0=b[i], rows=b[i + 1] - b[i], **base), g[b[i]:b[i + 1]])
+              for i in range(Pn)]
+
+    def peers(i):
+        up, dn = i - 1, i + 1
+        if periodic:
+            up, dn = up % Pn, dn % Pn
+        return up, dn
+
+    def exchange(g_rows=False):
+        torch.cuda.synchronize()
+        hs = [s.pca_halo_ptrs() for s in strips]
+        for i in range(Pn):
+            up, dn = peers(i)
+            if 0 <= up < Pn:
+                copy(hs[i].recv_top, hs[up].send_bottom, hs[i].row_bytes)
+                if g_rows:
+                    copy(hs[i].g_recv_top, hs[up].g_send_bottom, hs[i].g_row_bytes)
+            if 0 <= dn < Pn:
+                copy(hs[i].recv_bottom, hs[dn].send_top, hs[i].row_bytes)
+                if g_rows:
+                    copy(hs[i].g_recv_bottom, hs[dn].g_send_top, hs[i].g_row_bytes)
+        torch.cuda.synchronize()
+
+    exchange(g_rows=True)
+    l0 = [s.pca_get_stats().sweep_launches for s in strips]
+    for _ in range(5):          # 5 passes = 10 sweeps, one exchange per pass
+        for s in strips:
+            s.pca_sweep(2)
+        exchange()
+    for s in strips:            # an odd trailing sweep (2-deep halos again afterwards)
+        s.pca_sweep(1)
+    exchange()
+    for s, l in zip(strips, l0):
+        assert s.pca_get_stats().sweep_launches - l == 6  # 5 passes + 1 single sweep
+    got = np.concatenate([s.state()[0] for s in strips], axis=0)
+    gc = np.concatenate([s.counts()[0] for s in strips], axis=0)
+    x_o, cnt_o = orc.pca_run(oracle_model(P.make_config(H, W, 2, **base)), g, g, 11, 1.0, 0.3, 3, 31,
+                             burn_in=3)
+    assert np.array_equal(got, x_o)
+    assert np.array_equal(gc, cnt_o[1].astype(np.uint16))
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_row_strips_two_sweeps_per_pass_over_peers(cuda_device, periodic):
+    """The same with attached peers (device-initiated halo path, one phase per pass: the pass
+    kernel, then its 2 edge rows of x_{t+2} copied into the neighbours' halos; the g halo rows
+    pushed once in the first pass), runs of several passes per call."""
+    import torch
+
+    from test_gpu_peers import _attach, _strips
+
+    H, W = 48, 1040
+    g = synth.degrade(synth.smooth_labels(H, W, 2, 9), 2, 0.45, 10)[None]
+    base = dict(neighborhood=8, periodic=periodic, sigma=0.45, beta0=1.0, beta_step=0.3, beta_period=3,
+                seed=41, mpm_burn_in=2, sweeps_per_pass=2, kernel=P.KERNEL_BINARY)
+    # one stream per strip, as on separate GPUs: a call with several phases (the g push, then
+    # the passes) waits on the neighbours' phases, which they issue after this call returns
+    strips = _strips(H, W, 2, [0, 16, 31, 48], base, g, [torch.cuda.Stream() for _ in range(3)])
+    _attach(strips, periodic)
+    l0 = [s.pca_get_stats().sweep_launches for s in strips]
+    for n in (2, 5, 4):
+        for s in strips:
+            s.pca_sweep(n)
+    torch.cuda.synchronize()
+    for s, l in zip(strips, l0):
+        assert s.pca_get_stats().sweep_launches - l == 1 + 3 + 2  # passes (+ the odd sweep)
+    got = np.concatenate([s.state() for s in strips], axis=1)[0]
+    gc = np.concatenate([s.counts() for s in strips], axis=-2)[0]
+    x_o, cnt_o = orc.pca_run(oracle_model(P.make_config(H, W, 2, **base)), g[0], g[0], 11, 1.0, 0.3, 3, 41,
+                             burn_in=2)
+    assert np.array_equal(got, x_o)
+    assert np.array_equal(gc, cnt_o[1].astype(np.uint16))
+    for s in strips:
+        s.pca_destroy()
