@@ -35,7 +35,7 @@ def test_workloads():
     assert (w1["H"], w1["W"], w1["rows"], w1["levels"]) == (8192, 8192, 8192, 2)
     w8 = bench.workload(8)
     assert (w8["H"], w8["W"], w8["rows"]) == (32768, 32768, 4096)  # config 4 at P = 8
-    assert bench.BYTES_PER_SU == 7
+    assert bench.BYTES_PER_SU == 7 and bench.BYTES_PER_SU_PACKED == 2.375
 
 
 @pytest.mark.timeout(300)
