@@ -208,7 +208,9 @@ class PcaContext:
     The workspace is a torch uint8 CUDA tensor owned by this object.  ``stream`` defaults
     to torch's current stream."""
 
-    def __init__(self, cfg: pca_config, g, x0=None, stream=None, device=None):
+    def __init__(self, cfg: pca_config, g, x0=None, stream=None, device=None, guard: int = 0):
+        """guard > 0 (testing): that many bytes after the workspace are filled with 0xA5;
+        guard_intact() tells whether any call wrote past the workspace's end."""
         import torch
 
         if not torch.cuda.is_available():
@@ -221,9 +223,12 @@ class PcaContext:
         self.image_shape = (cfg.batch, self.rows, (cfg.width + 7) // 8) if cfg.packed_io else self.shape
         nbytes = pca_workspace_bytes(cfg)
         with torch.cuda.device(self.device):
-            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+            self.workspace = torch.empty(nbytes + 256 + guard, dtype=torch.uint8, device=self.device)
             off = (-self.workspace.data_ptr()) % 256
             self._ws_ptr = self.workspace.data_ptr() + off
+            self._guard = self.workspace[off + nbytes:off + nbytes + guard] if guard else None
+            if guard:
+                self._guard.fill_(0xA5)
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
             self._keep = [g, x0]
             h = ctypes.c_void_p()
@@ -394,6 +399,13 @@ class PcaContext:
             self.handle = None
             self._staged_inputs = []
             self._async_outputs = []
+
+    def guard_intact(self) -> bool:
+        """No byte after the workspace's end was written (contexts made with guard > 0)."""
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        return bool((self._guard == 0xA5).all().item())
 
     # ---- conveniences (host NumPy results) ----
     def state(self) -> np.ndarray:

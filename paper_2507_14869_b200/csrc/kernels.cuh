@@ -25,6 +25,26 @@
 
 #include "philox.cuh"
 
+// Device-side bound checks of the debug build (build(defines=("PCA_DEBUG=1",)): a violated
+// invariant prints where and traps, so the launch fails with cudaErrorLaunchFailure instead of
+// corrupting memory silently.  compute-sanitizer is closed on the GPU pool this was built on;
+// these checks plus the workspace guard test stand in for memcheck.
+#ifdef PCA_DEBUG
+#include <cstdio>
+#define PCA_DCHECK(cond)                                                                        \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("PCA_DCHECK failed: %s at %s:%d (block %d,%d,%d thread %d)\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x);  \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define PCA_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace pcab200 {
 
 constexpr int XOFF = 16;           // data column 0 sits at byte 16 of a padded row

@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
         const int nx = (rbeg - 1 + jx + 1 <= rend) ? 2 : 1;
         const int jr = 2 * it - 2;         // g / count row rbeg+jr
         const int nr = it == 0 ? 0 : min(2, rend - rbeg - jr);
+        PCA_DCHECK(nx * XROW_BYTES + nr * (GROW_BYTES + ((CREG || RED) ? 0 : CROW_BYTES)) <= STAGE_BYTES);
+        PCA_DCHECK(rbeg - 1 + jx >= -HALO && rbeg - 1 + jx + nx - 1 < G.rows + HALO);
         mbar_expect_tx(&bars[s], nx * xbytes + nr * (gbytes + ((CREG || RED) ? 0u : cbytes)));
         for (int q = 0; q < nx; ++q)
             bulk_g2s(st + XOFS + q * XROW_BYTES, xin + (long long)(jx + q) * G.xpitch, xbytes, &bars[s]);

@@ -144,6 +144,8 @@ __global__ void __launch_bounds__(32, MIN_CTAS)
     auto issue = [&](int it, int s) {
         uint8_t* st = ring + s * STAGE_BYTES;
         const bool gr = it >= 2, cr = it >= 4 && cbytes;
+        PCA_DCHECK(rbeg - 2 + it >= -HALO && rbeg - 2 + it < G.rows + HALO);
+        PCA_DCHECK(!gr || (rbeg - 3 + it >= -GHALO && rbeg - 3 + it < G.rows + GHALO));
         mbar_expect_tx(&bars[s], wbytes + (gr ? wbytes : 0u) + (cr ? cbytes : 0u));
         bulk_g2s(st + XOFS, xin + (long long)it * G.xpitch, wbytes, &bars[s]);
         if (gr) bulk_g2s(st + GOFS, gin + (long long)it * G.gpitch, wbytes, &bars[s]);

@@ -347,6 +347,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                     const bool need = (needm >> b) & 1u;
                     const unsigned m = __ballot_sync(FULL, need);
                     const int pos = qbase + __popc(m & lt);
+                    PCA_DCHECK(!need || pos < 128);
                     if (need) queue[pos] = (uint8_t)(lane * 4 + b);
                     qpos[b] = need ? pos : -1;
                     qbase += __popc(m);
@@ -379,6 +380,7 @@ __device__ __forceinline__ void gen_rows(const GeneralSweepParams& p, GenSmem<LT
                         else if (LT == 0 && p.pfx != nullptr) w = decide_sparse<NB>(p, sm.A, jb);
                         if (w < 0) w = decide_fp64<NB>(p, sm.A, jb);
                     }
+                    PCA_DCHECK(w >= 0 && w < L);
                     res[i] = (uint8_t)w;
                 }
                 __syncwarp();

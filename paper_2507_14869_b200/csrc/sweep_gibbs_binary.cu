@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(32, GCTAS)
         const int r = row_of(j);
         const bool has_own = j < n;   // item n carries only row r_{n-1} + 1
         const bool has_g = j > 0;
+        PCA_DCHECK(xbytes * (has_own ? 2u : 1u) + (has_g ? gbytes + cbytes : 0u) <= (uint32_t)GSTAGE);
         mbar_expect_tx(&bars[s], xbytes * (has_own ? 2u : 1u) + (has_g ? gbytes + cbytes : 0u));
         bulk_g2s(st, xnb + (long long)(r - 1 + HALO) * G.xpitch, xbytes, &bars[s]);
         if (has_own) bulk_g2s(st + XROW, xown + (long long)(r + HALO) * G.xpitch, xbytes, &bars[s]);

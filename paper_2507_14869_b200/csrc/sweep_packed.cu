@@ -111,6 +111,9 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
         const bool two_x = rbeg + jx <= rend;
         const int jr = 2 * it - 2;
         const int nr = it == 0 ? 0 : min(2, rend - rbeg - jr);
+        PCA_DCHECK(rbeg - 1 + jx >= -HALO && rbeg + jx + (two_x ? 1 : 0) - 1 < G.rows + HALO);
+        PCA_DCHECK(nr == 0 || (rbeg + jr >= 0 && rbeg + jr + nr - 1 < G.rows));
+        PCA_DCHECK(64 * seg + P_XROW <= p.pp && 64 * seg + P_GROW <= p.gpp);
         mbar_expect_tx_s(bar, (two_x ? 2 : 1) * P_XROW + nr * P_GROW);
         const uint8_t* xs = xin + (long long)jx * p.pp;
         bulk_g2s_s(st, xs, P_XROW, bar);

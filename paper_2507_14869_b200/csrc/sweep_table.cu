@@ -181,6 +181,7 @@ __device__ __forceinline__ void drain(const GeneralSweepParams& p, uint32_t qoff
                                       int chain, int count_enable, int qn, int lane) {
     __syncwarp();  // the records and the producers' quad stores are visible to the whole warp
     const Geometry& G = p.c.geo;
+    PCA_DCHECK(qn <= QCAP);
     for (int i = lane; i < qn; i += 32) {
         const uint8_t* rec = tab_smem_buf + qoff + i * (uint32_t)sizeof(Rec);
         const uint4 tail = *reinterpret_cast<const uint4*>(rec + 32);  // gw, xw, rc0, mask
@@ -192,6 +193,7 @@ __device__ __forceinline__ void drain(const GeneralSweepParams& p, uint32_t qoff
             const int gi = (int)__byte_perm(tail.x, 0u, 0x4440u + b);
             const int xi = (int)__byte_perm(tail.y, 0u, 0x4440u + b);
             const int w = decide_hist_fp64<L>(h, gi, xi, r);
+            PCA_DCHECK(w >= 0 && w < L && gi < L && xi < L && row >= 0 && row < G.rows && c0 + b < G.W);
             put_site<PEERS>(p, x_out, chain, row, c0 + b, (uint8_t)w);
             if (count_enable) {
                 uint16_t* cw = p.c.counts + chain * G.cchain + (long long)w * G.cplane +
@@ -297,6 +299,7 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
             const uint2 sl = *reinterpret_cast<const uint2*>(tab_smem_buf + S.slot + 8 * ((h[b] * hmul) >> hsh));
             rare |= (sl.x != h[b]) ? (1u << b) : 0u;
             const uint32_t off = sl.y + __byte_perm(GX, 0u, 0x4440u + b) * (uint32_t)(4 * TP);
+            PCA_DCHECK(!(sl.x == h[b] && ((vmask >> b) & 1u) && act) || off + 4 * TP <= p.tab_bytes - p.tab_thr);
             uint32_t T[4];
             if (TP == 2) {
                 const uint2 v = PCA_TAB_THR_GLOBAL ? __ldg(reinterpret_cast<const uint2*>(S.gthr + off))
@@ -321,6 +324,7 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
         {
             const unsigned m = __ballot_sync(FULL, rare != 0u);
             if (rare) {
+                PCA_DCHECK(qn + __popc(m & lt) < QCAP);
                 uint8_t* rec = tab_smem_buf + S.queue + (qn + __popc(m & lt)) * (uint32_t)sizeof(Rec);
                 *reinterpret_cast<uint4*>(rec) = make_uint4(h[0], h[1], h[2], h[3]);
                 *reinterpret_cast<uint4*>(rec + 16) = rnd;
