@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1: halo rows by NCCL send/recv (default) or stored by the sweep "
                          "kernel straight into the neighbours' memory (pca_attach_peers, CUDA IPC)")
+    ap.add_argument("--graphs", type=int, default=None,
+                    help="capture each pca_sweep(S) run into a CUDA graph and replay it every step "
+                         "(pca_config.graphs); default: on for N = 1, off for row strips (N > 1)")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU only (gloo, stub context): exercise the multi-rank orchestration "
                          "(self-launch, strip partition, unique-id broadcast, max-over-ranks "
@@ -379,9 +382,10 @@ def run_ours(args):
     g_dev = torch.from_numpy(g).to(dev).reshape(1, rows, W).contiguous()
     t_dev = torch.from_numpy(truth).to(dev).reshape(1, rows, W).contiguous()
     mpm_dev = torch.empty_like(g_dev)
+    graphs = args.graphs if args.graphs is not None else (1 if world == 1 else 0)
     kw = dict(neighborhood=wl["nbhd"], periodic=wl["periodic"], sigma=wl["sigma"], q=0.51,
               beta0=wl["beta"], beta_step=0.0, beta_period=1 << 30, seed=11, mpm_burn_in=0,
-              rows_per_thread=args.rows_per_thread)
+              rows_per_thread=args.rows_per_thread, graphs=graphs if wl["levels"] == 2 else 0)
     peers = []
     if world > 1:  # this rank's row strip, NCCL attached (unique id broadcast by torch.distributed)
         ctx = pdist.strip_context(kw, wl["H"], W, wl["levels"], g_dev, stream=stream)
@@ -577,6 +581,8 @@ def run_ours(args):
                               "is the method's own reuse" if packed_k else
                               "working set ~320 MiB/GPU > 126 MB L2: inputs larger than L2, no flush"),
                        "kernel": {KERNEL_PACKED: "PACKED", KERNEL_BINARY: "BINARY"}.get(kernel_used, kernel_used),
+                       "cuda_graphs": bool(kw["graphs"]),
+                       "graph_replays": int(st1.graph_replays - st0.graph_replays),
                        "parallelism": wl["parallelism"] + (f", halo {args.halo}" if world > 1 else ""),
                        "psnr_ssim_last": [float(psnr[0, 0]), float(ssim[0, 0])],
                        "psnr_ssim_mpm": [float(psnr[0, 1]), float(ssim[0, 1])]},

@@ -128,7 +128,12 @@ typedef struct pca_config {
                            /* truth, LAST / MPM estimates, state) is bit-packed: each row is     */
                            /* ceil(width/8) bytes, column c at bit c%8 (LSB first) of byte c/8;  */
                            /* 8x fewer host<->device bytes.  The sweep itself runs on uint8.    */
-    int32_t reserved[4];   /* must be zero                                                     */
+    int32_t graphs;        /* 1 = pca_sweep(n) runs are captured into CUDA graphs and replayed */
+                           /* when the same run recurs (same t, n, counted, state buffer, table */
+                           /* stage): one graph launch instead of one launch (or, on NCCL row  */
+                           /* strips, ~8 stream operations) per sweep.  levels == 2; not with  */
+                           /* attached peers (their phase words change every call)            */
+    int32_t reserved[3];   /* must be zero                                                     */
 } pca_config;
 
 typedef struct pca_stats {
@@ -139,6 +144,7 @@ typedef struct pca_stats {
     double beta;             /* beta of the most recent sweep (beta0 before the first)       */
     int32_t kernel;          /* PCA_KERNEL_BINARY, _GENERAL, _TABLE or _PACKED actually used */
     int32_t nranks;          /* NCCL ranks attached (1 if none)                              */
+    int64_t graph_replays;   /* pca_sweep runs replayed from a captured CUDA graph (graphs)  */
 } pca_stats;
 
 /* Halo rows of the CURRENT state buffer, for caller-driven (loopback) exchange between

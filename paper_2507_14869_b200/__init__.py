@@ -58,14 +58,15 @@ class pca_config(ctypes.Structure):
         ("mpm_burn_in", ctypes.c_int32), ("row0", ctypes.c_int32), ("rows", ctypes.c_int32),
         ("kernel", ctypes.c_int32), ("rows_per_thread", ctypes.c_int32),
         ("sweeps_per_pass", ctypes.c_int32), ("inertia_p", ctypes.c_int32),
-        ("packed_io", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4),
+        ("packed_io", ctypes.c_int32), ("graphs", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3),
     ]
 
 
 class pca_stats(ctypes.Structure):
     _fields_ = [("sweeps_done", ctypes.c_int64), ("counted_sweeps", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("sweep_launches", ctypes.c_int64),
-                ("beta", ctypes.c_double), ("kernel", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+                ("beta", ctypes.c_double), ("kernel", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("graph_replays", ctypes.c_int64)]
 
 
 class pca_peer(ctypes.Structure):
@@ -147,7 +148,7 @@ def _check(status: int, where: str):
 def make_config(height, width, levels, *, batch=1, neighborhood=8, periodic=False, J=1.0 / 3.0,
                 q=0.51, sigma=0.25, beta0=1.25, beta_step=0.25, beta_period=250, chain0=0,
                 coef_scale=1.0, seed=0, mpm_burn_in=-1, row0=0, rows=0, kernel=KERNEL_AUTO,
-                rows_per_thread=0, sweeps_per_pass=0, inertia_p=0, packed_io=0) -> pca_config:
+                rows_per_thread=0, sweeps_per_pass=0, inertia_p=0, packed_io=0, graphs=0) -> pca_config:
     """pca_config with the paper's defaults (J = 1/3, q = 0.51, beta
     1.25 + 0.25 every 250 sweeps; Moore-8 neighbourhood, free boundary)."""
     c = pca_config()
@@ -161,6 +162,7 @@ def make_config(height, width, levels, *, batch=1, neighborhood=8, periodic=Fals
     c.sweeps_per_pass = int(sweeps_per_pass)
     c.inertia_p = int(inertia_p)
     c.packed_io = int(packed_io)
+    c.graphs = int(graphs)
     return c
 
 

@@ -286,8 +286,12 @@ pca_status validate(const pca_config* c) {
     if (c->packed_io != 0 && c->packed_io != 1) return fail(PCA_EINVAL, "packed_io must be 0 or 1");
     if (c->packed_io && c->levels != 2)
         return fail(PCA_EUNSUPPORTED, "bit-packed images need levels == 2");
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i)
         if (c->reserved[i] != 0) return fail(PCA_EINVAL, "reserved fields must be zero");
+    if (c->graphs != 0 && c->graphs != 1) return fail(PCA_EINVAL, "graphs must be 0 or 1");
+    if (c->graphs && c->levels != 2)
+        return fail(PCA_EUNSUPPORTED, "graph-captured sweep runs need levels == 2 (the tables of more "
+                                      "levels are uploaded by host copies)");
     return PCA_OK;
 }
 
@@ -395,6 +399,20 @@ struct pca_ctx {
     std::vector<uint32_t> uthr_host;
     uint32_t* uthr = nullptr;
     std::vector<uint8_t> tab_host;  // the histogram-table blob of the current stage (TABLE kernel)
+    // cfg.graphs: captured pca_sweep runs, keyed by the host state they start from, with the
+    // host state they leave (replayed runs apply it without re-running the host logic)
+    struct SweepGraph {
+        int64_t t, counted, tab_stage;
+        int32_t n, cur, gpk_valid;
+        cudaGraphExec_t exec;
+        int64_t t_after, counted_after, tab_stage_after, launches_d, sweep_launches_d;
+        int32_t cur_after, prev_valid_after, gpk_valid_after;
+        double beta_after;
+        uint32_t bthr_after[THR_ENTRIES];
+    };
+    std::vector<SweepGraph> graphs;
+    int64_t graph_replays = 0;
+    cudaStream_t cap = nullptr;  // the capture stream (the caller's may be the legacy default stream)
     uint8_t* xp[2] = {nullptr, nullptr};  // PACKED kernel: bit-packed state buffers
     uint8_t* gpk = nullptr;               // PACKED kernel: bit-packed g
     int gpk_valid = 0;                    // gpk holds the current g
@@ -615,7 +633,10 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
         m.coef_a = a;
         m.coef_b = b;
         m.coef_c = cq;
-        if (c.inertia_p != 0) {
+        // (two levels: every kernel decides from the binary thresholds above, so the host
+        // copies of the multi-level tables are skipped -- which keeps a two-level sweep run
+        // free of host copies, as CUDA-graph capture requires)
+        if (c.inertia_p != 0 && c.levels > 2) {
             const int L = c.levels;
             for (int xl = 0; xl < L; ++xl)
                 for (int s = 0; s < L; ++s)
@@ -645,7 +666,7 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
             CK(ctx, cudaMemcpyAsync(const_cast<double*>(m.w0), w0, 2 * n3 * sizeof(double),
                                     cudaMemcpyHostToDevice, ctx->stream));
         }
-        if (ctx->lay.uthr_entries) {
+        if (ctx->lay.uthr_entries && c.levels > 2) {
             // uniform neighbourhood (all NB neighbours carry s*): the oracle's per-site law
             // (max-subtracted softmax, ascending cumulative sum) in the same fp64 order, and
             // T_k = ceil(F_k 2^32) - 1 so that "u < F_k" <=> "r <= T_k".
@@ -1309,12 +1330,92 @@ pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0) {
     return do_reset(ctx, g, x0);
 }
 
+static pca_status sweep_direct(pca_ctx* ctx, int32_t n);
+
+// cfg.graphs: the run is captured once per starting host state into a CUDA graph (stream
+// capture of exactly the operations sweep_direct enqueues: kernels, table parameter-block
+// kernels, NCCL sends/receives, fork/join events) and replayed afterwards
+static pca_status sweep_graph(pca_ctx* ctx, int32_t n) {
+    for (auto& gr : ctx->graphs) {
+        if (gr.t == ctx->t && gr.n == n && gr.cur == ctx->cur && gr.counted == ctx->counted &&
+            gr.tab_stage == ctx->tab_stage && gr.gpk_valid == ctx->gpk_valid) {
+            CK(ctx, cudaGraphLaunch(gr.exec, ctx->stream));
+            ctx->t = gr.t_after;
+            ctx->cur = gr.cur_after;
+            ctx->counted = gr.counted_after;
+            ctx->prev_valid = gr.prev_valid_after;
+            ctx->tab_stage = gr.tab_stage_after;
+            ctx->beta_last = gr.beta_after;
+            ctx->gpk_valid = gr.gpk_valid_after;
+            memcpy(ctx->bthr_host, gr.bthr_after, sizeof(ctx->bthr_host));
+            ctx->launches += gr.launches_d;
+            ctx->sweep_launches += gr.sweep_launches_d;
+            ctx->graph_replays++;
+            return PCA_OK;
+        }
+    }
+    pca_ctx::SweepGraph gr{};
+    gr.t = ctx->t;
+    gr.n = n;
+    gr.cur = ctx->cur;
+    gr.counted = ctx->counted;
+    gr.tab_stage = ctx->tab_stage;
+    gr.gpk_valid = ctx->gpk_valid;
+    const int64_t l0 = ctx->launches, s0 = ctx->sweep_launches;
+    if (ctx->lay.rows < ctx->cfg.height && !ctx->side) {  // the strip schedule's side stream
+        CK(ctx, cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CK(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CK(ctx, cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    }
+    // capture on a private stream (the legacy default stream cannot be captured): the run's
+    // operations are enqueued there while capturing, and the graph is launched on the caller's
+    if (!ctx->cap) CK(ctx, cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+    cudaStream_t user = ctx->stream;
+    CK(ctx, cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+    ctx->stream = ctx->cap;
+    pca_status st = sweep_direct(ctx, n);
+    ctx->stream = user;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->cap, &graph);
+    if (st != PCA_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ec != cudaSuccess) return cuda_fail(ctx, ec, "cudaStreamEndCapture (sweep run)");
+    const cudaError_t ei = cudaGraphInstantiate(&gr.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return cuda_fail(ctx, ei, "cudaGraphInstantiate (sweep run)");
+    CK(ctx, cudaGraphLaunch(gr.exec, ctx->stream));
+    gr.t_after = ctx->t;
+    gr.cur_after = ctx->cur;
+    gr.counted_after = ctx->counted;
+    gr.prev_valid_after = ctx->prev_valid;
+    gr.tab_stage_after = ctx->tab_stage;
+    gr.beta_after = ctx->beta_last;
+    gr.gpk_valid_after = ctx->gpk_valid;
+    memcpy(gr.bthr_after, ctx->bthr_host, sizeof(ctx->bthr_host));
+    gr.launches_d = ctx->launches - l0;
+    gr.sweep_launches_d = ctx->sweep_launches - s0;
+    if (ctx->graphs.size() >= 8) {  // a small cache: runs recur (e.g. reset + n sweeps per step)
+        cudaGraphExecDestroy(ctx->graphs.front().exec);
+        ctx->graphs.erase(ctx->graphs.begin());
+    }
+    ctx->graphs.push_back(gr);
+    return PCA_OK;
+}
+
 pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     DeviceScope device_scope_;
     NvtxRange nvtx_("pca_sweep");
     pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
+    if (ctx->cfg.graphs && n > 0 && !ctx->p2p) return sweep_graph(ctx, n);
+    return sweep_direct(ctx, n);
+}
+
+static pca_status sweep_direct(pca_ctx* ctx, int32_t n) {
+    pca_status st = PCA_OK;
     const bool strip = ctx->lay.rows < ctx->cfg.height;
     // two sweeps per HBM pass (sweep_binary2.cu, opt-in): levels == 2, W % 16 == 0; on a row
     // strip the halo is 2 rows deep and exchanged once per pass (half the messages per sweep,
@@ -2072,6 +2173,7 @@ pca_status pca_get_stats(pca_ctx* ctx, pca_stats* out) {
     out->beta = ctx->beta_last;
     out->kernel = ctx->kernel;
     out->nranks = ctx->nranks;
+    out->graph_replays = ctx->graph_replays;
     return PCA_OK;
 }
 
@@ -2278,6 +2380,8 @@ pca_status pca_destroy(pca_ctx* ctx) {
         cudaEventDestroy(ctx->ev_out_ready);
         cudaEventDestroy(ctx->ev_out_free);
     }
+    for (auto& gr : ctx->graphs) cudaGraphExecDestroy(gr.exec);
+    if (ctx->cap) cudaStreamDestroy(ctx->cap);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     delete ctx;
     return PCA_OK;

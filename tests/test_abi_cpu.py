@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(lib):
 def test_config_struct_layout_matches_header():
     # 6 int32, 5 double, 2 int32, double, uint64, 8 int32, 4 int32 reserved (natural alignment)
     assert ctypes.sizeof(P.pca_config) == 24 + 40 + 8 + 8 + 8 + 20 + 28
-    assert P.pca_config.seed.offset == 80 and P.pca_config.inertia_p.offset == 112 and P.pca_config.packed_io.offset == 116 and P.pca_config.reserved.offset == 120
+    assert P.pca_config.seed.offset == 80 and P.pca_config.inertia_p.offset == 112 and P.pca_config.packed_io.offset == 116 and P.pca_config.graphs.offset == 120 and P.pca_config.reserved.offset == 124
 
 
 def test_workspace_and_validation(lib):
@@ -59,7 +59,7 @@ def test_workspace_and_validation(lib):
     c.sweeps_per_pass = 3
     assert lib.pca_workspace_bytes(ctypes.byref(c)) == 0
     c = P.make_config(64, 64, 2)
-    c.reserved[3] = 1
+    c.reserved[2] = 1
     assert lib.pca_workspace_bytes(ctypes.byref(c)) == 0
 
 
