@@ -45,7 +45,10 @@ namespace {
 #define PCA_P_K 4
 #endif
 #ifndef PCA_P_CTAS
-#define PCA_P_CTAS 16
+#define PCA_P_CTAS 14  // 14 x 1-warp CTAs: 76.3 us (16: 76.6, 20: 82.5; free boundary 82.4 vs 84.5)
+#endif
+#ifndef PCA_P_QN
+#define PCA_P_QN 2  // rows updated together (their Philox chains interleaved)
 #endif
 constexpr int P_XROW = 96;                  // packed x bytes staged per row: cols [c0-128, c0+640)
 constexpr int P_GROW = 64;                  // packed g bytes per row: cols [c0, c0+512)
@@ -168,14 +171,18 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
         }
     };
 
-    // update local rows r0 and (nrow == 2) r0+1 from the window X0..X3 (x rows r0-1 .. r0+2)
-    auto update2 = [&](int r0, int nrow, const uint8_t* st, const PRow& X0, const PRow& X1,
-                       const PRow& X2, const PRow& X3) {
+    // update QN local rows r0 + q0 + qq (qq < QN, rows past nrow skipped) from the window X0..X3
+    // (x rows r0-1 .. r0+2); QN = 2 interleaves the two rows' Philox chains (more ILP, more
+    // registers), QN = 1 updates one row per call
+    auto updq = [&](int r0, int nrow, int q0, const uint8_t* st, const PRow& X0, const PRow& X1,
+                    const PRow& X2, const PRow& X3) {
+        constexpr int QN = PCA_P_QN;
         const PRow* Wn[4] = {&X0, &X1, &X2, &X3};
-        uint32_t IDX4[2][4];
-        bool edge[2];
+        uint32_t IDX4[QN][4];
+        bool edge[QN];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int qq = 0; qq < QN; ++qq) {
+            const int q = q0 + qq;
             const PRow& U = *Wn[q];
             const PRow& M = *Wn[q + 1];
             const PRow& D = *Wn[q + 2];
@@ -199,18 +206,21 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                IDX4[q][i] = (S[i] << 4) | (spread4((g16 >> (4 * i)) & 0xFu) << 3) | (M.w[i] << 2);
-            edge[q] = !PER && (k == 0 || k == nchunks - 1 || grow == 0 || grow == G.H - 1);
-        }
-        if (nrow < 2) {
+                IDX4[qq][i] = (S[i] << 4) | (spread4((g16 >> (4 * i)) & 0xFu) << 3) | (M.w[i] << 2);
+            edge[qq] = !PER && (k == 0 || k == nchunks - 1 || grow == 0 || grow == G.H - 1);
+            if (q >= nrow) {  // past the run: its stage slot holds stale bytes; decide on index 0
 #pragma unroll
-            for (int i = 0; i < 4; ++i) IDX4[1][i] = 0u;
+                for (int i = 0; i < 4; ++i) IDX4[qq][i] = 0u;
+            }
         }
-        uint32_t O[2][4], B[2] = {0u, 0u};
+        uint32_t O[QN][4], B[QN];
+#pragma unroll
+        for (int qq = 0; qq < QN; ++qq) B[qq] = 0u;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int qq = 0; qq < QN; ++qq) {
+                const int q = q0 + qq;
                 const int grow = G.row0 + r0 + q;
                 const uint4 rnd = philox4x32_10(
                     make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain), p.c.keys);
@@ -218,11 +228,11 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
                 uint32_t bits = 0u;
 #pragma unroll
                 for (int b = 3; b >= 0; --b) {
-                    uint32_t off = __byte_perm(IDX4[q][i], 0u, 0x4440 + b);
+                    uint32_t off = __byte_perm(IDX4[qq][i], 0u, 0x4440 + b);
                     if (PER) {
                         off += NB * 36 * 4;
                     } else {
-                        const int np = edge[q] ? p_neighbours_present<NB>(grow, G.H, ccol + 4 * i + b, G.W) : NB;
+                        const int np = edge[qq] ? p_neighbours_present<NB>(grow, G.H, ccol + 4 * i + b, G.W) : NB;
                         off += (uint32_t)np * 144u;
                     }
                     const uint32_t T = *reinterpret_cast<const uint32_t*>(thr_b + off);
@@ -231,19 +241,20 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
                         : "r"(T), "r"(rw[b]));
                 }
                 const uint32_t nib = ~bits & 0xFu;  // bit b: site 4i + b is 1
-                B[q] |= nib << (4 * i);
-                O[q][i] = spread4(nib);
+                B[qq] |= nib << (4 * i);
+                O[qq][i] = spread4(nib);
             }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            if (q == 1 && nrow < 2) break;
+        for (int qq = 0; qq < QN; ++qq) {
+            const int q = q0 + qq;
+            if (q >= nrow) break;
             const int r = r0 + q;
             if (cnt) {  // byte-wise adds: no carries, deltas stay <= 255 between folds
                 const uint4 c = CR[q];
                 *reinterpret_cast<uint4*>(co + (long long)(r - rbeg) * G.cpitch) =
-                    make_uint4(c.x + O[q][0], c.y + O[q][1], c.z + O[q][2], c.w + O[q][3]);
+                    make_uint4(c.x + O[qq][0], c.y + O[qq][1], c.z + O[qq][2], c.w + O[qq][3]);
             }
-            store_row(r, B[q]);
+            store_row(r, B[qq]);
         }
     };
 
@@ -258,7 +269,9 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
         read_x(st, 1, B1);
         if (it > 0) {
             const int r0 = rbeg + 2 * it - 2;
-            update2(r0, r0 + 1 < rend ? 2 : 1, st, A0, A1, B0, B1);
+            const int nrow = r0 + 1 < rend ? 2 : 1;
+            updq(r0, nrow, 0, st, A0, A1, B0, B1);
+            if (PCA_P_QN == 1 && nrow == 2) updq(r0, nrow, 1, st, A0, A1, B0, B1);
             load_counts(r0 + 2);
         }
         __syncwarp();

@@ -31,8 +31,8 @@
 // Data movement: a thread owns a quad of 4 sites (one Philox4x32-10 call) and walks a run of
 // rows with a rolling 3-row window of one-hot words (the next x row and g row prefetched one
 // row ahead, as in sweep_general.cu); the table blob reaches each block's shared memory with
-// one TMA bulk copy.
-#include <cooperative_groups.h>
+// one TMA bulk copy.  One launch per sweep: runs of sweeps on small lattices (one cooperative
+// launch) use the general kernel's multi-sweep variant, which is faster there.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -42,8 +42,6 @@
 
 namespace pcab200 {
 namespace {
-
-namespace cg = cooperative_groups;
 
 constexpr int TB_THREADS = 256;
 constexpr int TB_WARPS = TB_THREADS / 32;
@@ -443,36 +441,6 @@ __global__ void __launch_bounds__(TB_THREADS, PCA_TAB_MINB)
                                   rbeg, rend, d.R);
 }
 
-// small lattices: `nsweeps` sweeps of one beta stage and counting mode in one cooperative
-// launch (as sweep_general.cu's sweep_multi_kernel)
-template <int NB, int L>
-__global__ void __launch_bounds__(TB_THREADS, PCA_TAB_MINB)
-    sweep_table_multi_kernel(const __grid_constant__ GeneralSweepParams p, int R, int nsweeps, int batch) {
-    const TabShared S = tab_setup(p);
-    const TDecomp d = tdecomp((p.c.geo.W + 3) >> 2, p.c.rhi - p.c.rlo, R);
-    const int items = d.nxb * d.nrb * batch;
-    for (int sw = 0; sw < nsweeps; ++sw) {
-        const uint8_t* xi = (sw & 1) ? p.c.x_out : p.c.x_in;
-        uint8_t* xo = (sw & 1) ? const_cast<uint8_t*>(p.c.x_in) : p.c.x_out;
-        for (int it = blockIdx.x; it < items; it += gridDim.x) {
-            const int xb = it % d.nxb;
-            const int rb = (it / d.nxb) % d.nrb;
-            const int chain = it / (d.nxb * d.nrb);
-            const int qd = xb * d.QW + (threadIdx.x & (d.QW - 1));
-            const int rbeg = p.c.rlo + (rb * d.RS + threadIdx.x / d.QW) * d.R;
-            const int rend = min(rbeg + d.R, p.c.rhi);
-            tab_rows<NB, L, true, false>(p, S, xi, xo, p.c.t + (uint32_t)sw, p.c.count_enable, qd, chain,
-                                         rbeg, rend, d.R);
-        }
-        if (gridDim.x == 1) {
-            __syncthreads();
-        } else {
-            __threadfence();
-            cg::this_grid().sync();
-        }
-    }
-}
-
 template <int NB, int L>
 struct TabLaunch {
     static LaunchInfo& get(int smem) {
@@ -486,11 +454,8 @@ struct TabLaunch {
                 cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
                 cudaFuncSetAttribute(sweep_table_kernel<NB, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_SMEM_MAX);
                 cudaFuncSetAttribute(sweep_table_kernel<NB, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_SMEM_MAX);
-                cudaFuncSetAttribute(sweep_table_multi_kernel<NB, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, TAB_SMEM_MAX);
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.occ, sweep_table_kernel<NB, L, false>, TB_THREADS, smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.mocc, sweep_table_multi_kernel<NB, L>, TB_THREADS, smem);
                 if (li.occ < 1) li.occ = 1;
-                if (li.mocc < 1) li.mocc = 1;
                 li.ok.store(true, std::memory_order_release);
             }
         }
@@ -509,19 +474,7 @@ int launch_tab(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t
     if (nr <= 0) return 0;
     const TDecomp d1 = tdecomp(nquads, nr, 1);
     const long long quadrows = (long long)d1.nxb * d1.QW * nr * batch;
-    if (nsweeps > 1) {
-        const long long slots = (long long)TL.sms * TL.mocc;
-        long long R = (quadrows + slots * TB_THREADS - 1) / (slots * TB_THREADS);
-        if (R < 1) R = 1;
-        const TDecomp d = tdecomp(nquads, nr, (int)R);
-        const long long items = (long long)d.nxb * d.nrb * batch;
-        const int grid = (int)(items < slots ? items : slots);
-        GeneralSweepParams pp = p;
-        int Ri = (int)R, ns = nsweeps, b = batch;
-        void* args[] = {&pp, &Ri, &ns, &b};
-        return (int)cudaLaunchCooperativeKernel((const void*)sweep_table_multi_kernel<NB, L>, dim3(grid),
-                                                dim3(TB_THREADS), args, smem, s);
-    }
+    if (nsweeps > 1) return (int)cudaErrorInvalidValue;  // runs of sweeps: the general kernel's
     const long long target = (long long)PCA_TAB_WAVES * TL.sms * TL.occ * TB_THREADS;
     long long R = (quadrows + target - 1) / target;
     if (R < 1) R = 1;
