@@ -111,15 +111,19 @@ template <int L>
 __device__ __forceinline__ int decide_hist_fp64(uint32_t h, int gi, int xi, uint32_t r) {
     const double* A = sm_A();
     const double* Wrow = sm_W0() + (gi * L + xi) * L;
+    double w[L];
     double Z = 0.0;
 #pragma unroll
-    for (int s = 0; s < L; ++s) Z += A[(h >> (4 * s)) & 0xFu] * Wrow[s];
+    for (int s = 0; s < L; ++s) {
+        w[s] = A[(h >> (4 * s)) & 0xFu] * Wrow[s];
+        Z += w[s];
+    }
     const double target = (double)r * (1.0 / 4294967296.0) * Z;
     double F = 0.0;
     int res = 0;
 #pragma unroll
     for (int s = 0; s < L - 1; ++s) {
-        F += A[(h >> (4 * s)) & 0xFu] * Wrow[s];  // the same products, the same order
+        F += w[s];
         res += (F <= target) ? 1 : 0;
     }
     return res;

@@ -971,3 +971,44 @@ def test_largest_single_lattice_32768_squared(cuda_device):
     tally.check()
     assert np.array_equal(ctx.counts()[0], acc)
     ctx.pca_destroy()
+
+
+def _random_new_kernel_configs(n, seed):
+    """Random configurations for the round-2 kernels: PACKED (two levels, W a multiple of 512)
+    and TABLE (3..5 levels), with extreme coefficients among them (the table kernel then
+    hands those beta stages to the general kernel's log-domain path)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        packed = i % 2 == 0
+        L = 2 if packed else int(rng.choice([3, 4, 5]))
+        nb = int(rng.choice([4, 8]))
+        per = bool(rng.integers(2))
+        H = int(rng.integers(3, 40))
+        W = int(rng.choice([512, 1024, 1536])) if packed else int(rng.integers(3 if per else 1, 700))
+        sigma = float(rng.choice([rng.uniform(0.05, 0.8), 0.01]))  # 0.01: b = 5000, weights underflow
+        kw = dict(neighborhood=nb, periodic=per, sigma=sigma,
+                  q=float(rng.choice([0.0, 0.51, rng.uniform(0, 5)])), beta0=float(rng.uniform(0.3, 3)),
+                  beta_step=float(rng.uniform(0, 1)), beta_period=int(rng.integers(1, 4)),
+                  coef_scale=float(rng.choice([1.0, 0.5])), inertia_p=int(rng.integers(0, 3)),
+                  J=float(rng.uniform(0.1, 1.0)), seed=int(rng.integers(1 << 40)),
+                  chain0=int(rng.integers(0, 1000)), batch=int(rng.integers(1, 4)),
+                  mpm_burn_in=int(rng.integers(-1, 3)),
+                  kernel=P.KERNEL_PACKED if packed else P.KERNEL_TABLE)
+        out.append((H, W, L, kw))
+    return out
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_randomised_new_kernel_configurations_lockstep(cuda_device, case):
+    """4 lockstep sweeps of the packed / table kernels against the oracle on random
+    configurations (smooth states with random sprinkles: table rows and queued sites)."""
+    H, W, L, kw = _random_new_kernel_configs(16, 77)[case]
+    cfg = P.make_config(H, W, L, **kw)
+    B = kw["batch"]
+    g = np.stack([synth.random_labels((H, W), L, seed=case * 10 + b) for b in range(B)])
+    x0 = np.stack([synth.smooth_labels(H, W, L, seed=case * 10 + 5 + b) for b in range(B)])
+    x0[:, ::4, ::3] = synth.random_labels(x0[:, ::4, ::3].shape, L, seed=case)
+    ctx = make_ctx(cfg, g, x0)
+    assert ctx.pca_get_stats().kernel == kw["kernel"]
+    lockstep(ctx, cfg, 4).check()
