@@ -53,6 +53,9 @@ namespace {
 #ifndef PCA_T_RED
 #define PCA_T_RED 0
 #endif
+#ifndef PCA_B_PRE
+#define PCA_B_PRE 1  // the row-independent Philox prefix in registers (philox.cuh)
+#endif
 #ifndef PCA_F_K
 #define PCA_F_K 4
 #endif
@@ -154,6 +157,13 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     uint16_t* co = p.c.counts + chain * G.cchain + ccol + (long long)rbeg * G.cpitch;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const uint8_t* thr_b = reinterpret_cast<const uint8_t*>(s_thr);
+    // the lane's 4 Philox counters (4k+i, row, t, tagchain): rounds 0..2 minus the row, once
+    // (philox.cuh philox_pre / philox_row: 34 instead of 40 instructions per call)
+    PhiloxPre ppre[4];
+    if (PCA_B_PRE) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ppre[i] = philox_pre((uint32_t)(4 * k + i), p.c.t, tagchain, p.c.keys);
+    }
     // CREG: the count rows of the next two updated rows, loaded one item ahead
     uint4 CR[2][2];
     auto load_counts = [&](int rfirst) {
@@ -253,8 +263,9 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
         uint32_t O[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const uint4 rnd = philox4x32_10(
-                make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+            const uint4 rnd = PCA_B_PRE ? philox_row(ppre[i], (uint32_t)grow, p.c.keys)
+                                        : philox4x32_10(make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t,
+                                                                   tagchain), p.c.keys);
             const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
             // sub.cc sets the carry of T + ~r + 1, i.e. T >= r: the complement of the decision
             // w = (r > T); shifted into a 4-bit word (site b -> bit b, sites taken 3..0)
@@ -352,8 +363,9 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
         uint32_t O[2][4];
         auto decide = [&](int q, int i) {
             const int grow = G.row0 + r0 + q;
-            const uint4 rnd = philox4x32_10(
-                make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+            const uint4 rnd = PCA_B_PRE ? philox_row(ppre[i], (uint32_t)grow, p.c.keys)
+                                        : philox4x32_10(make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t,
+                                                                   tagchain), p.c.keys);
             const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
 #if PCA_CARRY
             // sub.cc sets the carry of T + ~r + 1, i.e. T >= r: the complement of the decision

@@ -45,10 +45,18 @@ namespace {
 #define PCA_P_K 4
 #endif
 #ifndef PCA_P_CTAS
-#define PCA_P_CTAS 14  // 14 x 1-warp CTAs: 76.3 us (16: 76.6, 20: 82.5; free boundary 82.4 vs 84.5)
+#define PCA_P_CTAS 16
 #endif
 #ifndef PCA_P_QN
-#define PCA_P_QN 2  // rows updated together (their Philox chains interleaved)
+#define PCA_P_QN 1  // rows updated together (2: their Philox chains interleaved, more registers)
+#endif
+#ifndef PCA_P_PRE
+// 1: the row-independent Philox prefix of the lane's 4 counters kept in registers (philox.cuh
+// philox_pre / philox_row: 34 instead of 40 instructions per call).  Measured with 50-sweep
+// calls, torus MPM on / off / free boundary, us per sweep: prefix + 1 row per update + 16 CTAs
+// 74.3 / 68.9 / 82.4; prefix + 2 joint rows + 14 CTAs 74.3 / 67.1 / 88.6; no prefix + 2 joint
+// rows + 14 CTAs (round-2 first version) 76.3 / 70.7 / 82.4
+#define PCA_P_PRE 1
 #endif
 constexpr int P_XROW = 96;                  // packed x bytes staged per row: cols [c0-128, c0+640)
 constexpr int P_GROW = 64;                  // packed g bytes per row: cols [c0, c0+512)
@@ -105,6 +113,12 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
     uint8_t* co = p.dcounts + chain * p.dchain + ccol + (long long)rbeg * G.cpitch;
     const uint32_t tagchain = (TAG_PCA << 24) | (p.c.chain0 + (uint32_t)chain);
     const uint8_t* thr_b = reinterpret_cast<const uint8_t*>(s_thr);
+    // the lane's 4 Philox counters (4k+i, row, t, tagchain): rounds 0..2 minus the row, once
+    PhiloxPre ppre[4];
+    if (PCA_P_PRE) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ppre[i] = philox_pre((uint32_t)(4 * k + i), p.c.t, tagchain, p.c.keys);
+    }
 
     // shared-window addresses of the ring and its barriers, computed once
     const uint32_t ring_s = smem_u32(ring), bars_s = smem_u32(bars);
@@ -222,8 +236,9 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
             for (int qq = 0; qq < QN; ++qq) {
                 const int q = q0 + qq;
                 const int grow = G.row0 + r0 + q;
-                const uint4 rnd = philox4x32_10(
-                    make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t, tagchain), p.c.keys);
+                const uint4 rnd = PCA_P_PRE ? philox_row(ppre[i], (uint32_t)grow, p.c.keys)
+                                            : philox4x32_10(make_uint4((uint32_t)(4 * k + i), (uint32_t)grow,
+                                                                       p.c.t, tagchain), p.c.keys);
                 const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
                 uint32_t bits = 0u;
 #pragma unroll

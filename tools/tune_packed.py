@@ -29,7 +29,7 @@ for name, kw in [("moore_torus_mpm", dict(mpm_burn_in=0)), ("moore_torus_nompm",
 print(json.dumps(res))
 '''
 out = {}
-for lib in sorted(glob.glob(os.path.join(ROOT, "build_variants", "packed_*.so"))) + [os.path.join(ROOT, "paper_2507_14869_b200", "libpca_b200.so")]:
+for lib in sorted(glob.glob(os.path.join(ROOT, "build_variants", os.environ.get("VARIANTS", "packed_*.so")))) + [os.path.join(ROOT, "paper_2507_14869_b200", "libpca_b200.so")]:
     env = dict(os.environ, ROOT=ROOT, PCA_B200_LIB_OVERRIDE=lib)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-300:]
