@@ -268,7 +268,7 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
         onehots(nxt, OD);
         const uint32_t xdn = nxt[1];
         const uint32_t gword = gnext;
-        if (act && r + 1 < rend) {
+        if (act) {  // (the last row's prefetch reads x row rend+1 and g row rend: halo rows, unused)
             load_row(xp, nxt);
             gnext = __ldg(reinterpret_cast<const uint32_t*>(gp));
         }
