@@ -560,6 +560,27 @@ def run_ours(args):
     variants = None
     if rank == 0 and n == 1 and not args.no_variants:
         variants = run_variants(P, torch, dev, stream)
+        if packed_k:
+            # the same sweeps on the byte-state kernel (round 1's headline, HBM-bound at 7 B/SU):
+            # its time and HBM fraction, for continuity with the packed kernel's issue roofline
+            bctx = P.PcaContext(P.make_config(wl["H"], W, wl["levels"], **dict(kw, kernel=KERNEL_BINARY,
+                                                                               graphs=0)), g_dev, stream=stream)
+            bctx.pca_sweep(10)
+            bctx.pca_reset(None, None)
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            bctx.pca_sweep(S)
+            b1.record(stream)
+            torch.cuda.synchronize(dev)
+            bs = b0.elapsed_time(b1) * 1e-3 / S
+            bt, bsrc = load_traffic("sweep_binary")
+            variants["byte_state_kernel"] = {
+                "workload": wl["name"] + " (the byte-state kernel, PCA_KERNEL_BINARY)",
+                "us_per_sweep": bs * 1e6, "value": rows * W / bs, "unit": UNIT,
+                "roofline": {"bound": "hbm", "achieved": BYTES_PER_SU * rows * W / bs / 1e9, "peak": peak,
+                             "unit": "GB/s", "frac": BYTES_PER_SU * rows * W / bs / 1e9 / peak,
+                             "alg_bytes_per_site_update": BYTES_PER_SU, "traffic": bt, "traffic_source": bsrc}}
+            bctx.pca_destroy()
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
