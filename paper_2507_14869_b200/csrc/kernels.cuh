@@ -251,8 +251,9 @@ int launch_sweep_binary2(const Binary2SweepParams& p, int batch, int rows_per_th
 int launch_sweep_packed(const PackedSweepParams& p, int batch, void* stream);
 int launch_state_to_packed(const Geometry& G, const uint8_t* xb, uint8_t* xp, int pp, long long pchain,
                            int batch, void* stream);
+// halo_up / halo_dn: also write the halo rows above / below (a torus, or a strip's neighbour)
 int launch_state_from_packed(const Geometry& G, const uint8_t* xp, int pp, long long pchain, uint8_t* xb,
-                             int batch, void* stream);
+                             int batch, void* stream, int halo_up, int halo_dn);
 int launch_fold_counts(const Geometry& G, uint16_t* counts, uint8_t* delta, long long dchain, int batch,
                        void* stream);
 int launch_g_to_packed(const Geometry& G, const uint8_t* gb, uint8_t* gp, int gpp, long long gpchain, int batch,

@@ -141,10 +141,9 @@ struct TabKeys {
     bool ok = false;
 };
 
-// the bit-packed kernel: two levels, one context owning the whole lattice, W % 512 == 0
+// the bit-packed kernel: two levels, W % 512 == 0 (a whole lattice or a row strip)
 bool packed_eligible(const pca_config* c) {
-    return c->levels == 2 && (c->rows == 0 || c->rows == c->height) && c->width % 512 == 0 &&
-           c->height >= 3;
+    return c->levels == 2 && c->width % 512 == 0 && c->height >= 3;
 }
 
 bool table_eligible(const pca_config* c) {
@@ -1113,6 +1112,7 @@ pca_status do_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0, bool stag
 pca_status sweep_packed_run(pca_ctx* ctx, int32_t n) {
     const pca_config& c = ctx->cfg;
     const int B = c.batch;
+    const bool strip = ctx->lay.rows < c.height;
     if (!ctx->gpk_valid) {
         LAUNCH(ctx, launch_g_to_packed(ctx->geo, ctx->g, ctx->gpk, ctx->pk.gpp, ctx->pk.gchain, B, ctx->stream));
         ctx->gpk_valid = 1;
@@ -1144,10 +1144,43 @@ pca_status sweep_packed_run(pca_ctx* ctx, int32_t n) {
         ctx->pk.x_out = ctx->xp[pc ^ 1];
         ctx->pk.g = ctx->gpk;
         ctx->pk.thr = ctx->bin.thr;
-        ctx->launches++;
-        ctx->sweep_launches++;
-        const int e = launch_sweep_packed(ctx->pk, B, ctx->stream);
-        if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (packed)");
+        const int R = ctx->lay.rows;
+        auto launch_packed_rows = [&](int rlo, int rhi, cudaStream_t s) -> int {
+            ctx->launches++;
+            ctx->sweep_launches++;
+            ctx->pk.c.rlo = rlo;
+            ctx->pk.c.rhi = rhi;
+            return launch_sweep_packed(ctx->pk, B, s);
+        };
+        if (strip && R >= 3) {
+            // a row strip: the two edge rows first, then (over NCCL) their packed rows (W/8 + 32
+            // bytes each) to the neighbours on the main stream, overlapping the interior rows on
+            // the side stream (the byte kernels' schedule, pca_sweep); a caller-exchanged strip
+            // takes the same launches with no exchange
+            if (!ctx->side) {
+                CK(ctx, cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+                CK(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+                CK(ctx, cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+            }
+            CK(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+            CK(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            int e = launch_packed_rows(0, 1, ctx->stream);
+            if (!e) e = launch_packed_rows(R - 1, R, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (packed edge rows)");
+            st = exchange_rows(ctx, ctx->xp[pc ^ 1], (size_t)ctx->pk.pp, (size_t)ctx->pk.xchain, HALO, 1);
+            if (st != PCA_OK) return st;
+            e = launch_packed_rows(1, R - 1, ctx->side);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (packed interior rows)");
+            CK(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+            CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+        } else {
+            const int e = launch_packed_rows(0, R, ctx->stream);
+            if (e) return cuda_fail(ctx, (cudaError_t)e, "sweep (packed)");
+            if (strip) {  // fewer than 3 rows (no exchange for a caller-exchanged strip)
+                st = exchange_rows(ctx, ctx->xp[pc ^ 1], (size_t)ctx->pk.pp, (size_t)ctx->pk.xchain, HALO, 1);
+                if (st != PCA_OK) return st;
+            }
+        }
         pc ^= 1;
         ctx->t = t + 1;
         ctx->counted += count;
@@ -1160,12 +1193,18 @@ pca_status sweep_packed_run(pca_ctx* ctx, int32_t n) {
     pca_status st = fold();  // the canonical uint16 counts are complete again
     if (st != PCA_OK) return st;
     const int cur = ctx->cur ^ (n & 1);
+    // the halo rows hold real rows where a neighbour is (a torus, or a strip's neighbouring
+    // rank); a free boundary's outer halo rows keep the byte buffers' sentinel
+    const int hu = c.periodic || c.row0 > 0, hd = c.periodic || c.row0 + ctx->lay.rows < c.height;
     LAUNCH(ctx, launch_state_from_packed(ctx->geo, ctx->xp[pc], ctx->pk.pp, ctx->pk.xchain, ctx->x[cur], B,
-                                         ctx->stream));
+                                         ctx->stream, hu, hd));
     LAUNCH(ctx, launch_state_from_packed(ctx->geo, ctx->xp[pc ^ 1], ctx->pk.pp, ctx->pk.xchain,
-                                         ctx->x[cur ^ 1], B, ctx->stream));
+                                         ctx->x[cur ^ 1], B, ctx->stream, hu, hd));
     ctx->cur = cur;
     ctx->prev_valid = 1;
+    // a strip over NCCL: the byte state's 2-deep halos from the neighbours (the packed runs
+    // exchanged 1-deep packed halos only); a caller-exchanged strip's caller does this
+    if (strip) return exchange(ctx, ctx->x[ctx->cur]);
     return PCA_OK;
 }
 
@@ -1434,7 +1473,10 @@ static pca_status sweep_direct(pca_ctx* ctx, int32_t n) {
     // small lattices: runs of sweeps in one cooperative launch (sweep_multi_kernel)
     const bool small = !strip && !pairs &&
                        (size_t)ctx->lay.rows * ctx->cfg.width * ctx->cfg.batch <= multi_max_sites();
-    if (ctx->kernel == PCA_KERNEL_PACKED && n > 0 && !(small && n >= 2)) return sweep_packed_run(ctx, n);
+    // the packed kernel, except on strips with attached peers (their device-initiated halo stores
+    // live in the byte kernel: those sweeps run it on the byte state)
+    if (ctx->kernel == PCA_KERNEL_PACKED && n > 0 && !(small && n >= 2) && !ctx->p2p)
+        return sweep_packed_run(ctx, n);
     for (int32_t i = 0; i < n; ++i) {
         const int64_t t = ctx->t;
         if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
@@ -1523,7 +1565,7 @@ static pca_status sweep_direct(pca_ctx* ctx, int32_t n) {
         auto launch_rows = [&](int rlo, int rhi, cudaStream_t s) -> int {
             ctx->launches++;
             ctx->sweep_launches++;
-            if (ctx->kernel == PCA_KERNEL_BINARY) {
+            if (ctx->kernel == PCA_KERNEL_BINARY || ctx->kernel == PCA_KERNEL_PACKED) {
                 ctx->bin.c.rlo = rlo;
                 ctx->bin.c.rhi = rhi;
                 return launch_sweep_binary(ctx->bin, ctx->cfg.batch, ctx->rows_per_thread, s);

@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
     const Geometry& G = p.c.geo;
     const int seg = blockIdx.x;
     const int chain = blockIdx.z;
-    const int rbeg = blockIdx.y * R;
-    const int rend = min(rbeg + R, G.rows);
+    const int rbeg = p.c.rlo + blockIdx.y * R;
+    const int rend = min(rbeg + R, p.c.rhi);
     if (rbeg >= rend) return;
     const int nitems = (rend - rbeg + 3) >> 1;  // item i: x rows rbeg-1+2i, rbeg+2i; g rows rbeg+2i-2, +1
     const int col0 = 512 * seg;
@@ -321,9 +321,11 @@ int launch_p(const PackedSweepParams& p, int batch, cudaStream_t s) {
     const Geometry& G = p.c.geo;
     const long long segs = G.W / 512 + ((G.W % 512) ? 1 : 0);
     const long long target = (long long)li.sms * li.occ;
-    long long R = ((long long)G.rows * segs * batch + target - 1) / target;
+    const int nr = p.c.rhi - p.c.rlo;
+    if (nr <= 0) return 0;
+    long long R = ((long long)nr * segs * batch + target - 1) / target;
     if (R < 2) R = 2;
-    const int nrb = (int)((G.rows + R - 1) / R);
+    const int nrb = (int)((nr + R - 1) / R);
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((unsigned)segs, nrb, batch);
     sweep_packed_kernel<NB, PER, NOCOUNT><<<grid, 32, P_SMEM, s>>>(p, (int)R);
@@ -351,13 +353,15 @@ __global__ void to_packed_kernel(Geometry G, const uint8_t* __restrict__ xb, uin
 }
 
 __global__ void from_packed_kernel(Geometry G, const uint8_t* __restrict__ xp, int pp, long long pchain,
-                                   uint8_t* __restrict__ xb) {
+                                   uint8_t* __restrict__ xb, int halo_up, int halo_dn) {
     const int chain = blockIdx.z;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;  // padded row index
     const int nch = G.W >> 4;
     if (k >= nch) return;
-    if (!G.periodic && (j < HALO || j >= G.rows + HALO)) return;  // free: sentinel halo rows stay
+    // halo rows: written where a neighbour's rows live there (a torus, or a strip's neighbour);
+    // a free boundary's outer halo rows keep the sentinel
+    if ((j < HALO && !halo_up) || (j >= G.rows + HALO && !halo_dn)) return;
     const uint32_t b16 = *reinterpret_cast<const uint16_t*>(xp + chain * pchain + (long long)j * pp + 16 + 2 * k);
     const uint4 v = make_uint4(spread4(b16 & 0xFu), spread4((b16 >> 4) & 0xFu), spread4((b16 >> 8) & 0xFu),
                                spread4((b16 >> 12) & 0xFu));
@@ -438,10 +442,10 @@ int launch_state_to_packed(const Geometry& G, const uint8_t* xb, uint8_t* xp, in
 }
 
 int launch_state_from_packed(const Geometry& G, const uint8_t* xp, int pp, long long pchain, uint8_t* xb,
-                             int batch, void* stream) {
+                             int batch, void* stream, int halo_up, int halo_dn) {
     const int nch = G.W >> 4;
     dim3 grid((nch + 127) / 128, G.rows + 2 * HALO, batch);
-    from_packed_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(G, xp, pp, pchain, xb);
+    from_packed_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(G, xp, pp, pchain, xb, halo_up, halo_dn);
     return (int)cudaGetLastError();
 }
 

@@ -96,7 +96,7 @@ def test_packed_full_size_8192(cuda_device):
 
 def test_packed_kernel_rejects_ineligible_configs(cuda_device):
     for kw in (dict(height=64, width=500, levels=2), dict(height=64, width=512, levels=3),
-               dict(height=64, width=512, levels=2, row0=0, rows=32)):
+               dict(height=2, width=512, levels=2)):
         with pytest.raises(P.PcaError):
             P.pca_workspace_bytes(P.make_config(kw.pop("height"), kw.pop("width"), kw.pop("levels"),
                                                 kernel=P.KERNEL_PACKED, **kw))
@@ -118,3 +118,93 @@ def test_packed_count_deltas_fold_across_long_runs(cuda_device):
         assert np.array_equal(a.counts(), b.counts())
     assert a.pca_get_stats().counted_sweeps == 900
     assert np.array_equal(a.estimate(P.EST_MPM), b.estimate(P.EST_MPM))
+
+
+def _loopback_exchange(strips, periodic):
+    """Copy every strip's 2-row edges into its neighbours' halo rows, chain by chain (the caller's
+    exchange of a strip context without NCCL or peers, pca_halo_ptrs)."""
+    import torch
+
+    from test_gpu_parity import _cudart_memcpy
+
+    copy = _cudart_memcpy()
+    torch.cuda.synchronize()
+    hs = [s.pca_halo_ptrs() for s in strips]
+    n = len(strips)
+    for b in range(strips[0].cfg.batch):
+        for i in range(n):
+            up, dn = i - 1, i + 1
+            if periodic:
+                up, dn = up % n, dn % n
+            o = b * hs[i].chain_stride
+            if 0 <= up < n:
+                copy(hs[i].recv_top + o, hs[up].send_bottom + b * hs[up].chain_stride, hs[i].row_bytes)
+            if 0 <= dn < n:
+                copy(hs[i].recv_bottom + o, hs[dn].send_top + b * hs[dn].chain_stride, hs[i].row_bytes)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+@pytest.mark.parametrize("nb", [8, 4])
+def test_packed_row_strips_loopback(cuda_device, periodic, nb):
+    """Row strips on the packed kernel: each sweep is the strip's edge rows and its
+    interior as separate row ranges of the packed kernel, unpacked with the neighbours' halo rows;
+    strips of 2 rows (one launch), 3 rows and more, batch of 2 chains, exchanged by the caller
+    after every sweep, reproduce the unsharded packed chain and the oracle's chain bit for bit."""
+    H, W, B = 64, 1024, 2
+    truth = np.stack([synth.smooth_labels(H, W, 2, seed=30 + b) for b in range(B)])
+    g = np.stack([synth.degrade(truth[b], 2, 0.4, seed=40 + b) for b in range(B)])
+    base = dict(batch=B, neighborhood=nb, periodic=periodic, sigma=0.4, seed=13, mpm_burn_in=3,
+                beta_period=4, kernel=P.KERNEL_PACKED)
+    full = make_ctx(P.make_config(H, W, 2, **base), g)
+    bounds = [0, 2, 5, 26, 64]
+    strips = [make_ctx(P.make_config(H, W, 2, row0=bounds[i], rows=bounds[i + 1] - bounds[i], **base),
+                       np.ascontiguousarray(g[:, bounds[i]:bounds[i + 1]])) for i in range(len(bounds) - 1)]
+    for s in strips:
+        assert s.pca_get_stats().kernel == P.KERNEL_PACKED
+    _loopback_exchange(strips, periodic)
+    n = 9
+    for _ in range(n):
+        for s in strips:
+            s.pca_sweep(1)
+        _loopback_exchange(strips, periodic)
+    full.pca_sweep(n)
+    got = np.concatenate([s.state() for s in strips], axis=1)
+    assert np.array_equal(got, full.state())
+    gc = np.concatenate([s.counts() for s in strips], axis=-2)
+    assert np.array_equal(gc, full.counts())
+    for ch in range(B):
+        x_o, cnt_o = orc.pca_run(oracle_model(full.cfg), g[ch], g[ch], n, 1.25, 0.25, 4, 13, chain=ch,
+                                 burn_in=3)
+        assert np.array_equal(got[ch], x_o)
+        assert np.array_equal(gc[ch], cnt_o[1].astype(np.uint16))
+    # 3 launches per sweep on strips of >= 3 rows (edges, interior), 1 on the 2-row strip
+    assert strips[0].pca_get_stats().sweep_launches == n
+    assert strips[1].pca_get_stats().sweep_launches == 3 * n
+    for s in strips:
+        s.pca_destroy()
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_packed_strips_attached_to_peers_run_the_byte_kernel(cuda_device, periodic):
+    """A packed-eligible strip with device-initiated peers sweeps the byte state with the binary
+    kernel (the peer stores live there): still the unsharded chain bit for bit."""
+    import torch
+
+    from test_gpu_peers import _attach, _strips
+
+    H, W = 40, 512
+    g = synth.degrade(synth.smooth_labels(H, W, 2, 3), 2, 0.4, 4)[None]
+    base = dict(neighborhood=8, periodic=periodic, sigma=0.4, seed=21, mpm_burn_in=2)
+    full = P.PcaContext(P.make_config(H, W, 2, **base), g)
+    strips = _strips(H, W, 2, [0, 13, 40], base, g, torch.cuda.Stream())
+    assert strips[0].pca_get_stats().kernel == P.KERNEL_PACKED
+    _attach(strips, periodic)
+    for _ in range(7):
+        for s in strips:
+            s.pca_sweep(1)
+    full.pca_sweep(7)
+    assert np.array_equal(np.concatenate([s.state() for s in strips], axis=1), full.state())
+    assert np.array_equal(np.concatenate([s.counts() for s in strips], axis=-2), full.counts())
+    for s in strips:
+        s.pca_destroy()
