@@ -227,6 +227,8 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
     const uint8_t* gcol = p.c.g + chain * G.gchain + XOFF + c0;
     const uint32_t hmul = p.tab_magic;
     const int hsh = 32 - p.tab_hbits;
+    // the row-independent Philox prefix of the quad's counter (qd, row, t, tag|chain)
+    const PhiloxPre ppre = philox_pre((uint32_t)qd, t, tagchain, p.c.keys);
 
     auto load_row = [&](const uint8_t* xr, uint32_t (&w)[3]) {
         if (COH) {
@@ -276,7 +278,7 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
         gp += G.gpitch;
         const int grow = G.row0 + r;
         uint4 rnd = make_uint4(0, 0, 0, 0);
-        if (act) rnd = philox4x32_10(make_uint4((uint32_t)qd, (uint32_t)grow, t, tagchain), p.c.keys);
+        if (act) rnd = philox_row(ppre, (uint32_t)grow, p.c.keys);
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
         // ---- neighbour histograms, one 32-bit word of nibbles per site ----
         uint32_t h[4];
@@ -362,31 +364,20 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
             }
             // ---- fused MPM counts of the table-decided sites (queued ones: at the drain) ----
             if (count_enable) {
-                uint32_t rem = 0x01010101u & ~((rare * 0x00204081u) & 0x01010101u);
-                const uint32_t k0 = outw & 0xFFu;
-                if (nvalid == 4 && rem == 0x01010101u && outw == k0 * 0x01010101u) {
-                    // the common case: one label for the whole quad, one reduction
-                    atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)k0 * G.cplane),
-                              0x0001000100010001ull);
-                } else if (nvalid == 4) {
-                    while (rem) {
-                        const uint32_t k = __byte_perm(outw, 0u, 0x4440u + ((__ffs(rem) - 1) >> 3));
-                        const uint32_t e = outw ^ (k * 0x01010101u);
-                        const uint32_t nz = (((e & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | e) & 0x80808080u;
-                        const uint32_t eq = (~nz >> 7) & rem;
-                        const unsigned long long inc =
-                            (unsigned long long)__byte_perm(eq, 0u, 0x4140) |
-                            ((unsigned long long)__byte_perm(eq, 0u, 0x4342) << 32);
-                        atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)k * G.cplane), inc);
-                        rem &= ~eq;
-                    }
-                } else {
-                    for (int b = 0; b < nvalid; ++b)
-                        if ((rem >> (8 * b)) & 1u) {
-                            const int w = (int)((outw >> (8 * b)) & 0xFFu);
-                            atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)w * G.cplane),
-                                      1ull << (16 * b));
-                        }
+                // one reduction per distinct label of the quad's valid table-decided sites (a
+                // uniform quad, the common case, is the loop's single iteration: no separate path,
+                // so a warp with mixed quads does not run both); byte b of rem/eq: site b
+                uint32_t rem = ((vmask & ~rare) * 0x00204081u) & 0x01010101u;
+                while (rem) {
+                    const uint32_t k = __byte_perm(outw, 0u, 0x4440u + ((__ffs(rem) - 1) >> 3));
+                    const uint32_t e = outw ^ (k * 0x01010101u);
+                    const uint32_t nz = (((e & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | e) & 0x80808080u;
+                    const uint32_t eq = (~nz >> 7) & rem;
+                    const unsigned long long inc =
+                        (unsigned long long)__byte_perm(eq, 0u, 0x4140) |
+                        ((unsigned long long)__byte_perm(eq, 0u, 0x4342) << 32);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)k * G.cplane), inc);
+                    rem &= ~eq;
                 }
             }
         }
