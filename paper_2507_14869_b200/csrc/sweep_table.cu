@@ -278,7 +278,7 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
         gp += G.gpitch;
         const int grow = G.row0 + r;
         uint4 rnd = make_uint4(0, 0, 0, 0);
-        if (act) rnd = philox_row(ppre, (uint32_t)grow, p.c.keys);
+        if (act) rnd = philox_row<true>(ppre, (uint32_t)grow, p.c.keys);
         const uint32_t rr[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
         // ---- neighbour histograms, one 32-bit word of nibbles per site ----
         uint32_t h[4];
