@@ -188,6 +188,15 @@ __device__ __forceinline__ void drain(const GeneralSweepParams& p, uint32_t qoff
         const uint8_t* rec = tab_smem_buf + qoff + i * (uint32_t)sizeof(Rec);
         const uint4 tail = *reinterpret_cast<const uint4*>(rec + 32);  // gw, xw, rc0, mask
         const int row = (int)(tail.z >> 16), c0 = (int)(tail.z & 0xFFFFu);
+        // the record's row bases, once per record; a quad away from the torus column pads, the
+        // wrapped halo rows and the peers' rows stores its bytes plainly (put_site otherwise)
+        uint8_t* xq = x_out + chain * G.xchain + (long long)(row + HALO) * G.xpitch + XOFF + c0;
+        unsigned long long* cq = reinterpret_cast<unsigned long long*>(
+            p.c.counts + chain * G.cchain + (long long)row * G.cpitch + c0);
+        const bool special =
+            (G.periodic && (c0 < 16 || c0 + 4 > G.W - 16 ||
+                            (G.self_halo_rows && (row < HALO || row >= G.rows - HALO)))) ||
+            (PEERS && (row == 0 || row == G.rows - 1));
         for (uint32_t m = tail.w; m != 0u; m &= m - 1u) {
             const int b = __ffs(m) - 1;
             const uint32_t h = *reinterpret_cast<const uint32_t*>(rec + 4 * b);
@@ -196,12 +205,9 @@ __device__ __forceinline__ void drain(const GeneralSweepParams& p, uint32_t qoff
             const int xi = (int)__byte_perm(tail.y, 0u, 0x4440u + b);
             const int w = decide_hist_fp64<L>(h, gi, xi, r);
             PCA_DCHECK(w >= 0 && w < L && gi < L && xi < L && row >= 0 && row < G.rows && c0 + b < G.W);
-            put_site<PEERS>(p, x_out, chain, row, c0 + b, (uint8_t)w);
-            if (count_enable) {
-                uint16_t* cw = p.c.counts + chain * G.cchain + (long long)w * G.cplane +
-                               (long long)row * G.cpitch + c0;
-                atomicAdd(reinterpret_cast<unsigned long long*>(cw), 1ull << (16 * b));
-            }
+            if (special) put_site<PEERS>(p, x_out, chain, row, c0 + b, (uint8_t)w);
+            else xq[b] = (uint8_t)w;
+            if (count_enable) atomicAdd(cq + (long long)w * (G.cplane >> 2), 1ull << (16 * b));
         }
     }
     __syncwarp();  // the queue is free again
