@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--graphs", type=int, default=None,
                     help="capture each pca_sweep(S) run into a CUDA graph and replay it every step "
                          "(pca_config.graphs); default: on for N = 1, off for row strips (N > 1)")
+    ap.add_argument("--variant-only", default=None, choices=["c5", "c3_l5"],
+                    help="run ONE run of one multi-level variant and exit (no line): the target "
+                         "of the all-launch instruction capture (tools/ncu_variant_summary.py)")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU only (gloo, stub context): exercise the multi-rank orchestration "
                          "(self-launch, strip partition, unique-id broadcast, max-over-ranks "
@@ -209,7 +212,7 @@ def load_instr_per_su(tag):
     return None, None
 
 
-def run_variants(P, torch, dev, stream):
+def run_variants(P, torch, dev, stream, only=None, runs=2):
     """The paper's multi-level workloads on one GPU: C5 per GPU (one 512^2 truth,
     l = 5, sigma = 0.25, x 128 noise seeds = 128 chains, Moore-8, free boundary, the paper's
     protocol: 1000 sweeps, beta 1.25 + 0.25 / 250, MPM burn-in 750) and C3 at l = 5 (8192^2
@@ -230,6 +233,8 @@ def run_variants(P, torch, dev, stream):
          dict(sigma=0.25, periodic=True, beta0=1.5, beta_step=0.0, mpm_burn_in=0)),
     ]
     for tag, name, H, W, B, S, kw in cases:
+        if only is not None and tag != only:
+            continue
         if B > 1:
             truth1 = synth.smooth_labels(H, W, 5, seed=7)
             truth = np.repeat(truth1[None], B, 0)
@@ -242,7 +247,7 @@ def run_variants(P, torch, dev, stream):
         mpm = torch.empty_like(gd)
         ctx = P.PcaContext(P.make_config(H, W, 5, batch=B, seed=11, **kw), gd, stream=stream)
         ms = []
-        for _ in range(2):
+        for _ in range(runs):
             ctx.pca_reset(None, None)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -697,6 +702,16 @@ def main():
         return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.variant_only:
+        import torch
+
+        import paper_2507_14869_b200 as P
+
+        dev = torch.device("cuda", 0)
+        stream = torch.cuda.Stream(device=dev)
+        out = run_variants(P, torch, dev, stream, only=args.variant_only, runs=1)
+        print(json.dumps({k: {"us_per_sweep": v["us_per_sweep"], "sweeps": v["sweeps"]} for k, v in out.items()}))
+        return 0
     return run_ours(args)
 
 
