@@ -91,7 +91,7 @@ enum {
                             /* per-site neighbour histograms; integer thresholds for every     */
                             /* interior site with <= 2 distinct neighbour labels (one table    */
                             /* row per histogram, g, x), fp64 weights for the others           */
-    PCA_KERNEL_PACKED = 4   /* levels == 2, whole lattice, width % 512 == 0: the state and g   */
+    PCA_KERNEL_PACKED = 4   /* levels == 2, width % 512 == 0 (whole lattice or row strip): g and the state */
                             /* bit-packed in HBM (1 bit per site) during runs of sweeps; the   */
                             /* binary kernel's decisions (same chain)                          */
 };

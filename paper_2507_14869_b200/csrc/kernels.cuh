@@ -149,6 +149,12 @@ struct GeneralSweepParams {
     const uint8_t* tab;
     uint32_t tab_bytes, tab_slots, tab_thr, tab_magic;
     int tab_hbits;
+    // the table kernel's MPM counts as uint8 deltas [batch][levels][rows][cpitch] (chain stride
+    // tdc_chain, plane stride tdc_plane bytes), folded into the uint16 counts by the runtime at
+    // most every 255 counted sweeps and at the end of every pca_sweep call (launch_fold_counts
+    // per plane); nullptr: the table kernel adds into the uint16 counts
+    uint8_t* tdc;
+    long long tdc_chain, tdc_plane;
 };
 constexpr int TAB_OFF_W0 = 80;
 

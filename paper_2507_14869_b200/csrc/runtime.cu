@@ -337,6 +337,8 @@ Layout make_layout(const pca_config* c) {
         L.xp_bytes = B * (R + 2 * HALO) * (size_t)L.pp;
         L.gp_bytes = B * R * (size_t)L.gpp;
         L.dc_bytes = B * R * (size_t)L.cpitch;  // uint8 count deltas
+    } else if (table_eligible(c) && (c->kernel == PCA_KERNEL_AUTO || c->kernel == PCA_KERNEL_TABLE)) {
+        L.dc_bytes = B * (size_t)c->levels * R * (size_t)L.cpitch;  // the table kernel's uint8 deltas
     }
     L.off_xp = o; o = align256(o + 2 * align256(L.xp_bytes));
     L.off_gp = o; o = align256(o + L.gp_bytes);
@@ -386,6 +388,7 @@ struct pca_ctx {
     int prev_valid = 0;  // x[cur ^ 1] holds x_{t-1} (after a PCA or double-buffered Gibbs sweep)
     int64_t tab_stage = -1;
     int64_t gtab_stage = -1;
+    int tdc_pending = 0;  // counted table-kernel sweeps in the uint8 count deltas (<= 255)
     GibbsSweepParams gib;
     GibbsBinParams gbin;
     uint32_t bthr_host[THR_ENTRIES];  // binary thresholds of the current stage (host copy)
@@ -1288,7 +1291,12 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
         ctx->pk.dchain = (long long)L.rows * L.cpitch;
     }
     ctx->gen.tab = nullptr;
+    ctx->gen.tdc = nullptr;
+    if (ctx->kernel == PCA_KERNEL_TABLE && L.dc_bytes == 0) ctx->kernel = PCA_KERNEL_GENERAL;  // (not expected)
     if (ctx->kernel == PCA_KERNEL_TABLE) {
+        ctx->gen.tdc = ctx->ws + L.off_dc;
+        ctx->gen.tdc_plane = (long long)L.rows * L.cpitch;
+        ctx->gen.tdc_chain = (long long)cfg->levels * ctx->gen.tdc_plane;
         const TabKeys& K = tab_keys(cfg->levels, cfg->neighborhood);
         if (K.ok) {
             ctx->gen.tab = ctx->ws + L.off_tab;
@@ -1350,10 +1358,13 @@ pca_status pca_init(pca_ctx** out, const pca_config* cfg, void* workspace, size_
     if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "upload dtab"));
     e = cudaMemsetAsync(ctx->pflags, 0, 2 * sizeof(uint32_t), ctx->stream);
     if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "clear peer flags"));
-    if (ctx->xp[0]) {  // packed pads and (free boundary) halo rows stay zero; deltas start at 0
+    if (ctx->xp[0]) {  // packed pads and (free boundary) halo rows stay zero
         e = cudaMemsetAsync(ctx->xp[0], 0, 2 * align256(L.xp_bytes), ctx->stream);
-        if (e == cudaSuccess) e = cudaMemsetAsync(ctx->pk.dcounts, 0, L.dc_bytes, ctx->stream);
         if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "clear packed state"));
+    }
+    if (L.dc_bytes) {  // count deltas (packed or table kernel) start at 0
+        e = cudaMemsetAsync(ctx->ws + L.off_dc, 0, L.dc_bytes, ctx->stream);
+        if (e != cudaSuccess) return bail(cuda_fail(nullptr, e, "clear count deltas"));
     }
     st = do_reset(ctx, g, x0);
     if (st != PCA_OK) return bail(st);
@@ -1453,7 +1464,28 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     return sweep_direct(ctx, n);
 }
 
+// the table kernel's uint8 count deltas into the uint16 counts, plane by plane (deltas = 0)
+static pca_status fold_table_deltas(pca_ctx* ctx) {
+    if (ctx->tdc_pending == 0) return PCA_OK;
+    const int planes = ctx->cfg.levels;
+    for (int k = 0; k < planes; ++k)
+        LAUNCH(ctx, launch_fold_counts(ctx->geo, ctx->counts + (size_t)k * ctx->geo.cplane,
+                                       ctx->gen.tdc + (size_t)k * ctx->gen.tdc_plane, ctx->gen.tdc_chain,
+                                       ctx->cfg.batch, ctx->stream));
+    ctx->tdc_pending = 0;
+    return PCA_OK;
+}
+
+static pca_status sweep_direct_run(pca_ctx* ctx, int32_t n);
+
+// every call leaves the canonical uint16 counts complete (the table kernel's deltas folded)
 static pca_status sweep_direct(pca_ctx* ctx, int32_t n) {
+    const pca_status st = sweep_direct_run(ctx, n);
+    if (st != PCA_OK) return st;
+    return fold_table_deltas(ctx);
+}
+
+static pca_status sweep_direct_run(pca_ctx* ctx, int32_t n) {
     pca_status st = PCA_OK;
     const bool strip = ctx->lay.rows < ctx->cfg.height;
     // two sweeps per HBM pass (sweep_binary2.cu, opt-in): levels == 2, W % 16 == 0; on a row
@@ -1561,6 +1593,13 @@ static pca_status sweep_direct(pca_ctx* ctx, int32_t n) {
             return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
         fill_common(ctx, ctx->bin.c, t, count);
         fill_common(ctx, ctx->gen.c, t, count);
+        // a counted sweep on the table kernel adds into the uint8 deltas: fold before a byte
+        // could overflow
+        const bool tab_counts = count && ctx->kernel == PCA_KERNEL_TABLE && ctx->gen.tab != nullptr;
+        if (tab_counts && ctx->tdc_pending >= 255) {
+            st = fold_table_deltas(ctx);
+            if (st != PCA_OK) return st;
+        }
         // one sweep kernel over local rows [rlo, rhi) on stream s
         auto launch_rows = [&](int rlo, int rhi, cudaStream_t s) -> int {
             ctx->launches++;
@@ -1635,6 +1674,7 @@ static pca_status sweep_direct(pca_ctx* ctx, int32_t n) {
         ctx->prev_valid = 1;
         ctx->t = t + 1;
         ctx->counted += count;
+        ctx->tdc_pending += tab_counts ? 1 : 0;
     }
     return PCA_OK;
 }

@@ -393,7 +393,7 @@ __global__ void fold_counts_kernel(Geometry G, uint16_t* __restrict__ counts, ui
     const int chain = blockIdx.z;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = blockIdx.y;
-    if (k >= (G.W >> 4)) return;
+    if (k >= ((G.W + 15) >> 4)) return;  // whole 16-column chunks (a ragged tail adds zeros)
     uint4* dp = reinterpret_cast<uint4*>(delta + chain * dchain + (long long)r * G.cpitch + 16 * k);
     const uint4 d = *dp;
     uint4* cp = reinterpret_cast<uint4*>(counts + chain * G.cchain + (long long)r * G.cpitch + 16 * k);
@@ -412,7 +412,7 @@ __global__ void fold_counts_kernel(Geometry G, uint16_t* __restrict__ counts, ui
 
 int launch_fold_counts(const Geometry& G, uint16_t* counts, uint8_t* delta, long long dchain, int batch,
                        void* stream) {
-    const int nch = G.W >> 4;
+    const int nch = (G.W + 15) >> 4;
     dim3 grid((nch + 127) / 128, G.rows, batch);
     fold_counts_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(G, counts, delta, dchain);
     return (int)cudaGetLastError();

@@ -28,6 +28,11 @@
 // rows / peer rows) and adds its MPM count after a __syncwarp, which orders the two in the
 // warp.
 //
+// MPM counts: uint8 deltas per level plane (GeneralSweepParams.tdc), one 32-bit reduction per
+// distinct label of a quad with the per-site byte increments (half the count bytes of the
+// uint16 planes, no 64-bit increment assembly); the runtime folds them into the uint16 counts
+// at most every 255 counted sweeps and at the end of every pca_sweep call.
+//
 // Data movement: a thread owns a quad of 4 sites (one Philox4x32-10 call) and walks a run of
 // rows with a rolling 3-row window of one-hot words (the next x row and g row prefetched one
 // row ahead, as in sweep_general.cu); the table blob reaches each block's shared memory with
@@ -191,8 +196,7 @@ __device__ __forceinline__ void drain(const GeneralSweepParams& p, uint32_t qoff
         // the record's row bases, once per record; a quad away from the torus column pads, the
         // wrapped halo rows and the peers' rows stores its bytes plainly (put_site otherwise)
         uint8_t* xq = x_out + chain * G.xchain + (long long)(row + HALO) * G.xpitch + XOFF + c0;
-        unsigned long long* cq = reinterpret_cast<unsigned long long*>(
-            p.c.counts + chain * G.cchain + (long long)row * G.cpitch + c0);
+        unsigned* dq = reinterpret_cast<unsigned*>(p.tdc + chain * p.tdc_chain + (long long)row * G.cpitch + c0);
         const bool special =
             (G.periodic && (c0 < 16 || c0 + 4 > G.W - 16 ||
                             (G.self_halo_rows && (row < HALO || row >= G.rows - HALO)))) ||
@@ -207,7 +211,7 @@ __device__ __forceinline__ void drain(const GeneralSweepParams& p, uint32_t qoff
             PCA_DCHECK(w >= 0 && w < L && gi < L && xi < L && row >= 0 && row < G.rows && c0 + b < G.W);
             if (special) put_site<PEERS>(p, x_out, chain, row, c0 + b, (uint8_t)w);
             else xq[b] = (uint8_t)w;
-            if (count_enable) atomicAdd(cq + (long long)w * (G.cplane >> 2), 1ull << (16 * b));
+            if (count_enable) atomicAdd(dq + (long long)w * (p.tdc_plane >> 2), 1u << (8 * b));
         }
     }
     __syncwarp();  // the queue is free again
@@ -266,7 +270,9 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
     xp += 3 * G.xpitch;
     gp += G.gpitch;
     uint8_t* op = x_out + chain * G.xchain + (long long)(rbeg + HALO) * G.xpitch + XOFF + c0;
-    uint16_t* cp = p.c.counts + chain * G.cchain + (long long)rbeg * G.cpitch + c0;
+    // the MPM count deltas of this quad column (uint8 [levels] planes; sweep_table.cu header)
+    PCA_DCHECK(!count_enable || p.tdc != nullptr);
+    uint8_t* dp = p.tdc + chain * p.tdc_chain + (long long)rbeg * G.cpitch + c0;
     int qn = 0;  // pending records of the warp (warp-uniform)
 
     for (int it = 0; it < iters; ++it) {
@@ -373,16 +379,14 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
                 // one reduction per distinct label of the quad's valid table-decided sites (a
                 // uniform quad, the common case, is the loop's single iteration: no separate path,
                 // so a warp with mixed quads does not run both); byte b of rem/eq: site b
+                // (byte b of rem / eq: site b; the uint8 deltas take eq as the increment)
                 uint32_t rem = ((vmask & ~rare) * 0x00204081u) & 0x01010101u;
                 while (rem) {
                     const uint32_t k = __byte_perm(outw, 0u, 0x4440u + ((__ffs(rem) - 1) >> 3));
                     const uint32_t e = outw ^ (k * 0x01010101u);
                     const uint32_t nz = (((e & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | e) & 0x80808080u;
                     const uint32_t eq = (~nz >> 7) & rem;
-                    const unsigned long long inc =
-                        (unsigned long long)__byte_perm(eq, 0u, 0x4140) |
-                        ((unsigned long long)__byte_perm(eq, 0u, 0x4342) << 32);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(cp + (long long)k * G.cplane), inc);
+                    atomicAdd(reinterpret_cast<unsigned*>(dp + (long long)k * p.tdc_plane), eq);
                     rem &= ~eq;
                 }
             }
@@ -398,7 +402,7 @@ __device__ __forceinline__ void tab_rows(const GeneralSweepParams& p, const TabS
         }
         xmid = xdn;
         op += G.xpitch;
-        cp += G.cpitch;
+        dp += G.cpitch;
     }
 }
 

@@ -79,6 +79,34 @@ def test_table_kernel_lockstep_and_agreement(cuda_device, levels, nb, periodic, 
     assert np.array_equal(a.counts()[0], cnt_o.astype(np.uint16))
 
 
+@pytest.mark.parametrize("levels,nb,periodic", [(5, 8, False), (3, 4, True), (4, 8, True)])
+def test_table_kernel_count_deltas_fold_across_long_runs(cuda_device, levels, nb, periodic):
+    """The table kernel's uint8 count deltas (one plane per level) are folded into the uint16
+    counts before 255 counted sweeps accumulate and at the end of every call: 600 counted
+    sweeps in one call, 300 in another, then single sweeps, on a context above the multi-sweep
+    threshold with a ragged width (W % 16 != 0: the fold covers the last partial chunk), equal
+    the general kernel's uint16 counts, and every estimate that reads them agrees."""
+    H, W, B = 300, 517, 2
+    truth = np.stack([synth.smooth_labels(H, W, levels, seed=40 + b) for b in range(B)])
+    g = np.stack([synth.degrade(truth[b], levels, 0.3, seed=50 + b) for b in range(B)])
+    kw = dict(batch=B, neighborhood=nb, periodic=periodic, sigma=0.3, beta0=1.3, beta_step=0.0, seed=9,
+              mpm_burn_in=0)
+    a = make_ctx(P.make_config(H, W, levels, **kw), g)
+    b = make_ctx(P.make_config(H, W, levels, kernel=P.KERNEL_GENERAL, **kw), g)
+    assert a.pca_get_stats().kernel == P.KERNEL_TABLE
+    for n in (600, 300, 1, 1, 1):
+        for c in (a, b):
+            c.pca_sweep(n)
+        assert np.array_equal(a.state(), b.state())
+        assert np.array_equal(a.counts(), b.counts())
+    assert a.pca_get_stats().counted_sweeps == 903
+    for est in (P.EST_MPM, P.EST_CM):
+        assert np.array_equal(a.estimate(est), b.estimate(est))
+    pa, sa = a.pca_finalize(truth, np.zeros_like(truth))
+    pb, sb = b.pca_finalize(truth, np.zeros_like(truth))
+    assert np.array_equal(pa, pb) and np.array_equal(sa, sb)
+
+
 @pytest.mark.parametrize("q", [0.0, 0.51, 3.0, 1e6])
 def test_lockstep_inertia_extremes(cuda_device, q):
     cfg = P.make_config(48, 80, 2, neighborhood=8, periodic=False, q=q, sigma=0.5, seed=7)
