@@ -59,8 +59,12 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 #ifndef PCA_TAB_THR_GLOBAL
 #define PCA_TAB_THR_GLOBAL 0
 #endif
+// waves of resident blocks the row runs are sized for (measured, us per sweep at C5 t = 700 /
+// t = 900 / 8192^2 l = 5 t = 0 / t = 1000: 1 150/190/428/302, 2 111/139/400/263, 3 107/134/
+// 402/263, 4 101/127/392/259, 5 105/130/393/261, 6 104/129/392/264, 8 104/130/397/266, 12 108/
+// 132/398/269)
 #ifndef PCA_TAB_WAVES
-#define PCA_TAB_WAVES 2
+#define PCA_TAB_WAVES 4
 #endif
 constexpr int TAB_MAX_BYTES = 40 * 1024;  // blob limit (3..5 levels: <= 40 KB)
 
