@@ -58,6 +58,9 @@ namespace {
 // rows + 14 CTAs (round-2 first version) 76.3 / 70.7 / 82.4
 #define PCA_P_PRE 1
 #endif
+#ifndef PCA_P_WAVES
+#define PCA_P_WAVES 4  // waves of resident CTAs the row runs are sized for
+#endif
 constexpr int P_XROW = 96;                  // packed x bytes staged per row: cols [c0-128, c0+640)
 constexpr int P_GROW = 64;                  // packed g bytes per row: cols [c0, c0+512)
 constexpr int P_STAGE = 2 * P_XROW + 2 * P_GROW;  // 320
@@ -320,7 +323,7 @@ int launch_p(const PackedSweepParams& p, int batch, cudaStream_t s) {
     }
     const Geometry& G = p.c.geo;
     const long long segs = G.W / 512 + ((G.W % 512) ? 1 : 0);
-    const long long target = (long long)li.sms * li.occ;
+    const long long target = (long long)li.sms * li.occ * PCA_P_WAVES;
     const int nr = p.c.rhi - p.c.rlo;
     if (nr <= 0) return 0;
     long long R = ((long long)nr * segs * batch + target - 1) / target;
