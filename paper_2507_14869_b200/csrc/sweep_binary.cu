@@ -53,6 +53,10 @@ namespace {
 #ifndef PCA_T_RED
 #define PCA_T_RED 0
 #endif
+#ifndef PCA_B_WAVES
+#define PCA_B_WAVES 4  // waves of resident warps the row runs are sized for (8192^2 torus MPM on, us per
+                       // sweep: 1 wave 84.6, 2 84.2, 4 83.5; MPM off 71.7 / 70.6 / 70.9)
+#endif
 #ifndef PCA_B_PRE
 #define PCA_B_PRE 1  // the row-independent Philox prefix in registers (philox.cuh)
 #endif
@@ -511,7 +515,7 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
         // size R so the grid is about one full wave of resident warps: every warp walks one
         // contiguous run of rows with its pipeline primed once
         const long long segs = (G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
-        const long long target = (long long)sms * occ;
+        const long long target = (long long)sms * occ * PCA_B_WAVES;
         const long long work = (long long)(p.c.rhi - p.c.rlo) * segs * batch;
         R = (int)((work + target - 1) / target);
         if (R < 2) R = 2;
