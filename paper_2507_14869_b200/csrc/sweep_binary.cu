@@ -512,8 +512,8 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     }
     const int occ = li.occ, sms = li.sms;
     if (R <= 0) {
-        // size R so the grid is about one full wave of resident warps: every warp walks one
-        // contiguous run of rows with its pipeline primed once
+        // size R so the grid is PCA_B_WAVES waves of resident warps: every warp walks one
+        // contiguous run of rows with its pipeline primed once (several waves balance the tail)
         const long long segs = (G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
         const long long target = (long long)sms * occ * PCA_B_WAVES;
         const long long work = (long long)(p.c.rhi - p.c.rlo) * segs * batch;
