@@ -22,6 +22,11 @@
 #include "kernels.cuh"
 #include "tma_ring.cuh"
 
+#ifndef PCA_B2_WAVES
+#define PCA_B2_WAVES 1  // waves of resident warps the row runs are sized for (8192^2 torus, us
+                        // per sweep: 1 wave 100.5, 2 101.5, 4 105.5)
+#endif
+
 namespace pcab200 {
 namespace {
 
@@ -311,7 +316,7 @@ int launch_t(const Binary2SweepParams& p, int batch, int R, cudaStream_t s) {
     const int occ = li.occ, sms = li.sms;
     if (R <= 0) {
         const long long segs = (G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS;
-        const long long target = (long long)sms * occ;
+        const long long target = (long long)sms * occ * PCA_B2_WAVES;
         const long long work = (long long)(p.c.rhi - p.c.rlo) * segs * batch;
         R = (int)((work + target - 1) / target);
         if (R < 4) R = 4;

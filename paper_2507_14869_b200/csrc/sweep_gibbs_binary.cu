@@ -21,6 +21,11 @@
 #include "kernels.cuh"
 #include "tma_ring.cuh"
 
+#ifndef PCA_GB_WAVES
+#define PCA_GB_WAVES 4  // waves of resident warps the row runs are sized for (8192^2 torus Gibbs
+                        // sweep: 1 wave 135.2 us, 2 135.0, 4 126.9)
+#endif
+
 namespace pcab200 {
 namespace {
 
@@ -279,7 +284,7 @@ int launch_gb2(const GibbsBinParams& p, int batch, cudaStream_t s) {
     const int nproc = rfirst < p.c.rhi ? (p.c.rhi - rfirst + 1) / 2 : 0;
     if (nproc <= 0) return 0;
     const long long segs = (G.nchunks + SEG - 1) / SEG;
-    const long long target = (long long)sms * occ;
+    const long long target = (long long)sms * occ * PCA_GB_WAVES;
     long long R = ((long long)nproc * segs * batch + target - 1) / target;
     if (R < 1) R = 1;
     const long long nrb = (nproc + R - 1) / R;
