@@ -47,6 +47,10 @@ def main():
         ("c3 8192x8192 l2 moore torus mpm", P.make_config(8192, 8192, 2, periodic=True, sigma=0.5,
                                                            beta0=1.5, beta_step=0, mpm_burn_in=0),
          synth.degrade(synth.tiled_labels(8192, 8192, 2, 1), 2, 0.5, 2)[None], 50),
+        ("c3 8192x8192 l2 moore torus mpm, byte-state PCA kernel (the Gibbs kernel's data path)",
+         P.make_config(8192, 8192, 2, periodic=True, sigma=0.5, beta0=1.5, beta_step=0, mpm_burn_in=0,
+                       kernel=P.KERNEL_BINARY),
+         synth.degrade(synth.tiled_labels(8192, 8192, 2, 1), 2, 0.5, 2)[None], 50),
         ("c3 8192x8192 l5 moore torus mpm", P.make_config(8192, 8192, 5, periodic=True, sigma=0.25,
                                                            beta0=1.5, beta_step=0, mpm_burn_in=0),
          synth.degrade(synth.tiled_labels(8192, 8192, 5, 1), 5, 0.25, 2)[None], 10),
