@@ -268,8 +268,8 @@ pca_status validate(const pca_config* c) {
     }
     if (c->kernel < 0 || c->kernel > 4) return fail(PCA_EINVAL, "kernel must be 0..4");
     if (c->kernel == PCA_KERNEL_PACKED && !packed_eligible(c))
-        return fail(PCA_EUNSUPPORTED, "the packed kernel needs levels == 2, the whole lattice and "
-                                      "width %% 512 == 0");
+        return fail(PCA_EUNSUPPORTED, "the packed kernel needs levels == 2, width %% 512 == 0 and "
+                                      "height >= 3");
     if (c->kernel == PCA_KERNEL_TABLE && !table_eligible(c))
         return fail(PCA_EUNSUPPORTED, "the table kernel needs 3..%d levels, width and rows <= 65535",
                     TAB_MAX_LEVELS);
@@ -1132,15 +1132,22 @@ pca_status sweep_packed_run(pca_ctx* ctx, int32_t n) {
         }
         return PCA_OK;
     };
+    // a refused sweep (sweep index or counter limit) ends the run after the sweeps already
+    // done: their counts are folded and their state unpacked, as at the end of a full run
+    pca_status refused = PCA_OK;
+    int32_t done = 0;
     for (int32_t i = 0; i < n; ++i) {
         const int64_t t = ctx->t;
-        if (t >= (int64_t)0xFFFFFFFFLL) return fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
+        if (t >= (int64_t)0xFFFFFFFFLL) {
+            refused = fail(PCA_EUNSUPPORTED, "sweep index exceeds 2^32-1");
+            break;
+        }
         pca_status st = build_tables(ctx, t);
         if (st != PCA_OK) return st;
         const int count = (c.mpm_burn_in >= 0 && t >= c.mpm_burn_in) ? 1 : 0;
         if (count && ctx->counted + 1 > 65535) {
-            fold();
-            return fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+            refused = fail(PCA_EUNSUPPORTED, "more than 65535 counted sweeps overflow uint16 counts");
+            break;
         }
         fill_common(ctx, ctx->pk.c, t, count);
         ctx->pk.x_in = ctx->xp[pc];
@@ -1187,6 +1194,7 @@ pca_status sweep_packed_run(pca_ctx* ctx, int32_t n) {
         pc ^= 1;
         ctx->t = t + 1;
         ctx->counted += count;
+        ++done;
         pending += count;
         if (pending == 255) {
             st = fold();
@@ -1195,7 +1203,8 @@ pca_status sweep_packed_run(pca_ctx* ctx, int32_t n) {
     }
     pca_status st = fold();  // the canonical uint16 counts are complete again
     if (st != PCA_OK) return st;
-    const int cur = ctx->cur ^ (n & 1);
+    if (done == 0) return refused;  // nothing swept: the byte state is current
+    const int cur = ctx->cur ^ (done & 1);
     // the halo rows hold real rows where a neighbour is (a torus, or a strip's neighbouring
     // rank); a free boundary's outer halo rows keep the byte buffers' sentinel
     const int hu = c.periodic || c.row0 > 0, hd = c.periodic || c.row0 + ctx->lay.rows < c.height;
@@ -1207,8 +1216,11 @@ pca_status sweep_packed_run(pca_ctx* ctx, int32_t n) {
     ctx->prev_valid = 1;
     // a strip over NCCL: the byte state's 2-deep halos from the neighbours (the packed runs
     // exchanged 1-deep packed halos only); a caller-exchanged strip's caller does this
-    if (strip) return exchange(ctx, ctx->x[ctx->cur]);
-    return PCA_OK;
+    if (strip) {
+        st = exchange(ctx, ctx->x[ctx->cur]);
+        if (st != PCA_OK) return st;
+    }
+    return refused;
 }
 
 }  // namespace
@@ -1460,7 +1472,13 @@ pca_status pca_sweep(pca_ctx* ctx, int32_t n) {
     pca_status st = ready(ctx);
     if (st != PCA_OK) return st;
     if (n < 0) return fail(PCA_EINVAL, "n must be >= 0");
-    if (ctx->cfg.graphs && n > 0 && !ctx->p2p) return sweep_graph(ctx, n);
+    // a run that will be refused part-way (sweep index or counter limit) runs directly: its
+    // sweeps before the refusal execute and the host state matches them (a capture would be
+    // discarded with the host state already advanced)
+    const int64_t t0 = ctx->t, burn = ctx->cfg.mpm_burn_in;
+    const int64_t counted_n = burn < 0 ? 0 : std::max<int64_t>(0, t0 + n - std::max<int64_t>(t0, burn));
+    const bool refused = t0 + n > (int64_t)0xFFFFFFFFLL || ctx->counted + counted_n > 65535;
+    if (ctx->cfg.graphs && n > 0 && !ctx->p2p && !refused) return sweep_graph(ctx, n);
     return sweep_direct(ctx, n);
 }
 
@@ -1478,11 +1496,13 @@ static pca_status fold_table_deltas(pca_ctx* ctx) {
 
 static pca_status sweep_direct_run(pca_ctx* ctx, int32_t n);
 
-// every call leaves the canonical uint16 counts complete (the table kernel's deltas folded)
+// every call leaves the canonical uint16 counts complete (the table kernel's deltas folded),
+// also a call refused part-way (sweep index or counter limit) for the sweeps it did
 static pca_status sweep_direct(pca_ctx* ctx, int32_t n) {
     const pca_status st = sweep_direct_run(ctx, n);
-    if (st != PCA_OK) return st;
-    return fold_table_deltas(ctx);
+    if (st != PCA_OK && st != PCA_EUNSUPPORTED) return st;
+    const pca_status sf = fold_table_deltas(ctx);
+    return st != PCA_OK ? st : sf;
 }
 
 static pca_status sweep_direct_run(pca_ctx* ctx, int32_t n) {

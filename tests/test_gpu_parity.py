@@ -107,6 +107,36 @@ def test_table_kernel_count_deltas_fold_across_long_runs(cuda_device, levels, nb
     assert np.array_equal(pa, pb) and np.array_equal(sa, sb)
 
 
+@pytest.mark.parametrize("levels,W,kernel,graphs", [(2, 512, P.KERNEL_PACKED, 1), (2, 512, P.KERNEL_PACKED, 0),
+                                                   (5, 517, P.KERNEL_TABLE, 0), (2, 520, P.KERNEL_BINARY, 1)])
+def test_run_refused_at_the_counter_limit_keeps_a_consistent_state(cuda_device, levels, W, kernel, graphs):
+    """A run refused part-way (the 65535th counted sweep is the last a uint16 counter holds)
+    executes the sweeps before the refusal and leaves state, sweep index and counts consistent
+    with them -- on the packed kernel (its state is unpacked, its deltas folded), the table
+    kernel (deltas folded) and the byte kernel, with and without graph capture."""
+    H = 520  # above the multi-sweep threshold, so the per-kernel paths run
+    g = synth.degrade(synth.smooth_labels(H, W, levels, 3), levels, 0.4, 4)
+    kw = dict(neighborhood=8, periodic=True, sigma=0.4, seed=6, mpm_burn_in=0, kernel=kernel,
+              graphs=graphs if levels == 2 else 0)
+    a = make_ctx(P.make_config(H, W, levels, **kw), g)
+    ref = make_ctx(P.make_config(H, W, levels, **kw), g)
+    assert a.pca_get_stats().kernel == kernel
+    c0 = a.counts()
+    a.pca_write_counts(c0, 65530)
+    with pytest.raises(P.PcaError, match="65535"):
+        a.pca_sweep(12)
+    st = a.pca_get_stats()
+    assert st.sweeps_done == 5 and st.counted_sweeps == 65535
+    ref.pca_sweep(5)
+    assert np.array_equal(a.state(), ref.state())
+    assert np.array_equal(a.counts(), ref.counts())
+    assert np.array_equal(a.pca_changed_sites(), ref.pca_changed_sites())
+    with pytest.raises(P.PcaError, match="65535"):  # nothing left to count into
+        a.pca_sweep(1)
+    assert a.pca_get_stats().sweeps_done == 5
+    assert np.array_equal(a.state(), ref.state())
+
+
 @pytest.mark.parametrize("q", [0.0, 0.51, 3.0, 1e6])
 def test_lockstep_inertia_extremes(cuda_device, q):
     cfg = P.make_config(48, 80, 2, neighborhood=8, periodic=False, q=q, sigma=0.5, seed=7)
