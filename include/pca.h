@@ -214,7 +214,8 @@ pca_status pca_reset(pca_ctx* ctx, const uint8_t* g, const uint8_t* x0);
  * context owns a strip (rows < height) and NCCL is attached, each sweep is followed by
  * the halo exchange with the neighbouring ranks; without NCCL or peers, n must be <= 1 (<= 2
  * with sweeps_per_pass == 2: one pass) and the caller exchanges halos (pca_halo_ptrs).  Returns PCA_EUNSUPPORTED if the uint16 MPM
- * counters would overflow (> 65535 counted sweeps) or the sweep index would pass 2^32-1. */
+ * counters would overflow (> 65535 counted sweeps) or the sweep index would pass 2^32-1; the
+ * sweeps before the refused one run and are counted (state, sweep index and counts agree). */
 pca_status pca_sweep(pca_ctx* ctx, int32_t n);
 
 /* Write an estimate of the chain (kind PCA_EST_*) to out (host or device; layout in the
