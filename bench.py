@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--graphs", type=int, default=None,
                     help="capture each pca_sweep(S) run into a CUDA graph and replay it every step "
                          "(pca_config.graphs); default: on for N = 1, off for row strips (N > 1)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak (default): config 3 at N = 1, config 4's 4096 x 32768 rows per GPU at N > 1; "
+                         "strong: the 32768^2 lattice split over the N GPUs (N = 1: on one GPU)")
     ap.add_argument("--variant-only", default=None, choices=["c5", "c3_l5"],
                     help="run ONE run of one multi-level variant and exit (no line): the target "
                          "of the all-launch instruction capture (tools/ncu_variant_summary.py)")
@@ -92,17 +95,27 @@ def self_launch(args) -> int | None:
     return subprocess.run(cmd, cwd=ROOT).returncode
 
 
-def workload(n_gpus: int):
+def workload(n_gpus: int, scaling: str = "weak"):
+    if scaling == "strong":  # SURVEY 8(d) C4's secondary mode: the 32768^2 lattice fixed
+        if 32768 % n_gpus:
+            raise SystemExit("--scaling strong splits 32768 rows evenly: N must divide 32768")
+        split = (f"row strips {32768 // n_gpus}x32768 per GPU, NCCL halo exchange per sweep"
+                 if n_gpus > 1 else "the whole lattice on 1 B200")
+        return dict(name=f"config4 strong scaling: 32768x32768 torus, {split}, l=2, Moore-8, sigma=0.5, "
+                         f"beta=1.5, q=0.51, MPM every sweep",
+                    H=32768, W=32768, rows=32768 // n_gpus, levels=2, nbhd=8, periodic=True, sigma=0.5,
+                    beta=1.5, parallelism=f"row-strip x{n_gpus}" if n_gpus > 1 else "1 GPU",
+                    scaling="strong")
     if n_gpus == 1:
         return dict(name="config3: 8192x8192 single lattice on 1 B200, l=2, Moore-8 torus, "
                          "sigma=0.5, beta=1.5 fixed, q=0.51, MPM counts every sweep",
                     H=8192, W=8192, rows=8192, levels=2, nbhd=8, periodic=True, sigma=0.5,
-                    beta=1.5, parallelism="1 GPU")
+                    beta=1.5, parallelism="1 GPU", scaling="weak")
     return dict(name=f"config4 weak scaling: {4096 * n_gpus}x32768 torus (32768 wide), row strips "
                      f"4096x32768 per GPU, NCCL halo exchange per sweep, l=2, Moore-8, sigma=0.5, "
                      f"beta=1.5, q=0.51, MPM every sweep",
                 H=4096 * n_gpus, W=32768, rows=4096, levels=2, nbhd=8, periodic=True, sigma=0.5,
-                beta=1.5, parallelism=f"row-strip x{n_gpus}")
+                beta=1.5, parallelism=f"row-strip x{n_gpus}", scaling="weak")
 
 
 def make_inputs(wl, rank):
@@ -329,7 +342,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    wl = workload(args.gpus)
+    wl = workload(args.gpus, args.scaling)
     truth, g = make_inputs(wl, 0)
     rows = 512
     times = []
@@ -342,7 +355,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * rows * wl["W"] / v,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": wl["name"], "H": wl["H"], "W": wl["W"],
                                         "reference_sample_rows": rows, "sweeps_per_step": 1},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -379,7 +392,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     from paper_2507_14869_b200 import dist as pdist
 
-    wl = workload(n)
+    wl = workload(n, args.scaling)
     truth, g = make_inputs(wl, rank)
     rows, W = wl["rows"], wl["W"]
     assert pdist.strip_rows(wl["H"], max(world, 1), rank)[1] == rows
@@ -589,13 +602,14 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_oracle(wl, truth, g, rows=wl["rows"], sweeps=3)  # ~14 s of CPU work
+        # ~14 s of CPU work: 3 sweeps of at most 2^26 sites (8192^2; 2048 rows at 32768 wide)
+        cpu = cpu_baseline_oracle(wl, truth, g, rows=min(wl["rows"], (1 << 26) // wl["W"]), sweeps=3)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl["name"], "H": wl["H"], "W": W, "rows_per_gpu": rows,
                        "levels": wl["levels"], "sweeps_per_step": S,
                        "step": "reset + S fused sweeps (MPM on) + fused finalisation (MPM image, "
@@ -645,7 +659,7 @@ def run_dry(args):
     n = max(args.gpus, world)
     if world > 1:
         dist.init_process_group("gloo")
-    wl = workload(n)
+    wl = workload(n, args.scaling)
     row0, rows = pdist.strip_rows(wl["H"], world, rank)
     assert rows == wl["rows"], (rows, wl["rows"])
     uid = pdist.broadcast_unique_id() if world > 1 else b""
@@ -682,7 +696,7 @@ def run_dry(args):
     if rank == 0:
         print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": UNIT,
                           "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
-                          "ms_per_step": ms / max(1, args.warmup + args.steps),
+                          "ms_per_step": ms / max(1, args.warmup + args.steps), "scaling": wl["scaling"],
                           "config": {"workload": wl["name"], "H": wl["H"], "W": wl["W"],
                                      "rows_per_gpu": rows, "parallelism": wl["parallelism"]},
                           "ranks": [{"rank": r, "row0": a, "rows": b, "up": u, "down": d,

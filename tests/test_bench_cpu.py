@@ -60,3 +60,18 @@ def test_multi_gpu_self_launch_reaches_the_strip_path_dry_run():
     assert [(e["row0"], e["rows"]) for e in ranks] == [(0, 4096), (4096, 4096)]
     assert [(e["up"], e["down"]) for e in ranks] == [(1, 1), (0, 0)]  # a 2-rank ring (torus)
     assert all(e["unique_id_bytes"] == 128 for e in ranks)
+
+
+def test_strong_scaling_dry_run_splits_the_32768_lattice():
+    """`--scaling strong` (SURVEY 8(d) C4's secondary mode): the 32768^2 torus split over the
+    ranks, 16384 rows each at N = 2, and the line says strong."""
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run", "--scaling", "strong",
+                        "--steps", "1", "--warmup", "1"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=280, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.strip().startswith("{")][0])
+    assert d["scaling"] == "strong" and d["config"]["H"] == 32768 and d["config"]["W"] == 32768
+    assert sorted((e["row0"], e["rows"]) for e in d["ranks"]) == [(0, 16384), (16384, 16384)]
