@@ -58,6 +58,9 @@ namespace {
 // rows + 14 CTAs (round-2 first version) 76.3 / 70.7 / 82.4
 #define PCA_P_PRE 1
 #endif
+#ifndef PCA_P_PDL
+#define PCA_P_PDL 1  // programmatic dependent launch between consecutive sweep launches
+#endif
 #ifndef PCA_P_WAVES
 #define PCA_P_WAVES 4  // waves of resident CTAs the row runs are sized for
 #endif
@@ -91,6 +94,10 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     uint8_t* ring = smem + P_RING_OFF;
     const int lane = threadIdx.x;
+    // programmatic dependent launch: the next sweep's CTAs may be scheduled as soon as every CTA
+    // of this one is resident (they set up, then wait for this grid to complete: griddepcontrol.
+    // wait returns when the prerequisite grid has completed and its memory is visible)
+    if (PCA_P_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (lane == 0) {
         for (int s = 0; s <= PCA_P_K; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
@@ -125,6 +132,9 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
 
     // shared-window addresses of the ring and its barriers, computed once
     const uint32_t ring_s = smem_u32(ring), bars_s = smem_u32(bars);
+    // everything above reads only the parameters; the previous sweep's output (x_in, the count
+    // deltas) and the stage's thresholds only after the previous grid completed
+    if (PCA_P_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
     auto issue = [&](int it, int s) {
         const uint32_t st = ring_s + s * P_STAGE, bar = bars_s + 8 * s;
         const int jx = 2 * it;
@@ -331,6 +341,19 @@ int launch_p(const PackedSweepParams& p, int batch, cudaStream_t s) {
     const int nrb = (int)((nr + R - 1) / R);
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((unsigned)segs, nrb, batch);
+    if (PCA_P_PDL) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(32);
+        cfg.dynamicSmemBytes = P_SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return (int)cudaLaunchKernelEx(&cfg, sweep_packed_kernel<NB, PER, NOCOUNT>, p, (int)R);
+    }
     sweep_packed_kernel<NB, PER, NOCOUNT><<<grid, 32, P_SMEM, s>>>(p, (int)R);
     return (int)cudaGetLastError();
 }

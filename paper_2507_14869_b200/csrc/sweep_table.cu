@@ -63,6 +63,9 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 // t = 900 / 8192^2 l = 5 t = 0 / t = 1000: 1 150/190/428/302, 2 111/139/400/263, 3 107/134/
 // 402/263, 4 101/127/392/259, 5 105/130/393/261, 6 104/129/392/264, 8 104/130/397/266, 12 108/
 // 132/398/269)
+#ifndef PCA_TAB_PDL
+#define PCA_TAB_PDL 1  // programmatic dependent launch between consecutive sweep launches
+#endif
 #ifndef PCA_TAB_WAVES
 #define PCA_TAB_WAVES 4
 #endif
@@ -422,6 +425,13 @@ constexpr int TAB_SMEM_MAX = 16 + TAB_MAX_BYTES + TB_WARPS * QCAP * (int)sizeof(
 // the block's copy of the table blob (one bulk copy) and its warps' queues
 __device__ __forceinline__ TabShared tab_setup(const GeneralSweepParams& p) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(tab_smem_buf);
+    // programmatic dependent launch (as sweep_packed.cu): the next sweep's blocks may be
+    // scheduled once every block of this one is resident; they read the stage's table blob and
+    // the previous sweep's output only after the previous grid completed (griddepcontrol.wait)
+    if (PCA_TAB_PDL) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -490,7 +500,22 @@ int launch_tab(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t
     TDecomp d = tdecomp(nquads, nr, (int)R);
     while (d.nrb > 65535) d = tdecomp(nquads, nr, d.R * 2);
     dim3 grid((unsigned)d.nxb, (unsigned)d.nrb, batch);
-    if (p.c.peer_up != nullptr || p.c.peer_dn != nullptr)
+    const bool peers = p.c.peer_up != nullptr || p.c.peer_dn != nullptr;
+    if (PCA_TAB_PDL) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(TB_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return (int)(peers ? cudaLaunchKernelEx(&cfg, sweep_table_kernel<NB, L, true>, p, d.R)
+                           : cudaLaunchKernelEx(&cfg, sweep_table_kernel<NB, L, false>, p, d.R));
+    }
+    if (peers)
         sweep_table_kernel<NB, L, true><<<grid, TB_THREADS, smem, s>>>(p, d.R);
     else
         sweep_table_kernel<NB, L, false><<<grid, TB_THREADS, smem, s>>>(p, d.R);
