@@ -18,6 +18,7 @@
 #pragma once
 #include <atomic>
 #include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -225,6 +226,30 @@ inline std::mutex& launch_info_mutex() {
     static std::mutex m;
     return m;
 }
+// Programmatic dependent launch (PDL) between consecutive kernels of a stream: the kernel calls
+// pdl_begin() first (let the next grid be scheduled once every block of this one is resident,
+// then wait until the previous grid has completed and its memory is visible -- nothing is read
+// before that), and is launched with launch_pdl (the programmatic-serialization attribute).
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 constexpr int MAX_DEVICES = 64;
 inline int current_device() {
     int d = 0;

@@ -53,6 +53,9 @@ namespace {
 #ifndef PCA_T_RED
 #define PCA_T_RED 0
 #endif
+#ifndef PCA_B_PDL
+#define PCA_B_PDL 1  // programmatic dependent launch between consecutive sweeps (kernels.cuh)
+#endif
 #ifndef PCA_B_WAVES
 #define PCA_B_WAVES 4  // waves of resident warps the row runs are sized for (8192^2 torus MPM on, us per
                        // sweep: 1 wave 84.6, 2 84.2, 4 83.5; MPM off 71.7 / 70.6 / 70.9)
@@ -131,6 +134,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     uint8_t* ring = smem + C::RING_OFF;
     const int lane = threadIdx.x;
+    if (PCA_B_PDL) pdl_begin();
     if (lane == 0) {
         for (int s = 0; s <= KSTAGES; ++s) mbar_init(&bars[s], 1);  // bars[KSTAGES]: the table
         fence_mbar_init();
@@ -524,6 +528,7 @@ int launch_t(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
     if (nrb <= 0) return 0;
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((G.nchunks + SEG_CHUNKS - 1) / SEG_CHUNKS, nrb, batch);
+    if (PCA_B_PDL) return (int)launch_pdl(sweep_binary_kernel<NB, PER, F>, grid, dim3(32), RingCfg<PER>::SMEM, s, p, R);
     sweep_binary_kernel<NB, PER, F><<<grid, 32, RingCfg<PER>::SMEM, s>>>(p, R);
     return (int)cudaGetLastError();
 }

@@ -21,6 +21,9 @@
 #include "kernels.cuh"
 #include "tma_ring.cuh"
 
+#ifndef PCA_GB_PDL
+#define PCA_GB_PDL 1  // programmatic dependent launch between consecutive launches (kernels.cuh)
+#endif
 #ifndef PCA_GB_WAVES
 #define PCA_GB_WAVES 4  // waves of resident warps the row runs are sized for (8192^2 torus Gibbs
                         // sweep: 1 wave 135.2 us, 2 135.0, 4 126.9)
@@ -64,6 +67,7 @@ __global__ void __launch_bounds__(32, GCTAS)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     uint8_t* ring = smem + GRING_OFF;
     const int lane = threadIdx.x;
+    if (PCA_GB_PDL) pdl_begin();
     if (lane == 0) {
         for (int s = 0; s <= GK; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
@@ -290,6 +294,7 @@ int launch_gb2(const GibbsBinParams& p, int batch, cudaStream_t s) {
     const long long nrb = (nproc + R - 1) / R;
     if (nrb > 65535) return (int)cudaErrorInvalidConfiguration;
     dim3 grid((unsigned)segs, (unsigned)nrb, batch);
+    if (PCA_GB_PDL) return (int)launch_pdl(gibbs_binary_kernel<PER>, grid, dim3(32), GSMEM, s, p, (int)R);
     gibbs_binary_kernel<PER><<<grid, 32, GSMEM, s>>>(p, (int)R);
     return (int)cudaGetLastError();
 }
