@@ -465,6 +465,7 @@ template <int NB, int LT, bool PEERS>  // LT: levels known at compile time, 0 = 
 __global__ void __launch_bounds__(GEN_THREADS, PCA_GEN_MINB)
     sweep_general_kernel(const __grid_constant__ GeneralSweepParams p, int R) {
     __shared__ GenSmem<LT> sm;
+    pdl_begin();  // programmatic dependent launch (kernels.cuh): nothing is read before it
     gen_load_tables<LT>(p, sm);
     __syncthreads();
     const Decomp d = make_decomp(((p.c.geo.W + 3) >> 2), p.c.rhi - p.c.rlo, R);
@@ -575,10 +576,8 @@ int launch_g(const GeneralSweepParams& p, int batch, int nsweeps, cudaStream_t s
     while (d.nrb > 65535) d = make_decomp(nquads, nr, d.R * 2);
     dim3 grid((unsigned)d.nxb, (unsigned)d.nrb, batch);
     if (p.c.peer_up != nullptr || p.c.peer_dn != nullptr)
-        sweep_general_kernel<NB, LT, true><<<grid, GEN_THREADS, 0, s>>>(p, d.R);
-    else
-        sweep_general_kernel<NB, LT, false><<<grid, GEN_THREADS, 0, s>>>(p, d.R);
-    return (int)cudaGetLastError();
+        return (int)launch_pdl(sweep_general_kernel<NB, LT, true>, grid, dim3(GEN_THREADS), 0, s, p, d.R);
+    return (int)launch_pdl(sweep_general_kernel<NB, LT, false>, grid, dim3(GEN_THREADS), 0, s, p, d.R);
 }
 
 }  // namespace

@@ -465,6 +465,7 @@ template <int NB, int LT, bool FUSED>
 __global__ void __launch_bounds__(GB_THREADS, PCA_GB_MINB)
     sweep_gibbs_kernel(const __grid_constant__ GibbsSweepParams p, int R) {
     __shared__ GibbsSmem sm;
+    pdl_begin();  // programmatic dependent launch (kernels.cuh): nothing is read before it
     gibbs_load_tables<LT>(p, sm);
     __syncthreads();
     gibbs_rows<NB, LT, FUSED, false>(p, sm, p.colour, p.c.t, p.c.count_enable, blockIdx.x,
@@ -542,8 +543,7 @@ int launch_gb(const GibbsSweepParams& p, int batch, int nsweeps, cudaStream_t s)
                                                 dim3(GB_THREADS), args, 0, s);
     }
     dim3 grid((unsigned)xblocks, (unsigned)nrb, batch);
-    sweep_gibbs_kernel<NB, LT, FUSED><<<grid, GB_THREADS, 0, s>>>(p, (int)R);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(sweep_gibbs_kernel<NB, LT, FUSED>, grid, dim3(GB_THREADS), 0, s, p, (int)R);
 }
 
 }  // namespace
