@@ -34,6 +34,10 @@ def workload(name):
         g = synth.degrade(synth.tiled_labels(8192, 8192, 5, 1), 5, 0.25, 2)[None]
         return P.make_config(8192, 8192, 5, periodic=True, sigma=0.25, beta0=1.5, beta_step=0,
                              mpm_burn_in=0, kernel=KERNEL), g
+    if name == "c2_33":  # config 2's 33-level image (256^2, Moore free, sigma 0.1); small: the
+        # runtime runs each beta stage's sweeps in one cooperative launch (sweep_multi_kernel)
+        g = synth.degrade(synth.smooth_labels(256, 256, 33, 3), 33, 0.1, 4)[None]
+        return P.make_config(256, 256, 33, sigma=0.1, mpm_burn_in=750, kernel=KERNEL), g
     raise SystemExit(f"unknown workload {name}")
 
 
