@@ -183,10 +183,12 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
     // (the pad / halo copies are one rarely taken branch: lanes at the torus seam or rows next
     // to the wrapped halos)
     const bool seam = PER && (k == 0 || k == nchunks - 1);
+    // only runs that touch the first or last HALO rows of a self-wrapped torus write halo rows
+    const bool near_halo = PER && G.self_halo_rows && (rbeg < HALO || rend > G.rows - HALO);
     auto store_row = [&](int r, uint32_t bits16) {
         uint8_t* dst = xo + (long long)(r - rbeg) * p.pp;
         *reinterpret_cast<uint16_t*>(dst) = (uint16_t)bits16;
-        const bool hrow = PER && G.self_halo_rows && (r < HALO || r >= G.rows - HALO);
+        const bool hrow = near_halo && (r < HALO || r >= G.rows - HALO);
         if (seam || hrow) {
             auto put = [&](uint8_t* d) {
                 *reinterpret_cast<uint16_t*>(d) = (uint16_t)bits16;
