@@ -233,9 +233,14 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
                 S[2] = U.w[2] + D.w[2] + from_left(M.w[1], M.w[2]) + from_right(M.w[2], M.w[3]);
                 S[3] = U.w[3] + D.w[3] + from_left(M.w[2], M.w[3]) + from_right(M.w[3], M.r);
             }
+            // byte b: n1 << 4 | g << 3 | x << 2 (the fields do not overlap, so as multiply-adds on
+            // the FMA pipe: the ALU pipe is the busier one); g's 4 bits spread to bit 3 of each
+            // byte by one multiply (gn < 16: the shifted copies neither overlap nor carry)
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                IDX4[qq][i] = (S[i] << 4) | (spread4((g16 >> (4 * i)) & 0xFu) << 3) | (M.w[i] << 2);
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t gsp = (((g16 >> (4 * i)) & 0xFu) * 0x01020408u) & 0x08080808u;
+                IDX4[qq][i] = S[i] * 16u + M.w[i] * 4u + gsp;
+            }
             edge[qq] = !PER && (k == 0 || k == nchunks - 1 || grow == 0 || grow == G.H - 1);
             if (q >= nrow) {  // past the run: its stage slot holds stale bytes; decide on index 0
 #pragma unroll
