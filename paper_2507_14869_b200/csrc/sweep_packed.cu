@@ -58,6 +58,9 @@ namespace {
 // rows + 14 CTAs (round-2 first version) 76.3 / 70.7 / 82.4
 #define PCA_P_PRE 1
 #endif
+#ifndef PCA_P_LUT
+#define PCA_P_LUT 1  // a row's 16 bits to label bytes by two 256-entry shared-memory lookups
+#endif
 #ifndef PCA_P_PDL
 #define PCA_P_PDL 1  // programmatic dependent launch between consecutive sweep launches
 #endif
@@ -90,6 +93,8 @@ template <int NB, bool PER, bool NOCOUNT>
 __global__ void __launch_bounds__(32, PCA_P_CTAS)
     sweep_packed_kernel(const __grid_constant__ PackedSweepParams p, int R) {
     __shared__ __align__(16) uint32_t s_thr[THR_ENTRIES];
+    // byte -> its 8 bits as 8 label bytes (two words), filled once per CTA (PCA_P_LUT)
+    __shared__ __align__(16) uint2 s_spread[PCA_P_LUT ? 256 : 1];
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     uint8_t* ring = smem + P_RING_OFF;
@@ -102,6 +107,8 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
         for (int s = 0; s <= PCA_P_K; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
+    if (PCA_P_LUT)
+        for (int v = lane; v < 256; v += 32) s_spread[v] = make_uint2(spread4(v & 0xFu), spread4(v >> 4));
     __syncwarp();
     const Geometry& G = p.c.geo;
     const int seg = blockIdx.x;
@@ -176,8 +183,16 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
         const uint32_t h16 = *reinterpret_cast<const uint16_t*>(xr + j0);
         x.l = ((uint32_t)xr[j0 - 1] & 0x80u) << 17;  // bit 7 -> byte 3 bit 0
         x.r = (uint32_t)xr[j0 + 2] & 1u;
+        if (PCA_P_LUT) {
+            const uint2 lo = s_spread[h16 & 0xFFu], hi = s_spread[h16 >> 8];
+            x.w[0] = lo.x;
+            x.w[1] = lo.y;
+            x.w[2] = hi.x;
+            x.w[3] = hi.y;
+        } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) x.w[i] = spread4((h16 >> (4 * i)) & 0xFu);
+            for (int i = 0; i < 4; ++i) x.w[i] = spread4((h16 >> (4 * i)) & 0xFu);
+        }
     };
     // store the 16 new bits of local row r (+ torus pad copies, + wrapped halo rows)
     // (the pad / halo copies are one rarely taken branch: lanes at the torus seam or rows next
