@@ -61,6 +61,12 @@ namespace {
 #ifndef PCA_P_LUT
 #define PCA_P_LUT 1  // a row's 16 bits to label bytes by two 256-entry shared-memory lookups
 #endif
+#ifndef PCA_P_LUT_G
+#define PCA_P_LUT_G 1  // g's bits by the same table
+#endif
+#ifndef PCA_P_LUT_O
+#define PCA_P_LUT_O 0  // the new labels' count increments by the same table (measured slower)
+#endif
 #ifndef PCA_P_PDL
 #define PCA_P_PDL 1  // programmatic dependent launch between consecutive sweep launches
 #endif
@@ -251,10 +257,17 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
             // byte b: n1 << 4 | g << 3 | x << 2 (the fields do not overlap, so as multiply-adds on
             // the FMA pipe: the ALU pipe is the busier one); g's 4 bits spread to bit 3 of each
             // byte by one multiply (gn < 16: the shifted copies neither overlap nor carry)
+            if (PCA_P_LUT_G) {  // g's label bytes from the shared table, x 8 in the multiply-add
+                const uint2 glo = s_spread[g16 & 0xFFu], ghi = s_spread[g16 >> 8];
+                const uint32_t gw[4] = {glo.x, glo.y, ghi.x, ghi.y};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t gsp = (((g16 >> (4 * i)) & 0xFu) * 0x01020408u) & 0x08080808u;
-                IDX4[qq][i] = S[i] * 16u + M.w[i] * 4u + gsp;
+                for (int i = 0; i < 4; ++i) IDX4[qq][i] = S[i] * 16u + (gw[i] * 8u + M.w[i] * 4u);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t gsp = (((g16 >> (4 * i)) & 0xFu) * 0x01020408u) & 0x08080808u;
+                    IDX4[qq][i] = S[i] * 16u + M.w[i] * 4u + gsp;
+                }
             }
             edge[qq] = !PER && (k == 0 || k == nchunks - 1 || grow == 0 || grow == G.H - 1);
             if (q >= nrow) {  // past the run: its stage slot holds stale bytes; decide on index 0
@@ -292,8 +305,18 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
                 }
                 const uint32_t nib = ~bits & 0xFu;  // bit b: site 4i + b is 1
                 B[qq] |= nib << (4 * i);
-                O[qq][i] = spread4(nib);
+                if (!PCA_P_LUT_O) O[qq][i] = spread4(nib);
             }
+        if (PCA_P_LUT_O && cnt) {  // the new labels as count increments: the 16 bits by the table
+#pragma unroll
+            for (int qq = 0; qq < QN; ++qq) {
+                const uint2 lo = s_spread[B[qq] & 0xFFu], hi = s_spread[B[qq] >> 8];
+                O[qq][0] = lo.x;
+                O[qq][1] = lo.y;
+                O[qq][2] = hi.x;
+                O[qq][3] = hi.y;
+            }
+        }
 #pragma unroll
         for (int qq = 0; qq < QN; ++qq) {
             const int q = q0 + qq;
