@@ -549,7 +549,7 @@ int launch_f(const BinarySweepParams& p, int batch, int R, cudaStream_t s) {
 
 int launch_sweep_binary(const BinarySweepParams& p, int batch, int rows_per_thread, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    const int R = rows_per_thread;  // 0 = auto (one wave)
+    const int R = rows_per_thread;  // 0 = auto (PCA_B_WAVES waves)
     if (p.c.geo.nbhd == 8)
         return p.c.geo.periodic ? launch_f<8, true>(p, batch, R, s) : launch_f<8, false>(p, batch, R, s);
     return p.c.geo.periodic ? launch_f<4, true>(p, batch, R, s) : launch_f<4, false>(p, batch, R, s);
