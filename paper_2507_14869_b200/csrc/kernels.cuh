@@ -136,7 +136,8 @@ struct GeneralSweepParams {
     // tab = one 16-byte-aligned blob, refreshed per beta stage, copied whole into each block's
     // shared memory by one bulk copy:
     //   [0, TAB_OFF_W0)           A[0..8] (fp64)
-    //   [TAB_OFF_W0, tab_slots)   W0[g][x][s] = D[g][s] I[x][s] (fp64, the fp64 rare path)
+    //   [TAB_OFF_W0, tab_slots)   AW[g][x][s][n] = A[n] D[g][s] I[x][s], n = 0..8 (fp64, the
+    //                             rare path's weights w_s = AW[g][x][s][n_s])
     //   [tab_slots, tab_thr)      uint2 slot[1 << tab_hbits] = {histogram tag, byte offset of
     //                             the key's threshold rows in the thr block}; tag 0xFFFFFFFF =
     //                             empty

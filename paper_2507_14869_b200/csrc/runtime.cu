@@ -155,7 +155,8 @@ int tab_tp_host(int L) { return L == 3 ? 2 : 4; }
 
 size_t tab_nkeys(int L, int NB) { return (size_t)L + (size_t)L * (L - 1) / 2 * (NB - 1); }
 
-size_t tab_slots_off(int L) { return (TAB_OFF_W0 + 8 * (size_t)L * L * L + 15) & ~size_t(15); }
+// AW[g][x][s][n] = A[n] W0[g][x][s] (n = 0..8) follows A (kernels.cuh)
+size_t tab_slots_off(int L) { return (TAB_OFF_W0 + 8 * 9 * (size_t)L * L * L + 15) & ~size_t(15); }
 
 size_t tab_blob_bytes(int L, int NB, int hbits) {
     const size_t thr = tab_nkeys(L, NB) * L * L * tab_tp_host(L) * 4;
@@ -723,12 +724,15 @@ pca_status build_tables(pca_ctx* ctx, int64_t t) {
         uint8_t* blob = ctx->tab_host.data();
         std::fill(ctx->tab_host.begin(), ctx->tab_host.end(), 0);
         memcpy(blob, m.A, 9 * sizeof(double));
-        double* w0 = reinterpret_cast<double*>(blob + TAB_OFF_W0);
+        // AW[g][x][s][n] = A[n] * W0[g][x][s], W0 = D I: the fp64 products the rare path forms
+        // (IEEE multiplication: the device reading them decides exactly as if it multiplied)
+        double* aw = reinterpret_cast<double*>(blob + TAB_OFF_W0);
         for (int gl = 0; gl < L; ++gl)
             for (int xl = 0; xl < L; ++xl)
-                for (int s = 0; s < L; ++s)
-                    w0[(gl * L + xl) * L + s] =
-                        ctx->dtab_host[(size_t)gl * L + s] * exp(-cq * inertia_pen(c.inertia_p, xl, s, L));
+                for (int s = 0; s < L; ++s) {
+                    const double w0 = ctx->dtab_host[(size_t)gl * L + s] * exp(-cq * inertia_pen(c.inertia_p, xl, s, L));
+                    for (int n = 0; n < 9; ++n) aw[(((gl * L + xl) * L) + s) * 9 + n] = m.A[n] * w0;
+                }
         uint32_t* slot = reinterpret_cast<uint32_t*>(blob + m.tab_slots);
         for (int i = 0; i < (1 << K.hbits); ++i) {
             slot[2 * i] = 0xFFFFFFFFu;

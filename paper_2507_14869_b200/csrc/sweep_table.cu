@@ -69,7 +69,7 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 #ifndef PCA_TAB_WAVES
 #define PCA_TAB_WAVES 4
 #endif
-constexpr int TAB_MAX_BYTES = 40 * 1024;  // blob limit (3..5 levels: <= 40 KB)
+constexpr int TAB_MAX_BYTES = 48 * 1024;  // blob limit (3..5 levels: <= 42 KB)
 
 __host__ __device__ constexpr int tab_tp(int L) { return L == 3 ? 2 : 4; }
 
@@ -110,7 +110,7 @@ struct TabShared {
 __device__ __forceinline__ const double* sm_A() {
     return reinterpret_cast<const double*>(tab_smem_buf + BLOB);
 }
-__device__ __forceinline__ const double* sm_W0() {
+__device__ __forceinline__ const double* sm_AW() {
     return reinterpret_cast<const double*>(tab_smem_buf + BLOB + TAB_OFF_W0);
 }
 
@@ -121,13 +121,13 @@ __device__ __forceinline__ const double* sm_W0() {
 // general kernel's log-domain fallback is never needed here.
 template <int L>
 __device__ __forceinline__ int decide_hist_fp64(uint32_t h, int gi, int xi, uint32_t r) {
-    const double* A = sm_A();
-    const double* Wrow = sm_W0() + (gi * L + xi) * L;
+    // w_s = A[n_s] W0[g][x][s], read as the stage's precomputed products AW[g][x][s][n_s]
+    const double* AWrow = sm_AW() + (gi * L + xi) * L * 9;
     double w[L];
     double Z = 0.0;
 #pragma unroll
     for (int s = 0; s < L; ++s) {
-        w[s] = A[(h >> (4 * s)) & 0xFu] * Wrow[s];
+        w[s] = AWrow[s * 9 + ((h >> (4 * s)) & 0xFu)];
         Z += w[s];
     }
     const double target = (double)r * (1.0 / 4294967296.0) * Z;
