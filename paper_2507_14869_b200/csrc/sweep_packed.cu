@@ -67,6 +67,12 @@ namespace {
 #ifndef PCA_P_LUT_O
 #define PCA_P_LUT_O 0  // the new labels' count increments by the same table (measured slower)
 #endif
+// Philox products as one wide multiply (philox.cuh) on a torus; the split form on a free
+// boundary (us per direct 8192^2 sweep, wide / split: torus 65.4 / 66.4, strip shape 124.6 /
+// 126.8, free boundary 75.8 / 75.0)
+#ifndef PCA_P_WIDE
+#define PCA_P_WIDE PER
+#endif
 #ifndef PCA_P_PDL
 #define PCA_P_PDL 1  // programmatic dependent launch between consecutive sweep launches
 #endif
@@ -284,7 +290,7 @@ __global__ void __launch_bounds__(32, PCA_P_CTAS)
             for (int qq = 0; qq < QN; ++qq) {
                 const int q = q0 + qq;
                 const int grow = G.row0 + r0 + q;
-                const uint4 rnd = PCA_P_PRE ? philox_row(ppre[i], (uint32_t)grow, p.c.keys)
+                const uint4 rnd = PCA_P_PRE ? philox_row<PCA_P_WIDE>(ppre[i], (uint32_t)grow, p.c.keys)
                                             : philox4x32_10(make_uint4((uint32_t)(4 * k + i), (uint32_t)grow,
                                                                        p.c.t, tagchain), p.c.keys);
                 const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
