@@ -58,8 +58,8 @@ __device__ __forceinline__ PhiloxPre philox_pre(uint32_t x, uint32_t z, uint32_t
 
 // lo/hi halves of m * x: WIDE = one 64-bit product (ptxas emits IMAD.WIDE.U32), else __umulhi and
 // a 32-bit product (which ptxas may emit as IMAD.HI + IMAD, or fuse).  Which is faster depends on
-// the kernel around it (measured: the table kernel gains ~1% with WIDE, the packed kernel loses
-// 0.5 us per 8192^2 sweep), so the callers choose.
+// the kernel around it, so the callers choose (measured: the table kernel and the packed and byte
+// kernels on a torus gain 0.7-1.5% with WIDE; the packed kernel on a free boundary loses 1%).
 template <bool WIDE>
 __device__ __forceinline__ void philox_mulhilo(uint32_t m, uint32_t x, uint32_t& lo, uint32_t& hi) {
     if (WIDE) {

@@ -53,6 +53,11 @@ namespace {
 #ifndef PCA_T_RED
 #define PCA_T_RED 0
 #endif
+// Philox products as one wide multiply (philox.cuh) on a torus (8192^2 torus with MPM: 81.9 ->
+// 81.35 us per sweep), the split form on a free boundary (as sweep_packed.cu)
+#ifndef PCA_B_WIDE
+#define PCA_B_WIDE PER
+#endif
 #ifndef PCA_B_PDL
 #define PCA_B_PDL 1  // programmatic dependent launch between consecutive sweeps (kernels.cuh)
 #endif
@@ -271,7 +276,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
         uint32_t O[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const uint4 rnd = PCA_B_PRE ? philox_row(ppre[i], (uint32_t)grow, p.c.keys)
+            const uint4 rnd = PCA_B_PRE ? philox_row<PCA_B_WIDE>(ppre[i], (uint32_t)grow, p.c.keys)
                                         : philox4x32_10(make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t,
                                                                    tagchain), p.c.keys);
             const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
@@ -371,7 +376,7 @@ __global__ void __launch_bounds__(32, RingCfg<PER>::CTAS)
         uint32_t O[2][4];
         auto decide = [&](int q, int i) {
             const int grow = G.row0 + r0 + q;
-            const uint4 rnd = PCA_B_PRE ? philox_row(ppre[i], (uint32_t)grow, p.c.keys)
+            const uint4 rnd = PCA_B_PRE ? philox_row<PCA_B_WIDE>(ppre[i], (uint32_t)grow, p.c.keys)
                                         : philox4x32_10(make_uint4((uint32_t)(4 * k + i), (uint32_t)grow, p.c.t,
                                                                    tagchain), p.c.keys);
             const uint32_t rw[4] = {rnd.x, rnd.y, rnd.z, rnd.w};
