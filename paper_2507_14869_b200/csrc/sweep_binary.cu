@@ -1,4 +1,6 @@
-// sweep_binary.cu -- one synchronous lazy-PCA sweep for levels == 2 (the headline kernel).
+// sweep_binary.cu -- one synchronous lazy-PCA sweep for levels == 2 on the byte state (round 1's
+// headline kernel; since round 2 the bit-packed kernel, sweep_packed.cu, runs whole lattices and
+// strips with W % 512 == 0, and this one the other two-level cases and strips with peers).
 //
 // Per site i (R1): new label w_i = 0 iff u_i < p_i(0; x), with
 //   p_i(0) = e^{E(0)} / (e^{E(0)} + e^{E(1)}),
