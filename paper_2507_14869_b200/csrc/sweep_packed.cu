@@ -3,25 +3,30 @@
 //
 // The state x_t, x_{t+1} and the observation g live in HBM at ONE BIT per site (32 sites per
 // 32-bit word, column c at bit c % 8 of byte c / 8 of its row, LSB first), so a sweep moves
-// 3 bits of state per site-update instead of 3 bytes (plus the unchanged uint16 MPM count
-// read-modify-write when counting): 4.375 B/SU with MPM counts, 0.375 B/SU without.
+// 3 bits of state per site-update instead of 3 bytes (plus the uint8 MPM count-delta read-
+// modify-write when counting, below): 2.375 B/SU with MPM counts, 0.375 B/SU without.
 //
 // The chain is the byte kernel's (sweep_binary.cu) bit for bit: the same Philox words
 // (counter (col >> 2, row, t, tag << 24 | chain)), the same host-tabulated integer thresholds
 // T[(np, n1, g, x)] = ceil(p0 2^32) - 1 of PAPER.md:462-477, the same decision w = (r > T).
 // Per lane and row the 16 packed bits (+ the columns left and right) are expanded to SWAR
-// bytes (one multiply per 4 sites) and the byte kernel's neighbour sums and table lookups run
+// bytes (two lookups in a 256-entry shared table) and the byte kernel's neighbour sums and table lookups run
 // unchanged; the decisions are packed back to 16 bits.  A spin-level bit-sliced evaluation was
 // not used: the exact per-site law needs the 32-bit uniform and a table row per site, so
 // bit-slicing the neighbour counts saves little and the bits -> table-index transposition costs
 // more than it saves.
 //
-// Layout (one context, whole lattice, W % 512 == 0): xp[2]: uint8 [batch][rows + 2 HALO][pp],
+// Layout (one context, a whole lattice or a row strip, W % 512 == 0): xp[2]: uint8
+// [batch][rows + 2 HALO][pp],
 // pp = W/8 + 32: packed row j at (j + HALO) pp, column c at bit c%8 of byte 16 + c/8; bytes
 // [0, 16) / [16 + W/8, pp) are the column pads (on a torus the lane owning columns W-16..W-1
 // also writes them to bytes 14..15 and the lane owning 0..15 to bytes W/8+16..+17, the only pad
 // bits any lane reads; zero on a free boundary).  Halo rows: wrapped rows rewritten by every
-// sweep on a torus, zero on a free boundary.  gp: uint8 [batch][rows][W/8].
+// sweep on a torus, zero on a free boundary, the neighbours' packed rows on a strip (the
+// runtime's NCCL exchange, or the caller's).  gp: uint8 [batch][rows][W/8].
+//
+// Launch shape: row runs sized for 4 waves of resident CTAs, programmatic dependent launch
+// between consecutive sweeps.
 //
 // Data movement: one warp per CTA owns a 512-column segment of a run of rows; rows stream
 // through a 4-stage shared-memory ring of TMA bulk copies (96 B of packed x and 64 B of packed
